@@ -1,0 +1,314 @@
+// ORACLE — test infrastructure only (see oracle.hpp).
+//
+// C6/C7/C8 and the weight generator (K11's CPU twin).  The paper fixes none of
+// the decoder's numerics (it only says decode is memory-bandwidth bound,
+// P:361-363, and generation produces a trajectory per prompt); the
+// model is the Qwen2.5 family of Table 2.  Readings
+// (R12-R17):
+//   * fp64 arithmetic everywhere, with bf16 rounding exactly where the CUDA
+//     path materialises a bf16 tensor: norm outputs, q/k/v after bias+RoPE,
+//     attention output, SwiGLU product; weights are bf16 values;
+//   * RMSNorm y = bf16(x / sqrt(mean(x^2) + eps) * w)  (weight applied before
+//     the single rounding);
+//   * NeoX rotate-half RoPE, theta = 1e6, angles in fp64;
+//   * logits in full precision (compared in fp32).
+// End-to-end logits are "parity unpinned" beyond their components: the pins
+// are attention (naive softmax, ctx=1, equal keys), RMSNorm closed form, RoPE
+// norm preservation and relative-position property, GEMM vs fp64 dot.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "oracle.hpp"
+
+namespace oracle {
+
+float bf16_round(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) {  // inf / nan: truncate, keep nan quiet
+    if (u & 0x007fffffu) u |= 0x00400000u;
+    u &= 0xffff0000u;
+  } else {
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;  // round to nearest even
+  }
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+static uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+uint64_t weight_hash(uint64_t seed, uint64_t tensor_id, uint64_t i) {
+  uint64_t key = splitmix64(seed ^ (tensor_id * 0xD1B54A32D192ED03ull));
+  return splitmix64(key + i);
+}
+
+// u in [-1, 1) with 24 bits (exact in fp32); matrix/bias: bf16(u * 0.02*sqrt(3))
+// (std 0.02); norm weights: bf16(1 + u/8).
+float weight_value(uint64_t seed, uint64_t tensor_id, uint64_t i, int is_norm) {
+  uint64_t h = weight_hash(seed, tensor_id, i);
+  int32_t m = (int32_t)(h >> 40) - (1 << 23);
+  float u = (float)m * (1.0f / 8388608.0f);
+  if (is_norm) {
+    volatile float v = u * 0.125f;  // exact (power of two)
+    volatile float w = 1.0f + v;
+    return bf16_round(w);
+  }
+  volatile float p = u * 0.034641016f;  // one IEEE fp32 multiply, then RNE to bf16
+  return bf16_round(p);
+}
+
+void gen_tensor(uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, float* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = weight_value(seed, tensor_id, (uint64_t)i, is_norm);
+}
+
+uint64_t tensor_checksum(uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm) {
+  // sum over i of (bf16 bits of w_i) * (2i+1) mod 2^64 — order-independent
+  uint64_t total = 0;
+#pragma omp parallel for reduction(+ : total) schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    float w = weight_value(seed, tensor_id, (uint64_t)i, is_norm);
+    uint32_t u;
+    std::memcpy(&u, &w, 4);
+    total += (uint64_t)(u >> 16) * (2 * (uint64_t)i + 1);
+  }
+  return total;
+}
+
+// C7: o_h = softmax(q_h K^T / sqrt(hd)) V for each query head h, GQA group
+// g = nq/nkv (head h reads kv head h/g), in fp64.  P:361-363 names this the
+// memory-bound core of decoding.
+void attention_fp64(int nq, int nkv, int hd, int ctx, const float* q, const float* K, const float* V,
+                    double* out) {
+  const int g = nq / nkv;
+  const double scale = 1.0 / std::sqrt((double)hd);
+  std::vector<double> s(ctx);
+  for (int h = 0; h < nq; ++h) {
+    const int kh = h / g;
+    double mx = -INFINITY;
+    for (int j = 0; j < ctx; ++j) {
+      double acc = 0;
+      for (int e = 0; e < hd; ++e) acc += (double)q[h * hd + e] * (double)K[((int64_t)j * nkv + kh) * hd + e];
+      s[j] = acc * scale;
+      if (s[j] > mx) mx = s[j];
+    }
+    double den = 0;
+    for (int j = 0; j < ctx; ++j) {
+      s[j] = std::exp(s[j] - mx);
+      den += s[j];
+    }
+    for (int e = 0; e < hd; ++e) {
+      double acc = 0;
+      for (int j = 0; j < ctx; ++j) acc += s[j] * (double)V[((int64_t)j * nkv + kh) * hd + e];
+      out[h * hd + e] = acc / den;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// decoder_forward: teacher-forced causal forward of tokens[0..T), logits for
+// rows first_row..T-1.  Tensor ids: 0 embed [V,d], 1 lm_head
+// [V,d], 2 final norm [d]; layer l at 16+16l: +0 Wq, +1 Wk, +2 Wv, +3 bq,
+// +4 bk, +5 bv, +6 Wo, +7 Wgate, +8 Wup, +9 Wdown, +10 attn norm, +11 mlp norm.
+// ---------------------------------------------------------------------------
+static std::vector<float> tensor(uint64_t seed, uint64_t id, int64_t n, int is_norm) {
+  std::vector<float> w(n);
+  gen_tensor(seed, id, n, is_norm, w.data());
+  return w;
+}
+
+// y[t][r] = sum_k x[t][k] * W[r][k]   (W row-major [rows x cols]), fp64
+static void matmul(const std::vector<double>& x, int T, int cols, const std::vector<float>& W, int rows,
+                   std::vector<double>& y) {
+  y.assign((size_t)T * rows, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < rows; ++r) {
+    const float* w = &W[(size_t)r * cols];
+    for (int t = 0; t < T; ++t) {
+      const double* xt = &x[(size_t)t * cols];
+      double acc = 0;
+      for (int k = 0; k < cols; ++k) acc += xt[k] * (double)w[k];
+      y[(size_t)t * rows + r] = acc;
+    }
+  }
+}
+
+static void rmsnorm_bf16(const std::vector<double>& h, int T, int d, const std::vector<float>& w, double eps,
+                         std::vector<double>& x) {
+  x.resize((size_t)T * d);
+  for (int t = 0; t < T; ++t) {
+    double ss = 0;
+    for (int i = 0; i < d; ++i) ss += h[(size_t)t * d + i] * h[(size_t)t * d + i];
+    double r = 1.0 / std::sqrt(ss / d + eps);
+    for (int i = 0; i < d; ++i) x[(size_t)t * d + i] = bf16_round((float)(h[(size_t)t * d + i] * r * w[i]));
+  }
+}
+
+// NeoX rotate-half RoPE on one head vector at position pos.
+static void rope(double* v, int hd, int pos, double theta) {
+  const int half = hd / 2;
+  for (int i = 0; i < half; ++i) {
+    double inv = std::pow(theta, -2.0 * i / hd);
+    double a = pos * inv, c = std::cos(a), s = std::sin(a);
+    double x1 = v[i], x2 = v[i + half];
+    v[i] = x1 * c - x2 * s;
+    v[i + half] = x2 * c + x1 * s;
+  }
+}
+
+void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, int T, int first_row,
+                     double* logits) {
+  const int d = c.d, hd = c.hd, nq = c.nq, nkv = c.nkv;
+  std::vector<double> h((size_t)T * d);
+  {
+    // embedding rows (weights are bf16 values)
+    for (int t = 0; t < T; ++t)
+      for (int i = 0; i < d; ++i)
+        h[(size_t)t * d + i] = weight_value(seed, 0, (uint64_t)tokens[t] * d + i, 0);
+  }
+  std::vector<double> x, q, k, v, y, g, u;
+  for (int l = 0; l < c.n_layers; ++l) {
+    const uint64_t b = 16 + 16 * (uint64_t)l;
+    auto wn1 = tensor(seed, b + 10, d, 1);
+    rmsnorm_bf16(h, T, d, wn1, c.eps, x);
+    {
+      auto Wq = tensor(seed, b + 0, (int64_t)nq * hd * d, 0);
+      auto Wk = tensor(seed, b + 1, (int64_t)nkv * hd * d, 0);
+      auto Wv = tensor(seed, b + 2, (int64_t)nkv * hd * d, 0);
+      auto bq = tensor(seed, b + 3, nq * hd, 0), bk = tensor(seed, b + 4, nkv * hd, 0),
+           bv = tensor(seed, b + 5, nkv * hd, 0);
+      matmul(x, T, d, Wq, nq * hd, q);
+      matmul(x, T, d, Wk, nkv * hd, k);
+      matmul(x, T, d, Wv, nkv * hd, v);
+      for (int t = 0; t < T; ++t) {
+        for (int j = 0; j < nq * hd; ++j) q[(size_t)t * nq * hd + j] += bq[j];
+        for (int j = 0; j < nkv * hd; ++j) k[(size_t)t * nkv * hd + j] += bk[j], v[(size_t)t * nkv * hd + j] += bv[j];
+        for (int hh = 0; hh < nq; ++hh) rope(&q[((size_t)t * nq + hh) * hd], hd, t, c.theta);
+        for (int hh = 0; hh < nkv; ++hh) rope(&k[((size_t)t * nkv + hh) * hd], hd, t, c.theta);
+      }
+      for (auto& e : q) e = bf16_round((float)e);
+      for (auto& e : k) e = bf16_round((float)e);
+      for (auto& e : v) e = bf16_round((float)e);
+    }
+    // causal attention, position t attends to 0..t
+    std::vector<double> o((size_t)T * nq * hd);
+    {
+      std::vector<float> qf(nq * hd), Kf((size_t)T * nkv * hd), Vf((size_t)T * nkv * hd);
+      for (size_t i = 0; i < Kf.size(); ++i) Kf[i] = (float)k[i], Vf[i] = (float)v[i];
+      std::vector<double> ot(nq * hd);
+      for (int t = 0; t < T; ++t) {
+        for (int i = 0; i < nq * hd; ++i) qf[i] = (float)q[(size_t)t * nq * hd + i];
+        attention_fp64(nq, nkv, hd, t + 1, qf.data(), Kf.data(), Vf.data(), ot.data());
+        for (int i = 0; i < nq * hd; ++i) o[(size_t)t * nq * hd + i] = bf16_round((float)ot[i]);
+      }
+    }
+    {
+      auto Wo = tensor(seed, b + 6, (int64_t)d * nq * hd, 0);
+      matmul(o, T, nq * hd, Wo, d, y);
+      for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
+    }
+    auto wn2 = tensor(seed, b + 11, d, 1);
+    rmsnorm_bf16(h, T, d, wn2, c.eps, x);
+    {
+      auto Wg = tensor(seed, b + 7, (int64_t)c.ffn * d, 0);
+      matmul(x, T, d, Wg, c.ffn, g);
+    }
+    {
+      auto Wu = tensor(seed, b + 8, (int64_t)c.ffn * d, 0);
+      matmul(x, T, d, Wu, c.ffn, u);
+    }
+    for (size_t i = 0; i < g.size(); ++i) {
+      double sg = g[i] / (1.0 + std::exp(-g[i]));  // SiLU
+      g[i] = bf16_round((float)(sg * u[i]));
+    }
+    {
+      auto Wd = tensor(seed, b + 9, (int64_t)d * c.ffn, 0);
+      matmul(g, T, c.ffn, Wd, d, y);
+      for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
+    }
+  }
+  auto wf = tensor(seed, 2, d, 1);
+  const int R = T - first_row;
+  std::vector<double> hl((size_t)R * d);
+  std::memcpy(hl.data(), &h[(size_t)first_row * d], sizeof(double) * R * d);
+  rmsnorm_bf16(hl, R, d, wf, c.eps, x);
+  auto Wl = tensor(seed, 1, (int64_t)c.vocab * d, 0);
+  matmul(x, R, d, Wl, c.vocab, y);
+  std::memcpy(logits, y.data(), sizeof(double) * (size_t)R * c.vocab);
+}
+
+// C8 greedy: argmax, lowest index on ties.
+int32_t argmax_lowest(const float* x, int64_t n) {
+  int64_t best = 0;
+  for (int64_t i = 1; i < n; ++i)
+    if (x[i] > x[best]) best = i;
+  return (int32_t)best;
+}
+
+// Philox4x32-10 (Salmon et al., SC'11), Random123 constants.
+void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  uint32_t k[2] = {key_in[0], key_in[1]};
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0];
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c[3] ^ k[1];
+    uint32_t n3 = lo0;
+    c[0] = n0, c[1] = n1, c[2] = n2, c[3] = n3;
+    k[0] += 0x9E3779B9u;
+    k[1] += 0xBB67AE85u;
+  }
+  out[0] = c[0], out[1] = c[1], out[2] = c[2], out[3] = c[3];
+}
+
+// C8 top-p (R18): p = softmax(logits / tau) in fp64; nucleus = the
+// shortest prefix of tokens sorted by (p desc, id asc) with mass >= top_p;
+// u = 24-bit uniform from Philox4x32-10(key = seed, ctr = (sample_id, step));
+// inverse CDF over the nucleus (renormalised) in that order.
+int32_t sample_top_p(const float* logits, int64_t V, float temperature, float top_p, uint64_t seed,
+                     uint64_t sample_id, uint64_t step) {
+  std::vector<double> p(V);
+  double mx = -INFINITY;
+  for (int64_t i = 0; i < V; ++i) mx = std::max(mx, (double)logits[i] / temperature);
+  double den = 0;
+  for (int64_t i = 0; i < V; ++i) {
+    p[i] = std::exp((double)logits[i] / temperature - mx);
+    den += p[i];
+  }
+  for (auto& e : p) e /= den;
+  std::vector<int64_t> ord(V);
+  for (int64_t i = 0; i < V; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return p[a] > p[b]; });
+  double mass = 0;
+  int64_t n = 0;
+  while (n < V) {
+    mass += p[ord[n]];
+    ++n;
+    if (mass >= top_p) break;
+  }
+  uint32_t ctr[4] = {(uint32_t)sample_id, (uint32_t)(sample_id >> 32), (uint32_t)step, (uint32_t)(step >> 32)};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t r[4];
+  philox4x32_10(ctr, key, r);
+  double uu = (double)(r[0] >> 8) * (1.0 / 16777216.0) * mass;
+  double cum = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    cum += p[ord[j]];
+    if (uu < cum) return (int32_t)ord[j];
+  }
+  return (int32_t)ord[n - 1];
+}
+
+}  // namespace oracle
