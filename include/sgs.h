@@ -1,0 +1,233 @@
+/*
+ * sgs.h — C-ABI of the B200-native Stream Generation Service hot path
+ * (StreamRL, arXiv 2504.15930; PAPER.md = the paper's text, cited P:<line>).
+ *
+ * SGS exposes update(weights) and generate(prompts) (§3) and
+ * returns each completed sample "in a stream fashion".
+ * Prompts arrive with ranker-estimated output lengths;
+ * output lengths are forced for evaluation.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns an sgs_status; the message is in sgs_last_error().
+ *  - Inputs are caller-owned and copied before return.  Pointers documented
+ *    "device" are CUDA device pointers on the handle's device; "host" pointers
+ *    are ordinary (or pinned) host memory.
+ *  - A handle is single-threaded.  One handle = one generation instance =
+ *    one GPU (data-parallel instances are "entirely independent").
+ *  - After a CUDA or NCCL error the handle is poisoned: later calls return
+ *    SGS_E_STATE.
+ *  - Device memory comes from the caller (PyTorch) as one arena; the library
+ *    never calls cudaMalloc after sgs_init.
+ *  - device < 0 selects "null-device" mode: the host scheduler, allocator and
+ *    dispatcher run and trace exactly as on the GPU, no kernel is launched and
+ *    every generated token is 0 (CPU parity of the schedule).
+ */
+#ifndef SGS_H_
+#define SGS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sgs_handle sgs_handle;
+
+typedef enum {
+  SGS_OK = 0,
+  SGS_E_INVAL = -1,       /* bad argument; the call had no effect */
+  SGS_E_NOMEM = -2,       /* arena too small */
+  SGS_E_STATE = -3,       /* wrong state (poisoned handle, update while busy, no comm) */
+  SGS_E_CAPACITY = -4,    /* a sample can never fit (pages > pool or P+d-1 > max_ctx) */
+  SGS_E_CUDA = -5,
+  SGS_E_NCCL = -6,
+  SGS_E_UNSUPPORTED = -7  /* shape not supported by the sm_100a kernels */
+} sgs_status;
+
+/* Model shape (Table 2; fields the paper omits follow Qwen2.5). */
+typedef struct {
+  int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, d_ffn, vocab;
+  float rms_eps;      /* 1e-6 */
+  double rope_theta;  /* 1e6, NeoX rotate-half */
+} sgs_model_cfg;
+
+/* Integer T(b) profile (appendix): T(b)[ps] = t0_ns*1000 + k0_ps*b
+ * for b < b_star, continued with slope k1_ps above (t1 from continuity P:49). */
+typedef struct {
+  int64_t t0_ns, k0_ps, b_star, k1_ps;
+} sgs_tb_profile;
+
+enum { SGS_DISPATCH_SKEW = 0, SGS_DISPATCH_ROUND_ROBIN = 1, SGS_DISPATCH_RANDOM = 2 };
+enum { SGS_SCORE_SUM = 0, SGS_SCORE_MAX = 1 };
+enum { SGS_SAMPLE_GREEDY = 0, SGS_SAMPLE_TOP_P = 1 };
+enum {
+  SGS_F_KEEP_LOGITS = 1,     /* keep fp32 logits of the last iteration (teacher-forcing tests) */
+  SGS_F_NO_GRAPHS = 2        /* launch the decode iteration eagerly (no CUDA graphs) */
+};
+
+typedef struct {
+  int32_t max_batch;         /* B, the per-instance batch cap */
+  int32_t page_size;         /* KV page in tokens (16) */
+  int32_t max_ctx;           /* longest prompt + output - 1 a sample may reach */
+  int32_t max_prefill_tokens;/* prefill chunk, tokens (0 -> 16384) */
+  int64_t n_pages;           /* KV pool pages; 0 -> as many as fit in the arena */
+  void* arena;               /* device memory from the caller (ignored in null-device mode) */
+  int64_t arena_bytes;
+  void* stream;              /* cudaStream_t the library launches on (NULL = legacy default) */
+  int32_t device;            /* CUDA device ordinal; < 0 -> null-device mode */
+  int32_t n_instances;       /* N data-parallel instances (one per GPU / rank) */
+  int32_t instance_rank;     /* this handle's instance in [0, N) */
+  int32_t dispatch;          /* SGS_DISPATCH_* (Alg. 2 by default) */
+  int32_t alpha_pct;         /* long-tail threshold alpha in percent (20) */
+  int32_t score;             /* SGS_SCORE_SUM (literal P:935) or SGS_SCORE_MAX */
+  int32_t tail_ceil;         /* 0: floor(alpha*n), 1: ceil */
+  sgs_tb_profile profile;    /* T(b) used by Eq. 2 */
+  int32_t sampling;          /* SGS_SAMPLE_* */
+  float temperature, top_p;
+  uint64_t sample_seed;      /* Philox key for top-p */
+  uint64_t weight_seed;      /* hash-init seed when sgs_init gets no weights */
+  int32_t flags;             /* SGS_F_* */
+} sgs_engine_cfg;
+
+/* One prompt (host memory, copied by sgs_submit). */
+typedef struct {
+  uint64_t id;               /* unique within the handle's lifetime */
+  const int32_t* tokens;     /* host, len token ids in [0, vocab) */
+  int32_t len;               /* prompt length P >= 1 */
+} sgs_prompt;
+
+/* One completed sample, emitted in ascending id within an iteration. */
+typedef struct {
+  uint64_t id;
+  int32_t instance;
+  int32_t n_tokens;          /* = forced length d */
+  const int32_t* tokens;     /* host, library-owned, valid until the next sgs_step */
+  int64_t admit_iter, finish_iter;  /* per-instance iteration counter */
+  int32_t weight_version;
+  int32_t slot;
+} sgs_completion;
+
+/* Bytes the caller must provide as the arena for a given configuration
+ * (weights + KV pool of n_pages + scratch).  kv_page_bytes = bytes of one page
+ * over all layers, so callers can size n_pages from free memory. */
+sgs_status sgs_arena_bytes(const sgs_model_cfg* m, const sgs_engine_cfg* e, int64_t n_pages,
+                           int64_t* fixed_bytes, int64_t* kv_page_bytes);
+
+/* Create an instance.  weights == NULL: hash-initialise every tensor on the
+ * device from e->weight_seed.  Null-device mode ignores arena. */
+sgs_status sgs_init(const sgs_model_cfg* m, const sgs_engine_cfg* e, sgs_handle** out);
+void sgs_destroy(sgs_handle* h);
+const char* sgs_last_error(const sgs_handle* h); /* h may be NULL (init errors) */
+
+/* Submit one RL batch: n prompts with ranker hints and forced
+ * output lengths.  Every instance receives the SAME full batch;
+ * Alg. 2 runs identically on each and the handle keeps the samples
+ * dispatched to its instance_rank (no communication).  Validation: P >= 1,
+ * hint >= 1, forced >= 1, tokens in [0, vocab), unique ids; violations ->
+ * SGS_E_INVAL with no effect; a sample that can never fit -> SGS_E_CAPACITY.
+ * n_mine (optional) receives how many samples this instance kept. */
+sgs_status sgs_submit(sgs_handle* h, const sgs_prompt* prompts, int32_t n, const int32_t* output_len_hint,
+                      const int32_t* forced_len, int32_t* n_mine);
+
+/* Run one continuous-batching iteration (longest-first refill under B,
+ * P:996-998; prefill of admitted prompts + one decode step of the running
+ * samples) and return the samples that completed in it, ascending id.  With
+ * nothing queued or active: SGS_OK, *n_out = 0, no iteration is counted.
+ * Completions beyond cap stay queued and are returned (before any new
+ * iteration) by the next call. */
+sgs_status sgs_step(sgs_handle* h, sgs_completion* out, int32_t cap, int32_t* n_out);
+
+/* Samples queued + active on this instance. */
+sgs_status sgs_pending(const sgs_handle* h, int64_t* queued, int64_t* active);
+
+/* Weight sync: the only collective.  sgs_comm_unique_id on the
+ * root, share the 128 bytes (e.g. torch.distributed), sgs_comm_init on every
+ * rank, then sgs_update_weights broadcasts the root's weights to all ranks
+ * (ncclBroadcast over NVLink) and increments the weight version.  Requires no
+ * sample in flight (SGS_E_STATE otherwise). */
+sgs_status sgs_comm_unique_id(uint8_t out[128]);
+sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int32_t world);
+sgs_status sgs_update_weights(sgs_handle* h, int32_t root);
+/* Trainer proxy: regenerate this handle's weights from a new seed on device
+ * (the root does this before sgs_update_weights). */
+sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed);
+/* Order-independent 64-bit checksum of one logical weight tensor (DESIGN.md
+ * §3 tensor ids): sum_i bits16(w_i) * (2i+1) mod 2^64. */
+sgs_status sgs_weight_checksum(sgs_handle* h, int64_t tensor_id, uint64_t* out);
+sgs_status sgs_weight_version(const sgs_handle* h, int32_t* out);
+
+/* Trace for schedule parity (DESIGN.md §5 format, int64 stream): iteration
+ * records t,b,sumctx,nadm,ncomp,nalloc,nfree,adm...,comp...,alloc...,freed...
+ * (which = 0) or per-sample records id,slot,admit,finish,npages,pages...
+ * (which = 1, ascending id, samples admitted so far).  buf == NULL -> *n gets
+ * the length.  The iteration trace can be cleared with sgs_trace_clear. */
+sgs_status sgs_trace(const sgs_handle* h, int32_t which, int64_t* buf, int64_t cap, int64_t* n);
+sgs_status sgs_trace_clear(sgs_handle* h);
+
+/* fp32 logits of the last iteration (SGS_F_KEEP_LOGITS): rows = samples that
+ * produced a token, in (prefill-first, then ascending slot) order; ids[r] and
+ * pos[r] (index of the generated token, 0-based) identify each row. */
+sgs_status sgs_last_logits(sgs_handle* h, float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap,
+                           int32_t* rows);
+
+/* Device-side timing of the last iteration's kernels (CUDA events), ms. */
+sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms);
+/* Count of kernel launches (or graph launches' kernels) issued so far. */
+sgs_status sgs_kernel_launches(const sgs_handle* h, int64_t* n);
+
+/* T(b) fit (C3): hinge least squares over n measured (b, T_ns)
+ * points; out = {t0, k0, k1, t1, sse}, prof = rounded integer profile.
+ * Returns SGS_E_INVAL when no breakpoint is identifiable. */
+sgs_status sgs_fit_profile(int32_t n, const double* b, const double* T_ns, double out[5], sgs_tb_profile* prof);
+
+/* Alg. 2 on its own (pure host function): instance per sample. */
+sgs_status sgs_dispatch_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* ids, const int32_t* prompt_len,
+                             const int32_t* hint, int64_t pool_pages, int32_t* instance, int32_t* n_l);
+
+/* ------------------------------------------------------------------------
+ * Kernel-level entry points (device pointers; launched on `stream`).  These
+ * are the hot-path kernels the iteration is built from, exported so the
+ * parity tests can drive each one against the oracle.
+ * ------------------------------------------------------------------------ */
+
+/* a8/K1+K2: paged GQA decode attention (P:361-363 memory-bound decode).
+ * q:      device bf16 [b, nq, hd]
+ * kv:     device bf16 page pool, one layer: [n_pages][nkv][2][page][hd] with
+ *         16-byte chunks XOR-swizzled within each row
+ * block_table: device int32 [b, max_pages_per_seq]; ctx: device int32 [b]
+ * out:    device, [b, nq, hd], bf16 (out_fp32 = 0) or fp32 (out_fp32 = 1)
+ * workspace: device, >= sgs_attn_workspace_bytes(...) bytes
+ * Work is split over KV pages (split-K) and merged with the LSE combine. */
+int64_t sgs_attn_workspace_bytes(int32_t b, int32_t nq, int32_t nkv, int32_t hd, int32_t max_pages_per_seq);
+sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
+                                   int32_t b, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
+                                   int32_t max_pages_per_seq, int32_t max_ctx_hint, void* out, int32_t out_fp32,
+                                   void* workspace, int64_t workspace_bytes, int32_t split_pages, void* stream);
+
+/* K3/K4: tcgen05 bf16 GEMM, C[t, n] (+)= sum_k X[t, k] * W[n, k].
+ * W device bf16 [N, K] row-major; X device bf16 [T, K]; C device fp32 [T, ldc].
+ * mode 0: C = result; mode 1: C += result (atomic, split-K capable).
+ * splits: K splits (mode 1 only; 0 = automatic).  N % 128 == 0, K % 64 == 0. */
+sgs_status sgs_op_gemm(const void* W, const void* X, void* C, int32_t N, int32_t K, int32_t T, int32_t ldc,
+                       int32_t mode, int32_t splits, void* stream);
+
+/* a6/K6: y[t] = bf16(x[t] / sqrt(mean(x[t]^2) + eps) * w); x fp32 [T, d], w bf16 [d]. */
+sgs_status sgs_op_rmsnorm(const float* x, const void* w, void* y, int32_t T, int32_t d, float eps, void* stream);
+
+/* a7/K7: RoPE + KV append.  qkv fp32 [T, (nq+2nkv)*hd] (+ bias bf16),
+ * pos int32 [T], slot int32 [T] -> q bf16 [T, nq, hd]; k, v written into the
+ * page pool via block_table[slot][pos/page], pos % page.  cos_sin fp32
+ * [max_pos, hd/2, 2] from sgs_rope_table. */
+sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
+                              const int32_t* block_table, int32_t max_pages_per_seq, const float* cos_sin,
+                              void* q_out, void* kv, int32_t T, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
+                              void* stream);
+sgs_status sgs_rope_table(float* host_out, int32_t max_pos, int32_t hd, double theta);
+
+/* K9 greedy: ids[r] = argmax_v logits[r, v] (lowest index on ties). */
+sgs_status sgs_op_argmax(const float* logits, int32_t rows, int32_t V, int32_t* ids, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGS_H_ */

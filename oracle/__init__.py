@@ -90,6 +90,8 @@ def _declare(L):
     L.oracle_decoder_forward.argtypes = [P_i32, P_f64, ctypes.c_uint64, P_i32, ctypes.c_int32, ctypes.c_int32,
                                          P_f64]
     L.oracle_decoder_forward.restype = ctypes.c_int32
+    L.oracle_rmsnorm.argtypes = [P_f64, P_f32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P_f64]
+    L.oracle_rope.argtypes = [P_f64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
     L.oracle_argmax.argtypes = [P_f32, ctypes.c_int64]
     L.oracle_argmax.restype = ctypes.c_int32
     L.oracle_philox.argtypes = [P_u32, P_u32, P_u32]
@@ -274,6 +276,23 @@ def decoder_forward(shape, seed: int, tokens, first_row: int):
     if rc != 0:
         raise RuntimeError(lib().oracle_last_error().decode())
     return out
+
+
+def rmsnorm(x, w, eps):
+    """y = bf16(x / sqrt(mean(x^2) + eps) * w) row-wise; x [T, d] -> float64 [T, d] of bf16 values."""
+    x = np.ascontiguousarray(x, np.float64)
+    w = np.ascontiguousarray(w, np.float32)
+    T, d = x.shape
+    y = np.zeros_like(x)
+    lib().oracle_rmsnorm(_p(x, P_f64), _p(w, P_f32), T, d, eps, _p(y, P_f64))
+    return y
+
+
+def rope(v, pos: int, theta: float):
+    """NeoX rotate-half RoPE of one head vector (fp64)."""
+    v = np.array(v, np.float64)
+    lib().oracle_rope(_p(v, P_f64), len(v), int(pos), theta)
+    return v
 
 
 def argmax(x) -> int:

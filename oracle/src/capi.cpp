@@ -147,6 +147,16 @@ int32_t oracle_decoder_forward(const int32_t* cfg_i, const double* cfg_d, uint64
   }
 }
 
+// y = bf16(x / sqrt(mean(x^2) + eps) * w), rows of x [T x d]
+void oracle_rmsnorm(const double* x, const float* w, int32_t T, int32_t d, double eps, double* y) {
+  std::vector<double> h(x, x + (size_t)T * d), out;
+  rmsnorm_bf16(h, T, d, std::vector<float>(w, w + d), eps, out);
+  std::memcpy(y, out.data(), sizeof(double) * (size_t)T * d);
+}
+
+// NeoX rotate-half RoPE of one head vector (in place, fp64)
+void oracle_rope(double* v, int32_t hd, int32_t pos, double theta) { rope(v, hd, pos, theta); }
+
 int32_t oracle_argmax(const float* x, int64_t n) { return argmax_lowest(x, n); }
 
 void oracle_philox(const uint32_t* ctr4, const uint32_t* key2, uint32_t* out4) { philox4x32_10(ctr4, key2, out4); }

@@ -141,7 +141,7 @@ static void matmul(const std::vector<double>& x, int T, int cols, const std::vec
   }
 }
 
-static void rmsnorm_bf16(const std::vector<double>& h, int T, int d, const std::vector<float>& w, double eps,
+void rmsnorm_bf16(const std::vector<double>& h, int T, int d, const std::vector<float>& w, double eps,
                          std::vector<double>& x) {
   x.resize((size_t)T * d);
   for (int t = 0; t < T; ++t) {
@@ -153,7 +153,7 @@ static void rmsnorm_bf16(const std::vector<double>& h, int T, int d, const std::
 }
 
 // NeoX rotate-half RoPE on one head vector at position pos.
-static void rope(double* v, int hd, int pos, double theta) {
+void rope(double* v, int hd, int pos, double theta) {
   const int half = hd / 2;
   for (int i = 0; i < half; ++i) {
     double inv = std::pow(theta, -2.0 * i / hd);

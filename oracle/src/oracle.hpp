@@ -106,6 +106,9 @@ uint64_t tensor_checksum(uint64_t seed, uint64_t tensor_id, int64_t n, int is_no
 void attention_fp64(int nq, int nkv, int hd, int ctx, const float* q, const float* K, const float* V,
                     double* out);
 
+void rmsnorm_bf16(const std::vector<double>& h, int T, int d, const std::vector<float>& w, double eps,
+                  std::vector<double>& x);
+void rope(double* v, int hd, int pos, double theta);
 void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, int T, int first_row,
                      double* logits /* [(T-first_row) x vocab] */);
 

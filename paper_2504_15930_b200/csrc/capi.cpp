@@ -1,0 +1,230 @@
+// extern "C" implementation of include/sgs.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sgs.h"
+#include "engine/engine.hpp"
+#include "host/sched.hpp"
+#include "kernels/kernels.h"
+
+struct sgs_handle {
+  sgs::Engine eng;
+};
+
+static thread_local std::string g_init_err;
+
+extern "C" {
+
+sgs_status sgs_arena_bytes(const sgs_model_cfg* m, const sgs_engine_cfg* e, int64_t n_pages, int64_t* fixed_bytes,
+                           int64_t* kv_page_bytes) {
+  if (!m || !e || n_pages < 0) return SGS_E_INVAL;
+  sgs::ArenaLayout L0, L;
+  sgs::Engine::layout(*m, *e, 0, &L0);
+  sgs::Engine::layout(*m, *e, n_pages, &L);
+  if (fixed_bytes) *fixed_bytes = L0.total + 4096;
+  if (kv_page_bytes) *kv_page_bytes = L.kv_page_bytes;
+  return SGS_OK;
+}
+
+sgs_status sgs_init(const sgs_model_cfg* m, const sgs_engine_cfg* e, sgs_handle** out) {
+  if (!m || !e || !out) return SGS_E_INVAL;
+  auto* h = new sgs_handle();
+  sgs_status s = h->eng.init(*m, *e);
+  if (s != SGS_OK) {
+    g_init_err = h->eng.err;
+    delete h;
+    *out = nullptr;
+    return s;
+  }
+  *out = h;
+  return SGS_OK;
+}
+
+void sgs_destroy(sgs_handle* h) { delete h; }
+
+const char* sgs_last_error(const sgs_handle* h) { return h ? h->eng.err.c_str() : g_init_err.c_str(); }
+
+sgs_status sgs_submit(sgs_handle* h, const sgs_prompt* prompts, int32_t n, const int32_t* hint,
+                      const int32_t* forced_len, int32_t* n_mine) {
+  if (!h) return SGS_E_INVAL;
+  return h->eng.submit(prompts, n, hint, forced_len, n_mine);
+}
+
+sgs_status sgs_step(sgs_handle* h, sgs_completion* out, int32_t cap, int32_t* n_out) {
+  if (!h || !n_out || cap < 0 || (cap > 0 && !out)) return SGS_E_INVAL;
+  return h->eng.step(out, cap, n_out);
+}
+
+sgs_status sgs_pending(const sgs_handle* h, int64_t* queued, int64_t* active) {
+  if (!h) return SGS_E_INVAL;
+  if (queued) *queued = h->eng.sched.queued();
+  if (active) *active = h->eng.sched.active();
+  return SGS_OK;
+}
+
+sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int32_t world) {
+  if (!h || !id || world < 1 || rank < 0 || rank >= world) return SGS_E_INVAL;
+  return h->eng.comm_init(id, rank, world);
+}
+
+sgs_status sgs_update_weights(sgs_handle* h, int32_t root) {
+  if (!h) return SGS_E_INVAL;
+  return h->eng.update_weights(root);
+}
+
+sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed) {
+  if (!h) return SGS_E_INVAL;
+  return h->eng.load_weights_seed(seed);
+}
+
+sgs_status sgs_weight_checksum(sgs_handle* h, int64_t tensor_id, uint64_t* out) {
+  if (!h || !out) return SGS_E_INVAL;
+  return h->eng.checksum(tensor_id, out);
+}
+
+sgs_status sgs_weight_version(const sgs_handle* h, int32_t* out) {
+  if (!h || !out) return SGS_E_INVAL;
+  *out = h->eng.version;
+  return SGS_OK;
+}
+
+sgs_status sgs_trace(const sgs_handle* h, int32_t which, int64_t* buf, int64_t cap, int64_t* n) {
+  if (!h || !n) return SGS_E_INVAL;
+  std::vector<int64_t> tmp;
+  const std::vector<int64_t>* src;
+  if (which == 0) {
+    src = &h->eng.sched.trace_iters;
+  } else {
+    h->eng.sched.sample_trace(&tmp);
+    src = &tmp;
+  }
+  *n = (int64_t)src->size();
+  if (buf) std::memcpy(buf, src->data(), sizeof(int64_t) * (size_t)std::min<int64_t>(cap, *n));
+  return SGS_OK;
+}
+
+sgs_status sgs_trace_clear(sgs_handle* h) {
+  if (!h) return SGS_E_INVAL;
+  h->eng.sched.trace_iters.clear();
+  return SGS_OK;
+}
+
+sgs_status sgs_last_logits(sgs_handle* h, float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap,
+                           int32_t* rows) {
+  if (!h || !rows) return SGS_E_INVAL;
+  return h->eng.last_logits(logits, ids, tok_idx, cap, rows);
+}
+
+sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms) {
+  if (!h || !ms) return SGS_E_INVAL;
+  *ms = h->eng.last_ms;
+  return SGS_OK;
+}
+
+sgs_status sgs_kernel_launches(const sgs_handle* h, int64_t* n) {
+  if (!h || !n) return SGS_E_INVAL;
+  *n = h->eng.launches;
+  return SGS_OK;
+}
+
+sgs_status sgs_fit_profile(int32_t n, const double* b, const double* T_ns, double out[5], sgs_tb_profile* prof) {
+  if (n <= 0 || !b || !T_ns || !out || !prof) return SGS_E_INVAL;
+  int64_t bs = 0, p[4];
+  if (!sgs::fit_tb(n, b, T_ns, out, &bs, p)) return SGS_E_INVAL;
+  prof->t0_ns = p[0], prof->k0_ps = p[1], prof->b_star = p[2], prof->k1_ps = p[3];
+  return SGS_OK;
+}
+
+sgs_status sgs_dispatch_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* ids, const int32_t* prompt_len,
+                             const int32_t* hint, int64_t pool_pages, int32_t* instance, int32_t* n_l) {
+  if (!e || n < 0 || (n > 0 && (!ids || !prompt_len || !hint || !instance)) || e->n_instances < 1 ||
+      pool_pages < 1)
+    return SGS_E_INVAL;
+  sgs::DispatchCfg dc{e->n_instances, e->max_batch, e->page_size, pool_pages, e->profile.t0_ns, e->profile.k0_ps,
+                      e->profile.b_star, e->profile.k1_ps, e->alpha_pct, e->score, e->tail_ceil, e->dispatch,
+                      e->sample_seed};
+  const int nl = sgs::dispatch_alg2(dc, n, ids, prompt_len, hint, instance);
+  if (n_l) *n_l = nl;
+  return SGS_OK;
+}
+
+// ------------------------------------------------------------------ kernel-level entry points
+static sgs_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SGS_OK : SGS_E_CUDA; }
+
+int64_t sgs_attn_workspace_bytes(int32_t b, int32_t nq, int32_t nkv, int32_t hd, int32_t max_pages_per_seq) {
+  const int64_t items = (int64_t)b * nkv * max_pages_per_seq + 64;
+  return sgs::attn_workspace_bytes((int)items, (int)items, nq / nkv, hd);
+}
+
+sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
+                                   int32_t b, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
+                                   int32_t max_pages_per_seq, int32_t max_ctx_hint, void* out, int32_t out_fp32,
+                                   void* workspace, int64_t workspace_bytes, int32_t split_pages, void* stream) {
+  (void)max_ctx_hint;
+  if (b <= 0) return SGS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<int32_t> hctx(b);
+  if (cudaMemcpyAsync(hctx.data(), ctx, (size_t)b * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return SGS_E_CUDA;
+  for (int i = 0; i < b; ++i)
+    if (hctx[i] < 1 || (hctx[i] + page - 1) / page > max_pages_per_seq) return SGS_E_INVAL;
+  sgs::AttnPlan plan;
+  sgs::attn_plan(hctx.data(), b, nkv, page, split_pages, &plan);
+  const int g = nq / nkv;
+  const int64_t need = sgs::attn_workspace_bytes((int)plan.items.size(), plan.n_parts, g, hd);
+  if (need > workspace_bytes) return SGS_E_NOMEM;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  auto* d_items = reinterpret_cast<sgs::AttnItem*>(ws);
+  auto* d_combs = reinterpret_cast<sgs::AttnComb*>(ws + plan.items.size() * sizeof(sgs::AttnItem));
+  size_t off = plan.items.size() * sizeof(sgs::AttnItem) + plan.combs.size() * sizeof(sgs::AttnComb);
+  off = (off + 255) / 256 * 256;
+  float* part_o = reinterpret_cast<float*>(ws + off);
+  float* part_ml = part_o + (size_t)std::max(plan.n_parts, 1) * g * hd;
+  if (cudaMemcpyAsync(d_items, plan.items.data(), plan.items.size() * sizeof(sgs::AttnItem), cudaMemcpyHostToDevice,
+                      st) != cudaSuccess)
+    return SGS_E_CUDA;
+  if (!plan.combs.empty() &&
+      cudaMemcpyAsync(d_combs, plan.combs.data(), plan.combs.size() * sizeof(sgs::AttnComb), cudaMemcpyHostToDevice,
+                      st) != cudaSuccess)
+    return SGS_E_CUDA;
+  cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, d_items, (int)plan.items.size(), d_combs,
+                                   (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, out_fp32,
+                                   part_o, part_ml, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host plan vectors die here
+  return cuda_status(e);
+}
+
+sgs_status sgs_op_gemm(const void* W, const void* X, void* C, int32_t N, int32_t K, int32_t T, int32_t ldc,
+                       int32_t mode, int32_t splits, void* stream) {
+  if (!W || !X || !C || N <= 0 || K <= 0 || T < 0 || mode < 0 || mode > 2) return SGS_E_INVAL;
+  if (N % 128 || K % 64) return SGS_E_UNSUPPORTED;
+  return cuda_status(sgs::gemm_bf16(W, X, reinterpret_cast<float*>(C), N, K, T, ldc, mode, splits,
+                                    reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sgs_status sgs_op_rmsnorm(const float* x, const void* w, void* y, int32_t T, int32_t d, float eps, void* stream) {
+  if (!x || !w || !y || T < 0 || d <= 0) return SGS_E_INVAL;
+  return cuda_status(sgs::rmsnorm(x, w, y, nullptr, T, d, eps, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
+                              const int32_t* block_table, int32_t max_pages_per_seq, const float* cos_sin,
+                              void* q_out, void* kv, int32_t T, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
+                              void* stream) {
+  if (!qkv || !pos || !cos_sin || !q_out || T < 0) return SGS_E_INVAL;
+  return cuda_status(sgs::rope_append(qkv, bias, pos, slot, block_table, max_pages_per_seq, cos_sin, q_out, kv,
+                                      nullptr, nullptr, T, nq, nkv, hd, page, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sgs_status sgs_op_argmax(const float* logits, int32_t rows, int32_t V, int32_t* ids, void* stream) {
+  if (!logits || !ids || rows < 0 || V <= 0) return SGS_E_INVAL;
+  return cuda_status(sgs::argmax_rows(logits, rows, V, ids, nullptr, nullptr, nullptr, nullptr, 0,
+                                      reinterpret_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

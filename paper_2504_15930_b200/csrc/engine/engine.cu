@@ -1,0 +1,755 @@
+// Engine: one SGS generation instance on one B200.
+//
+// Per iteration (sgs_step): the host scheduler decides admissions (longest
+// first), page allocations and completions; the engine stages all
+// per-iteration metadata in one pinned buffer (one H2D copy), then runs
+//   prefill of the admitted prompts (chunks of <= max_prefill_tokens):
+//     embed -> L x [RMSNorm, QKV GEMM, RoPE+KV append, causal attention,
+//                   O GEMM (+residual), RMSNorm, gate/up GEMM, SwiGLU,
+//                   down GEMM (+residual)] -> final norm on the last token
+//     -> LM head -> greedy sample (token 1)
+//   decode of the running samples (one token each):
+//     same chain with paged split-K decode attention
+// and streams the completed samples back.  The residual stream is
+// fp32; every other activation is bf16 (R12).
+#include "engine.hpp"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "nccl.h"
+
+namespace sgs {
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64_t n_pages, ArenaLayout* L) {
+  const int64_t d = m.d_model, hd = m.head_dim, nq = m.n_q_heads, nkv = m.n_kv_heads, f = m.d_ffn, V = m.vocab;
+  const int64_t B = e.max_batch;
+  const int64_t pf = e.max_prefill_tokens > 0 ? e.max_prefill_tokens : 16384;
+  const int64_t tmax = std::max<int64_t>(pf, B);
+  const int64_t page = e.page_size;
+  const int64_t max_pages = (e.max_ctx + page - 1) / page + 1;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  // weights (contiguous so the weight sync can broadcast one range)
+  const int64_t per_layer = ((nq + 2 * nkv) * hd * d + (nq + 2 * nkv) * hd + d * nq * hd + 2 * f * d + d * f + 2 * d);
+  const int64_t wbytes = (m.n_layers * per_layer + 2 * V * d + d) * 2;
+  take(wbytes + 256 * (8 * m.n_layers + 8));
+  L->weights_bytes = o;
+  L->kv_page_bytes = m.n_layers * nkv * 2 * page * hd * 2;
+  L->off_kv = take(n_pages * L->kv_page_bytes);
+  L->kv_bytes = n_pages * L->kv_page_bytes;
+  const int64_t s0 = o;
+  L->off_h = take(tmax * d * 4);
+  L->off_x = take(tmax * d * 2);
+  L->off_qkv = take(tmax * (nq + 2 * nkv) * hd * 4);
+  L->off_q = take(tmax * nq * hd * 2);
+  L->off_kc = take(tmax * nkv * hd * 2);
+  L->off_vc = take(tmax * nkv * hd * 2);
+  L->off_ao = take(tmax * nq * hd * 2);
+  L->off_gu = take(tmax * 2 * f * 4);
+  L->off_mm = take(tmax * f * 2);
+  L->off_logits = take(B * V * 4);
+  L->off_rope = take((int64_t)(e.max_ctx + 1) * (hd / 2) * 2 * 4);
+  L->off_bt = take(B * max_pages * 4);
+  L->off_last = take(B * 4);
+  L->off_hist = take(B * (int64_t)(e.max_ctx + 1) * 4);
+  // per-iteration metadata: bt deltas, prefill tokens/pos/slot, decode rows, attention work lists
+  const int64_t max_items = 2 * 2 * 148 + 2 * B * nkv + 64;
+  L->meta_bytes = align_up(4 * (3 * (B * max_pages + B) + 3 * tmax + 8 * B + 2 * (tmax / 64 + B) + 16 * B) +
+                               max_items * (int64_t)(sizeof(AttnItem) + sizeof(AttnComb)) + 4096,
+                           256);
+  L->off_meta = take(L->meta_bytes);
+  L->attn_bytes = max_items * (nq / nkv) * (hd + 2) * 4;
+  L->off_attn = take(L->attn_bytes);
+  L->off_cksum = take(64);
+  L->scratch_bytes = o - s0;
+  L->total = o;
+  L->tmax = (int)tmax;
+  L->max_pages = (int)max_pages;
+  L->max_items = (int)max_items;
+  return SGS_OK;
+}
+
+sgs_status Engine::cuda_fail(cudaError_t e, const char* what) {
+  err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  poisoned = true;
+  return SGS_E_CUDA;
+}
+
+#define CK(call, what)                                  \
+  do {                                                  \
+    cudaError_t e__ = (call);                           \
+    if (e__ != cudaSuccess) return cuda_fail(e__, what); \
+  } while (0)
+
+Engine::~Engine() {
+  if (!null_) {
+    if (st_) cudaStreamSynchronize(st_);
+    if (meta_host_) cudaFreeHost(meta_host_);
+    if (tok_host_) cudaFreeHost(tok_host_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+  }
+}
+
+void Engine::build_tensor_table() {
+  tensors_.clear();
+  const int64_t d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn;
+  tensors_.push_back({0, embed_, (int64_t)m_.vocab * d, 0});
+  tensors_.push_back({1, lm_head_, (int64_t)m_.vocab * d, 0});
+  tensors_.push_back({2, nf_, d, 1});
+  for (int l = 0; l < m_.n_layers; ++l) {
+    const int64_t b = 16 + 16 * (int64_t)l;
+    auto* L = &layers_[l];
+    auto at = [](void* p, int64_t elems) { return (void*)((uint16_t*)p + elems); };
+    tensors_.push_back({b + 0, L->wqkv, nq * hd * d, 0});
+    tensors_.push_back({b + 1, at(L->wqkv, nq * hd * d), nkv * hd * d, 0});
+    tensors_.push_back({b + 2, at(L->wqkv, (nq + nkv) * hd * d), nkv * hd * d, 0});
+    tensors_.push_back({b + 3, L->bqkv, nq * hd, 0});
+    tensors_.push_back({b + 4, at(L->bqkv, nq * hd), nkv * hd, 0});
+    tensors_.push_back({b + 5, at(L->bqkv, (nq + nkv) * hd), nkv * hd, 0});
+    tensors_.push_back({b + 6, L->wo, d * nq * hd, 0});
+    tensors_.push_back({b + 7, L->wgu, f * d, 0});
+    tensors_.push_back({b + 8, at(L->wgu, f * d), f * d, 0});
+    tensors_.push_back({b + 9, L->wd, d * f, 0});
+    tensors_.push_back({b + 10, L->n1, d, 1});
+    tensors_.push_back({b + 11, L->n2, d, 1});
+  }
+}
+
+sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
+  m_ = m;
+  e_ = e;
+  if (e_.max_prefill_tokens <= 0) e_.max_prefill_tokens = 16384;
+  if (m.n_layers <= 0 || m.d_model <= 0 || m.n_q_heads <= 0 || m.n_kv_heads <= 0 || m.head_dim <= 0 ||
+      m.d_ffn <= 0 || m.vocab <= 0 || e.max_batch <= 0 || e.page_size <= 0 || e.max_ctx <= 0 ||
+      e.n_instances <= 0 || e.instance_rank < 0 || e.instance_rank >= e.n_instances ||
+      m.n_q_heads % m.n_kv_heads) {
+    err = "invalid model/engine configuration";
+    return SGS_E_INVAL;
+  }
+  null_ = e.device < 0;
+  max_gen_ = e.max_ctx + 1;
+  if (null_) {
+    n_pages_ = e.n_pages;
+    if (n_pages_ <= 0) {
+      err = "null-device mode needs n_pages > 0";
+      return SGS_E_INVAL;
+    }
+    sched.init(e.max_batch, e.page_size, n_pages_);
+    return SGS_OK;
+  }
+  // ---- device mode: shape support of the sm_100a kernels
+  if (e.page_size != 16 || !(m.head_dim == 32 || m.head_dim == 64 || m.head_dim == 128) ||
+      m.n_q_heads / m.n_kv_heads > 16 || m.d_model % 128 || m.d_ffn % 128 || m.vocab % 128 ||
+      ((m.n_q_heads + 2 * m.n_kv_heads) * m.head_dim) % 128 || (m.n_q_heads * m.head_dim) % 64) {
+    err = "shape not supported by the sm_100a kernels (page 16, hd 32/64/128, dims multiple of 128)";
+    return SGS_E_UNSUPPORTED;
+  }
+  CK(cudaSetDevice(e.device), "cudaSetDevice");
+  st_ = reinterpret_cast<cudaStream_t>(e.stream);
+  ArenaLayout L0;
+  layout(m, e_, 0, &L0);
+  n_pages_ = e.n_pages;
+  if (n_pages_ <= 0) n_pages_ = (e.arena_bytes - L0.total - 4096) / L0.kv_page_bytes;
+  if (n_pages_ <= 0) {
+    err = "arena too small for weights + scratch";
+    return SGS_E_NOMEM;
+  }
+  layout(m, e_, n_pages_, &L_);
+  if (!e.arena || e.arena_bytes < L_.total) {
+    err = "arena smaller than sgs_arena_bytes()";
+    return SGS_E_NOMEM;
+  }
+  arena_ = reinterpret_cast<uint8_t*>(e.arena);
+  // carve weights
+  {
+    const int64_t d = m.d_model, hd = m.head_dim, nq = m.n_q_heads, nkv = m.n_kv_heads, f = m.d_ffn;
+    int64_t o = 0;
+    auto w = [&](int64_t elems) {
+      void* p = arena_ + o;
+      o = align_up(o + elems * 2, 256);
+      return p;
+    };
+    embed_ = w((int64_t)m.vocab * d);
+    lm_head_ = w((int64_t)m.vocab * d);
+    nf_ = w(d);
+    layers_.resize(m.n_layers);
+    for (auto& l : layers_) {
+      l.wqkv = w((nq + 2 * nkv) * hd * d);
+      l.bqkv = w((nq + 2 * nkv) * hd);
+      l.wo = w(d * nq * hd);
+      l.wgu = w(2 * f * d);
+      l.wd = w(d * f);
+      l.n1 = w(d);
+      l.n2 = w(d);
+    }
+    for (int i = 0; i < m.n_layers; ++i)
+      layers_[i].kv = arena_ + L_.off_kv + (int64_t)i * n_pages_ * (L_.kv_page_bytes / m.n_layers);
+  }
+  h_ = reinterpret_cast<float*>(arena_ + L_.off_h);
+  x_ = arena_ + L_.off_x;
+  qkv_ = reinterpret_cast<float*>(arena_ + L_.off_qkv);
+  q_ = arena_ + L_.off_q;
+  kc_ = arena_ + L_.off_kc;
+  vc_ = arena_ + L_.off_vc;
+  ao_ = arena_ + L_.off_ao;
+  gu_ = reinterpret_cast<float*>(arena_ + L_.off_gu);
+  mm_ = arena_ + L_.off_mm;
+  logits_ = reinterpret_cast<float*>(arena_ + L_.off_logits);
+  rope_ = reinterpret_cast<float*>(arena_ + L_.off_rope);
+  bt_ = reinterpret_cast<int32_t*>(arena_ + L_.off_bt);
+  last_tok_ = reinterpret_cast<int32_t*>(arena_ + L_.off_last);
+  hist_ = reinterpret_cast<int32_t*>(arena_ + L_.off_hist);
+  meta_dev_ = arena_ + L_.off_meta;
+  attn_ws_ = arena_ + L_.off_attn;
+  cksum_dev_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_cksum);
+  CK(cudaMallocHost(&meta_host_, L_.meta_bytes), "cudaMallocHost(meta)");
+  tok_host_cap_ = (int64_t)e.max_batch * max_gen_;
+  CK(cudaMallocHost(&tok_host_, tok_host_cap_ * 4), "cudaMallocHost(tokens)");
+  CK(cudaEventCreate(&ev0_), "event");
+  CK(cudaEventCreate(&ev1_), "event");
+  // zero the KV pool (finite garbage only beyond ctx) and the small state
+  CK(cudaMemsetAsync(arena_ + L_.off_kv, 0, L_.kv_bytes, st_), "memset kv");
+  CK(cudaMemsetAsync(bt_, 0, (size_t)e.max_batch * L_.max_pages * 4, st_), "memset bt");
+  CK(cudaMemsetAsync(last_tok_, 0, (size_t)e.max_batch * 4, st_), "memset last");
+  // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
+  {
+    const int half = m.head_dim / 2;
+    std::vector<float> tab((size_t)(e.max_ctx + 1) * half * 2);
+    sgs_rope_table(tab.data(), e.max_ctx + 1, m.head_dim, m.rope_theta);
+    CK(cudaMemcpy(rope_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice), "rope table");
+  }
+  build_tensor_table();
+  sgs_status s = load_weights_seed(e.weight_seed);
+  if (s != SGS_OK) return s;
+  CK(cudaStreamSynchronize(st_), "init sync");
+  sched.init(e.max_batch, e.page_size, n_pages_);
+  return SGS_OK;
+}
+
+sgs_status Engine::load_weights_seed(uint64_t seed) {
+  if (null_) return SGS_OK;
+  for (const auto& t : tensors_) {
+    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_), "hash_init");
+    ++launches;
+  }
+  CK(cudaStreamSynchronize(st_), "hash_init sync");
+  return SGS_OK;
+}
+
+sgs_status Engine::checksum(int64_t tensor_id, uint64_t* out) {
+  if (null_) {
+    err = "no weights in null-device mode";
+    return SGS_E_STATE;
+  }
+  for (const auto& t : tensors_)
+    if (t.id == tensor_id) {
+      CK(cudaMemsetAsync(cksum_dev_, 0, 8, st_), "memset");
+      CK(checksum_bf16(t.ptr, t.n, cksum_dev_, st_), "checksum");
+      unsigned long long v = 0;
+      CK(cudaMemcpyAsync(&v, cksum_dev_, 8, cudaMemcpyDeviceToHost, st_), "checksum d2h");
+      CK(cudaStreamSynchronize(st_), "checksum sync");
+      *out = v;
+      return SGS_OK;
+    }
+  err = "unknown tensor id";
+  return SGS_E_INVAL;
+}
+
+// ------------------------------------------------------------------ submit
+sgs_status Engine::submit(const sgs_prompt* prompts, int32_t n, const int32_t* hint, const int32_t* forced,
+                          int32_t* n_mine) {
+  if (poisoned) {
+    err = "handle poisoned by an earlier error";
+    return SGS_E_STATE;
+  }
+  if (n < 0 || (n > 0 && (!prompts || !hint || !forced))) {
+    err = "null arrays";
+    return SGS_E_INVAL;
+  }
+  std::vector<uint64_t> ids(n);
+  std::vector<int32_t> P(n);
+  for (int i = 0; i < n; ++i) {
+    const sgs_prompt& p = prompts[i];
+    if (p.len < 1 || !p.tokens || hint[i] < 1 || forced[i] < 1) {
+      err = "prompt length, hint and forced length must be >= 1";
+      return SGS_E_INVAL;
+    }
+    for (int j = 0; j < p.len; ++j)
+      if (p.tokens[j] < 0 || p.tokens[j] >= m_.vocab) {
+        err = "token id out of range";
+        return SGS_E_INVAL;
+      }
+    ids[i] = p.id;
+    P[i] = p.len;
+  }
+  {
+    std::vector<uint64_t> s(ids);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end()) {
+      err = "duplicate ids in batch";
+      return SGS_E_INVAL;
+    }
+    for (uint64_t id : s)
+      if (std::binary_search(seen_ids_.begin(), seen_ids_.end(), id)) {
+        err = "id already submitted to this handle";
+        return SGS_E_INVAL;
+      }
+  }
+  for (int i = 0; i < n; ++i) {
+    const int64_t need = ((int64_t)P[i] + forced[i] - 1 + e_.page_size - 1) / e_.page_size;
+    if ((int64_t)P[i] + forced[i] - 1 > e_.max_ctx || need > n_pages_ ||
+        (!null_ && P[i] > e_.max_prefill_tokens)) {
+      err = "sample can never fit (max_ctx, page pool or prefill chunk)";
+      return SGS_E_CAPACITY;
+    }
+  }
+  // Alg. 2 dispatch, identical on every instance (no communication)
+  std::vector<int32_t> inst(n, 0);
+  DispatchCfg dc{e_.n_instances, e_.max_batch, e_.page_size, n_pages_, e_.profile.t0_ns, e_.profile.k0_ps,
+                 e_.profile.b_star, e_.profile.k1_ps, e_.alpha_pct, e_.score, e_.tail_ceil, e_.dispatch,
+                 e_.sample_seed + (uint64_t)batch_counter_};
+  dispatch_alg2(dc, n, ids.data(), P.data(), hint, inst.data());
+  std::vector<Sample> mine;
+  for (int i = 0; i < n; ++i) {
+    if (inst[i] != e_.instance_rank) continue;
+    Sample s;
+    s.id = ids[i];
+    s.P = P[i];
+    s.d = forced[i];
+    s.hint = hint[i];
+    s.batch = batch_counter_;
+    s.tok_off = (int64_t)prompt_store_.size();
+    prompt_store_.insert(prompt_store_.end(), prompts[i].tokens, prompts[i].tokens + P[i]);
+    mine.push_back(std::move(s));
+  }
+  for (uint64_t id : ids) seen_ids_.push_back(id);
+  std::sort(seen_ids_.begin(), seen_ids_.end());
+  if (n_mine) *n_mine = (int32_t)mine.size();
+  sched.submit(std::move(mine));
+  ++batch_counter_;
+  return SGS_OK;
+}
+
+// ------------------------------------------------------------------ step
+sgs_status Engine::step(sgs_completion* out, int32_t cap, int32_t* n_out) {
+  *n_out = 0;
+  if (poisoned) {
+    err = "handle poisoned by an earlier error";
+    return SGS_E_STATE;
+  }
+  handed_.clear();
+  if (ready_.empty()) {
+    IterPlan plan;
+    bool ran;
+    try {
+      ran = sched.plan(&plan);
+    } catch (const std::exception& ex) {
+      err = ex.what();
+      poisoned = true;
+      return SGS_E_STATE;
+    }
+    if (ran) {
+      sgs_status s = run_iteration(plan);
+      if (s != SGS_OK) return s;
+    }
+  }
+  int k = 0;
+  while (k < cap && !ready_.empty()) {
+    handed_.push_back(std::move(ready_.front()));
+    ready_.pop_front();
+    ++k;
+  }
+  for (int i = 0; i < k; ++i) {
+    const Completion& c = handed_[i];
+    out[i].id = c.id;
+    out[i].instance = e_.instance_rank;
+    out[i].n_tokens = (int32_t)c.tokens.size();
+    out[i].tokens = c.tokens.data();
+    out[i].admit_iter = c.admit_iter;
+    out[i].finish_iter = c.finish_iter;
+    out[i].weight_version = c.version;
+    out[i].slot = c.slot;
+  }
+  *n_out = k;
+  return SGS_OK;
+}
+
+cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate) {
+  const int splits = gemm_auto_splits(N, K, T);
+  cudaError_t e;
+  if (splits > 1) {
+    if (!accumulate) {
+      e = cudaMemsetAsync(C, 0, (size_t)T * N * 4, st_);
+      if (e != cudaSuccess) return e;
+    }
+    e = gemm_bf16(W, X, C, N, K, T, N, 1, splits, st_);
+  } else {
+    e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_);
+  }
+  ++launches;
+  return e;
+}
+
+sgs_status Engine::run_iteration(const IterPlan& plan) {
+  auto& S = sched.samples();
+  const int n_adm = (int)plan.admitted.size();
+  const int n_run = (int)plan.running.size();
+  if (null_) {
+    for (int32_t i : plan.completed) {
+      const Sample& s = S[i];
+      Completion c{s.id, s.slot, s.admit_iter, s.finish_iter, version, std::vector<int32_t>(s.d, 0)};
+      ready_.push_back(std::move(c));
+    }
+    return SGS_OK;
+  }
+  const int d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn,
+            V = m_.vocab;
+  const int qkvN = (nq + 2 * nkv) * hd;
+  // ---------------- stage metadata (host, pinned) -> one H2D copy
+  std::vector<int32_t> meta;
+  meta.reserve(4096);
+  auto put = [&](const int32_t* p, size_t n) {
+    const size_t at = meta.size();
+    meta.insert(meta.end(), p, p + n);
+    return at;
+  };
+  const size_t o_bt = put(plan.bt_deltas.data(), plan.bt_deltas.size());
+  const int n_bt = (int)plan.bt_deltas.size() / 3;
+  // prefill chunks
+  struct Chunk {
+    std::vector<int32_t> idx;
+    int T = 0, nqb = 0, row_base = 0;
+    size_t o_tok, o_pos, o_slot, o_offs, o_qb, o_last, o_pfslot, o_pftok;
+  };
+  std::vector<Chunk> chunks;
+  {
+    Chunk cur;
+    for (int32_t i : plan.admitted) {
+      if (cur.T > 0 && cur.T + S[i].P > e_.max_prefill_tokens) {
+        chunks.push_back(cur);
+        cur = Chunk();
+      }
+      cur.idx.push_back(i);
+      cur.T += S[i].P;
+    }
+    if (!cur.idx.empty()) chunks.push_back(cur);
+  }
+  int row_base = 0;
+  for (auto& c : chunks) {
+    std::vector<int32_t> tok, pos, slot, offs(1, 0), qb, last, pfs, pft;
+    for (size_t k = 0; k < c.idx.size(); ++k) {
+      const Sample& s = S[c.idx[k]];
+      tok.insert(tok.end(), prompt_store_.begin() + s.tok_off, prompt_store_.begin() + s.tok_off + s.P);
+      for (int j = 0; j < s.P; ++j) pos.push_back(j), slot.push_back(s.slot);
+      offs.push_back(offs.back() + s.P);
+      for (int b = 0; b < (s.P + 63) / 64; ++b) qb.push_back((int32_t)k), qb.push_back(b);
+      last.push_back(offs.back() - 1);
+      pfs.push_back(s.slot);
+      pft.push_back(0);
+    }
+    c.o_tok = put(tok.data(), tok.size());
+    c.o_pos = put(pos.data(), pos.size());
+    c.o_slot = put(slot.data(), slot.size());
+    c.o_offs = put(offs.data(), offs.size());
+    c.o_qb = put(qb.data(), qb.size());
+    c.nqb = (int)qb.size() / 2;
+    c.o_last = put(last.data(), last.size());
+    c.o_pfslot = put(pfs.data(), pfs.size());
+    c.o_pftok = put(pft.data(), pft.size());
+    c.row_base = row_base;
+    row_base += (int)c.idx.size();
+  }
+  // decode rows (ascending slot)
+  std::vector<int32_t> dslot, dpos, dctx, dtok;
+  for (int32_t i : plan.running) {
+    const Sample& s = S[i];
+    const int j = s.produced - 1;  // tokens generated before this iteration (plan already counted this one)
+    dslot.push_back(s.slot);
+    dpos.push_back(s.P + j - 1);
+    dctx.push_back(s.P + j);
+    dtok.push_back(j);
+  }
+  const size_t o_dslot = put(dslot.data(), dslot.size());
+  const size_t o_dpos = put(dpos.data(), dpos.size());
+  const size_t o_dctx = put(dctx.data(), dctx.size());
+  const size_t o_dtok = put(dtok.data(), dtok.size());
+  AttnPlan ap;
+  attn_plan(dctx.data(), n_run, nkv, e_.page_size, 0, &ap);
+  if ((int)ap.items.size() > L_.max_items || ap.n_parts > L_.max_items) {
+    err = "attention work list exceeds workspace";
+    poisoned = true;
+    return SGS_E_NOMEM;
+  }
+  while (meta.size() % 4) meta.push_back(0);
+  const size_t o_items = put(reinterpret_cast<const int32_t*>(ap.items.data()), ap.items.size() * 5);
+  const size_t o_combs = put(reinterpret_cast<const int32_t*>(ap.combs.data()), ap.combs.size() * 4);
+  if ((int64_t)meta.size() * 4 > L_.meta_bytes) {
+    err = "iteration metadata exceeds the staging buffer";
+    poisoned = true;
+    return SGS_E_NOMEM;
+  }
+  std::memcpy(meta_host_, meta.data(), meta.size() * 4);
+  const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_);
+  CK(cudaEventRecord(ev0_, st_), "event");
+  CK(cudaMemcpyAsync(meta_dev_, meta_host_, meta.size() * 4, cudaMemcpyHostToDevice, st_), "meta H2D");
+  CK(apply_bt_deltas(bt_, L_.max_pages, MD + o_bt, n_bt, st_), "bt deltas");
+  ++launches;
+
+  // ---------------- prefill
+  for (auto& c : chunks) {
+    sgs_status s = prefill_chunk(c.idx, c.row_base, MD + c.o_tok, MD + c.o_pos, MD + c.o_slot, MD + c.o_offs,
+                                 MD + c.o_qb, c.nqb, MD + c.o_last, MD + c.o_pfslot, MD + c.o_pftok, c.T);
+    if (s != SGS_OK) return s;
+  }
+  // ---------------- decode
+  if (n_run > 0) {
+    const int b = n_run;
+    const int32_t* d_slot = MD + o_dslot;
+    const int32_t* d_pos = MD + o_dpos;
+    const int32_t* d_ctx = MD + o_dctx;
+    const AttnItem* d_items = reinterpret_cast<const AttnItem*>(MD + o_items);
+    const AttnComb* d_combs = reinterpret_cast<const AttnComb*>(MD + o_combs);
+    float* part_o = reinterpret_cast<float*>(attn_ws_);
+    float* part_ml = part_o + (size_t)std::max(ap.n_parts, 1) * (nq / nkv) * hd;
+    CK(embed(embed_, nullptr, d_slot, last_tok_, h_, b, d, st_), "embed");
+    ++launches;
+    for (int l = 0; l < m_.n_layers; ++l) {
+      const Layer& Ly = layers_[l];
+      CK(rmsnorm(h_, Ly.n1, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm1");
+      CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, b, false), "gemm qkv");
+      CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, b, nq,
+                     nkv, hd, e_.page_size, st_),
+         "rope_append");
+      CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_items, (int)ap.items.size(), d_combs, (int)ap.combs.size(), nq,
+                     nkv, hd, e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, st_),
+         "attn_decode");
+      CK(gemm(Ly.wo, ao_, h_, d, nq * hd, b, true), "gemm o");
+      CK(rmsnorm(h_, Ly.n2, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm2");
+      CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, b, false), "gemm gate_up");
+      CK(silu_mul(gu_, mm_, b, f, st_), "silu");
+      CK(gemm(Ly.wd, mm_, h_, d, f, b, true), "gemm down");
+      launches += 5 + (ap.combs.empty() ? 0 : 1);
+    }
+    CK(rmsnorm(h_, nf_, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm f");
+    float* lg = logits_ + (size_t)row_base * V;
+    CK(gemm(lm_head_, x_, lg, V, d, b, false), "gemm lm_head");
+    CK(argmax_rows(lg, b, V, nullptr, d_slot, MD + o_dtok, last_tok_, hist_, max_gen_, st_), "argmax");
+    launches += 2;
+  }
+  // ---------------- completions: D2H of their tokens
+  int64_t off = 0;
+  std::vector<int64_t> toff;
+  for (int32_t i : plan.completed) {
+    const Sample& s = S[i];
+    if (off + s.d > tok_host_cap_) {
+      err = "token staging overflow";
+      poisoned = true;
+      return SGS_E_NOMEM;
+    }
+    CK(cudaMemcpyAsync(tok_host_ + off, hist_ + (size_t)s.slot * max_gen_, (size_t)s.d * 4, cudaMemcpyDeviceToHost,
+                       st_),
+       "tokens D2H");
+    toff.push_back(off);
+    off += s.d;
+  }
+  const int rows = row_base + n_run;
+  if (e_.flags & SGS_F_KEEP_LOGITS) {
+    kept_logits_.resize((size_t)rows * V);
+    if (rows) CK(cudaMemcpyAsync(kept_logits_.data(), logits_, (size_t)rows * V * 4, cudaMemcpyDeviceToHost, st_),
+                 "logits D2H");
+    kept_ids_.clear();
+    kept_tok_.clear();
+    for (auto& c : chunks)
+      for (int32_t i : c.idx) kept_ids_.push_back(S[i].id), kept_tok_.push_back(0);
+    for (int32_t i : plan.running) kept_ids_.push_back(S[i].id), kept_tok_.push_back(S[i].produced - 1);
+  }
+  CK(cudaEventRecord(ev1_, st_), "event");
+  CK(cudaStreamSynchronize(st_), "iteration sync");
+  CK(cudaEventElapsedTime(&last_ms, ev0_, ev1_), "elapsed");
+  for (size_t k = 0; k < plan.completed.size(); ++k) {
+    const Sample& s = S[plan.completed[k]];
+    Completion c{s.id, s.slot, s.admit_iter, s.finish_iter, version,
+                 std::vector<int32_t>(tok_host_ + toff[k], tok_host_ + toff[k] + s.d)};
+    ready_.push_back(std::move(c));
+  }
+  (void)n_adm;
+  return SGS_OK;
+}
+
+sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, const int32_t* d_tokens,
+                                 const int32_t* d_pos, const int32_t* d_slot, const int32_t* d_offs,
+                                 const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
+                                 const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T) {
+  const int d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn,
+            V = m_.vocab;
+  const int qkvN = (nq + 2 * nkv) * hd;
+  const int np = (int)idx.size();
+  CK(embed(embed_, d_tokens, nullptr, nullptr, h_, T, d, st_), "embed");
+  ++launches;
+  for (int l = 0; l < m_.n_layers; ++l) {
+    const Layer& Ly = layers_[l];
+    CK(rmsnorm(h_, Ly.n1, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm1");
+    CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, T, false), "gemm qkv");
+    CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, kc_, vc_, T, nq, nkv, hd,
+                   e_.page_size, st_),
+       "rope_append");
+    CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
+    CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
+    CK(rmsnorm(h_, Ly.n2, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm2");
+    CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, T, false), "gemm gate_up");
+    CK(silu_mul(gu_, mm_, T, f, st_), "silu");
+    CK(gemm(Ly.wd, mm_, h_, d, f, T, true), "gemm down");
+    launches += 5;
+  }
+  CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
+  float* lg = logits_ + (size_t)row_base * V;
+  CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
+  CK(argmax_rows(lg, np, V, nullptr, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, st_), "argmax");
+  launches += 2;
+  return SGS_OK;
+}
+
+sgs_status Engine::last_logits(float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap, int32_t* rows) {
+  const int n = (int)kept_ids_.size();
+  *rows = n;
+  if (!logits) return SGS_OK;
+  const int k = std::min(n, cap);
+  std::memcpy(logits, kept_logits_.data(), (size_t)k * m_.vocab * 4);
+  for (int i = 0; i < k; ++i) ids[i] = kept_ids_[i], tok_idx[i] = kept_tok_[i];
+  return SGS_OK;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen: the process's libnccl.so.2)
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+  bool ok = false;
+};
+
+static NcclApi* nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api.ok ? &api : nullptr;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.Broadcast && api.GroupStart && api.GroupEnd;
+  return api.ok ? &api : nullptr;
+}
+
+sgs_status Engine::comm_init(const uint8_t id[128], int rank, int world) {
+  if (null_) {
+    err = "no device";
+    return SGS_E_STATE;
+  }
+  NcclApi* api = nccl();
+  if (!api) {
+    err = "libnccl.so.2 not found";
+    return SGS_E_NCCL;
+  }
+  ncclUniqueId uid;
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl unique id size");
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm;
+  ncclResult_t r = api->CommInitRank(&comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    err = std::string("ncclCommInitRank: ") + api->GetErrorString(r);
+    return SGS_E_NCCL;
+  }
+  nccl_comm_ = comm;
+  nccl_rank_ = rank;
+  nccl_world_ = world;
+  return SGS_OK;
+}
+
+sgs_status Engine::update_weights(int root) {
+  if (poisoned) {
+    err = "handle poisoned";
+    return SGS_E_STATE;
+  }
+  if (!sched.idle()) {
+    err = "weight update with samples in flight";
+    return SGS_E_STATE;
+  }
+  if (null_) {
+    ++version;
+    return SGS_OK;
+  }
+  if (nccl_world_ > 1) {
+    if (!nccl_comm_) {
+      err = "sgs_comm_init not called";
+      return SGS_E_STATE;
+    }
+    NcclApi* api = nccl();
+    // the weights are one contiguous range at the arena start; broadcast in 256 MiB chunks
+    const size_t total = (size_t)L_.weights_bytes;
+    const size_t chunk = 256ull << 20;
+    api->GroupStart();
+    for (size_t o = 0; o < total; o += chunk) {
+      const size_t n = std::min(chunk, total - o);
+      ncclResult_t r = api->Broadcast(arena_ + o, arena_ + o, n, ncclUint8, root, (ncclComm_t)nccl_comm_, st_);
+      if (r != ncclSuccess) {
+        api->GroupEnd();
+        err = std::string("ncclBroadcast: ") + api->GetErrorString(r);
+        poisoned = true;
+        return SGS_E_NCCL;
+      }
+    }
+    ncclResult_t r = api->GroupEnd();
+    if (r != ncclSuccess) {
+      err = std::string("ncclGroupEnd: ") + api->GetErrorString(r);
+      poisoned = true;
+      return SGS_E_NCCL;
+    }
+    CK(cudaStreamSynchronize(st_), "broadcast sync");
+  }
+  ++version;
+  return SGS_OK;
+}
+
+}  // namespace sgs
+
+// ------------------------------------------------------------------ sgs_rope_table / sgs_comm_unique_id
+extern "C" sgs_status sgs_rope_table(float* out, int32_t max_pos, int32_t hd, double theta) {
+  if (!out || max_pos <= 0 || hd <= 0 || hd % 2) return SGS_E_INVAL;
+  const int half = hd / 2;
+  for (int p = 0; p < max_pos; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double a = (double)p * std::pow(theta, -2.0 * i / (double)hd);
+      out[((size_t)p * half + i) * 2] = (float)std::cos(a);
+      out[((size_t)p * half + i) * 2 + 1] = (float)std::sin(a);
+    }
+  return SGS_OK;
+}
+
+extern "C" sgs_status sgs_comm_unique_id(uint8_t out[128]) {
+  sgs::NcclApi* api = sgs::nccl();
+  if (!api) return SGS_E_NCCL;
+  ncclUniqueId uid;
+  if (api->GetUniqueId(&uid) != ncclSuccess) return SGS_E_NCCL;
+  std::memcpy(out, &uid, 128);
+  return SGS_OK;
+}

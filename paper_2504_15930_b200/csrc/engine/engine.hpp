@@ -1,0 +1,116 @@
+// One generation instance: device arena (weights | KV pool | scratch), the
+// host scheduler, and the per-iteration device program (prefill of admitted
+// prompts + one decode step of the running samples).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../../include/sgs.h"
+#include "../host/sched.hpp"
+#include "../kernels/kernels.h"
+
+namespace sgs {
+
+struct TensorRef {
+  int64_t id;
+  void* ptr;
+  int64_t n;
+  int is_norm;
+};
+
+struct ArenaLayout {
+  int64_t weights_bytes = 0, kv_bytes = 0, scratch_bytes = 0, total = 0, kv_page_bytes = 0;
+  // offsets (bytes from arena start)
+  int64_t off_kv = 0, off_h = 0, off_x = 0, off_qkv = 0, off_q = 0, off_kc = 0, off_vc = 0, off_ao = 0,
+          off_gu = 0, off_mm = 0, off_logits = 0, off_rope = 0, off_bt = 0, off_last = 0, off_hist = 0,
+          off_meta = 0, off_attn = 0, off_cksum = 0;
+  int64_t meta_bytes = 0, attn_bytes = 0;
+  int tmax = 0, max_pages = 0, max_items = 0;
+};
+
+struct Completion {
+  uint64_t id;
+  int32_t slot;
+  int64_t admit_iter, finish_iter;
+  int32_t version;
+  std::vector<int32_t> tokens;
+};
+
+class Engine {
+ public:
+  ~Engine();
+  sgs_status init(const sgs_model_cfg& m, const sgs_engine_cfg& e);
+  sgs_status submit(const sgs_prompt* prompts, int32_t n, const int32_t* hint, const int32_t* forced,
+                    int32_t* n_mine);
+  sgs_status step(sgs_completion* out, int32_t cap, int32_t* n_out);
+  sgs_status load_weights_seed(uint64_t seed);
+  sgs_status checksum(int64_t tensor_id, uint64_t* out);
+  sgs_status comm_init(const uint8_t id[128], int rank, int world);
+  sgs_status update_weights(int root);
+  sgs_status last_logits(float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap, int32_t* rows);
+
+  static sgs_status layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64_t n_pages, ArenaLayout* L);
+
+  std::string err;
+  bool poisoned = false;
+  Scheduler sched;
+  float last_ms = 0.f;
+  int64_t launches = 0;
+  int32_t version = 0;
+
+ private:
+  sgs_status cuda_fail(cudaError_t e, const char* what);
+  sgs_status run_iteration(const IterPlan& plan);
+  sgs_status prefill_chunk(const std::vector<int32_t>& idx, int row_base, const int32_t* d_tokens,
+                           const int32_t* d_pos, const int32_t* d_slot, const int32_t* d_offs,
+                           const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
+                           const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T);
+  cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
+  void build_tensor_table();
+
+  sgs_model_cfg m_{};
+  sgs_engine_cfg e_{};
+  bool null_ = true;
+  cudaStream_t st_ = nullptr;
+  ArenaLayout L_{};
+  uint8_t* arena_ = nullptr;
+  int64_t n_pages_ = 0;
+  int max_gen_ = 0;
+  // weights
+  struct Layer {
+    void *wqkv, *bqkv, *wo, *wgu, *wd, *n1, *n2;
+    void* kv;
+  };
+  std::vector<Layer> layers_;
+  void *embed_ = nullptr, *lm_head_ = nullptr, *nf_ = nullptr;
+  std::vector<TensorRef> tensors_;
+  // scratch
+  float *h_ = nullptr, *qkv_ = nullptr, *gu_ = nullptr, *logits_ = nullptr, *rope_ = nullptr;
+  void *x_ = nullptr, *q_ = nullptr, *kc_ = nullptr, *vc_ = nullptr, *ao_ = nullptr, *mm_ = nullptr;
+  int32_t *bt_ = nullptr, *last_tok_ = nullptr, *hist_ = nullptr;
+  uint8_t* meta_dev_ = nullptr;
+  uint8_t* meta_host_ = nullptr;  // pinned
+  uint8_t* attn_ws_ = nullptr;
+  unsigned long long* cksum_dev_ = nullptr;
+  int32_t* tok_host_ = nullptr;  // pinned, completed tokens
+  int64_t tok_host_cap_ = 0;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  // prompts (host)
+  std::vector<int32_t> prompt_store_;
+  std::vector<uint64_t> seen_ids_;
+  int batch_counter_ = 0;
+  std::deque<Completion> ready_;
+  std::vector<Completion> handed_;  // storage for the completions returned by the last step
+  // logits kept for tests
+  std::vector<float> kept_logits_;
+  std::vector<uint64_t> kept_ids_;
+  std::vector<int32_t> kept_tok_;
+  // nccl
+  void* nccl_comm_ = nullptr;
+  int nccl_rank_ = -1, nccl_world_ = 0;
+};
+
+}  // namespace sgs

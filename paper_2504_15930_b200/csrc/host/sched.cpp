@@ -1,0 +1,330 @@
+// Host control plane: page allocator, longest-first scheduler, Alg. 2, T(b) fit.
+//
+// Scheduler semantics (P = PAPER.md):
+//  * order: RL batches FIFO; within a batch by ranker hint descending, id
+//    ascending — "samples are assigned to the batch in descending order of
+//    their estimated output lengths. Once a sample is completed, the sample
+//    with the longest remaining output length is added";
+//  * refill: free slots (lowest index first) are filled from the queue head
+//    while active < B and the head's page reservation ceil((P+d-1)/page)
+//    fits the pool (BS "constrained by the GPU memory capacity");
+//    strict order, no backfill;
+//  * every active sample produces one token per iteration (prefill counts as
+//    the first) and completes after exactly d tokens (forced lengths,
+//    P:1105-1110); completions stream out in ascending id.
+#include "sched.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+
+namespace sgs {
+
+// ------------------------------------------------------------------ PageAllocator
+void PageAllocator::reset(int64_t n) {
+  n_ = n;
+  n_free_ = n;
+  words_.assign((size_t)((n + 63) / 64), ~0ull);
+  if (n % 64) words_.back() = (1ull << (n % 64)) - 1;
+  if (n == 0) words_.clear();
+  summary_.assign((words_.size() + 63) / 64, 0ull);
+  for (size_t w = 0; w < words_.size(); ++w)
+    if (words_[w]) summary_[w / 64] |= 1ull << (w % 64);
+}
+
+int64_t PageAllocator::alloc() {
+  for (size_t s = 0; s < summary_.size(); ++s) {
+    if (!summary_[s]) continue;
+    const size_t w = s * 64 + (size_t)__builtin_ctzll(summary_[s]);
+    const int bit = __builtin_ctzll(words_[w]);
+    words_[w] &= words_[w] - 1;
+    if (!words_[w]) summary_[s] &= ~(1ull << (w % 64));
+    --n_free_;
+    return (int64_t)w * 64 + bit;
+  }
+  return -1;
+}
+
+void PageAllocator::free(int64_t p) {
+  const size_t w = (size_t)(p / 64);
+  words_[w] |= 1ull << (p % 64);
+  summary_[w / 64] |= 1ull << (w % 64);
+  ++n_free_;
+}
+
+// ------------------------------------------------------------------ Scheduler
+void Scheduler::init(int max_batch, int page, int64_t n_pages) {
+  B_ = max_batch;
+  page_ = page;
+  pages_.reset(n_pages);
+  slot_of_.assign(max_batch, -1);
+}
+
+static inline int64_t reservation(const Sample& s, int page) { return ((int64_t)s.P + s.d - 1 + page - 1) / page; }
+
+void Scheduler::submit(std::vector<Sample>&& batch) {
+  const int32_t base = (int32_t)samples_.size();
+  std::vector<int32_t> idx(batch.size());
+  std::iota(idx.begin(), idx.end(), base);
+  for (auto& s : batch) samples_.push_back(std::move(s));
+  std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+    const Sample &x = samples_[a], &y = samples_[b];
+    if (x.hint != y.hint) return x.hint > y.hint;
+    return x.id < y.id;
+  });
+  queue_.insert(queue_.end(), idx.begin(), idx.end());
+}
+
+bool Scheduler::plan(IterPlan* p) {
+  p->admitted.clear();
+  p->running.clear();
+  p->completed.clear();
+  p->bt_deltas.clear();
+  p->alloc_log.clear();
+  p->free_log.clear();
+  if (idle()) return false;
+  p->t = t_;
+  // running samples are those active before admission
+  for (int s = 0; s < B_; ++s)
+    if (slot_of_[s] >= 0) p->running.push_back(slot_of_[s]);
+  // refill, strict longest-first
+  while (active_ < B_ && qhead_ < queue_.size()) {
+    const int32_t i = queue_[qhead_];
+    Sample& s = samples_[i];
+    const int64_t R = reservation(s, page_);
+    if (reserved_ + R > pages_.capacity()) break;
+    int slot = 0;
+    while (slot_of_[slot] >= 0) ++slot;
+    slot_of_[slot] = i;
+    s.slot = slot;
+    s.admit_iter = t_;
+    reserved_ += R;
+    ++active_;
+    ++qhead_;
+    p->admitted.push_back(i);
+    const int np = (s.P + page_ - 1) / page_;
+    for (int k = 0; k < np; ++k) {
+      const int64_t pg = pages_.alloc();
+      if (pg < 0) throw std::runtime_error("page pool exhausted (reservation invariant broken)");
+      s.pages.push_back((int32_t)pg);
+      p->alloc_log.push_back((int32_t)pg);
+      p->bt_deltas.insert(p->bt_deltas.end(), {slot, k, (int32_t)pg});
+    }
+  }
+  if (active_ == 0) throw std::runtime_error("queue head can never fit the page pool");
+  // running samples feed token j at position P + j - 1 (ascending slot)
+  int64_t sumctx = 0;
+  for (int32_t i : p->running) {
+    Sample& s = samples_[i];
+    const int64_t pos = (int64_t)s.P + s.produced - 1;
+    if (pos == (int64_t)s.pages.size() * page_) {
+      const int64_t pg = pages_.alloc();
+      if (pg < 0) throw std::runtime_error("page pool exhausted (reservation invariant broken)");
+      p->bt_deltas.insert(p->bt_deltas.end(), {s.slot, (int32_t)s.pages.size(), (int32_t)pg});
+      s.pages.push_back((int32_t)pg);
+      p->alloc_log.push_back((int32_t)pg);
+    }
+    sumctx += pos + 1;
+  }
+  for (int32_t i : p->admitted) sumctx += samples_[i].P;
+  p->sumctx = sumctx;
+  p->b = active_;
+  // every active sample produces one token; completions ascending id
+  for (int s = 0; s < B_; ++s) {
+    const int32_t i = slot_of_[s];
+    if (i < 0) continue;
+    Sample& x = samples_[i];
+    if (++x.produced == x.d) p->completed.push_back(i);
+  }
+  std::sort(p->completed.begin(), p->completed.end(),
+            [&](int32_t a, int32_t b) { return samples_[a].id < samples_[b].id; });
+  for (int32_t i : p->completed) {
+    Sample& s = samples_[i];
+    s.finish_iter = t_;
+    for (int32_t pg : s.pages) {
+      pages_.free(pg);
+      p->free_log.push_back(pg);
+    }
+    slot_of_[s.slot] = -1;
+    reserved_ -= reservation(s, page_);
+    --active_;
+  }
+  if (tracing) {
+    auto& o = trace_iters;
+    o.push_back(t_);
+    o.push_back(p->b);
+    o.push_back(p->sumctx);
+    o.push_back((int64_t)p->admitted.size());
+    o.push_back((int64_t)p->completed.size());
+    o.push_back((int64_t)p->alloc_log.size());
+    o.push_back((int64_t)p->free_log.size());
+    for (int32_t i : p->admitted) o.push_back((int64_t)samples_[i].id);
+    for (int32_t i : p->completed) o.push_back((int64_t)samples_[i].id);
+    for (int32_t pg : p->alloc_log) o.push_back(pg);
+    for (int32_t pg : p->free_log) o.push_back(pg);
+  }
+  ++t_;
+  return true;
+}
+
+void Scheduler::sample_trace(std::vector<int64_t>* out) const {
+  std::vector<int32_t> idx;
+  for (int32_t i = 0; i < (int32_t)samples_.size(); ++i)
+    if (samples_[i].admit_iter >= 0) idx.push_back(i);
+  std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return samples_[a].id < samples_[b].id; });
+  for (int32_t i : idx) {
+    const Sample& s = samples_[i];
+    out->push_back((int64_t)s.id);
+    out->push_back(s.slot);
+    out->push_back(s.admit_iter);
+    out->push_back(s.finish_iter);
+    out->push_back((int64_t)s.pages.size());
+    for (int32_t pg : s.pages) out->push_back(pg);
+  }
+}
+
+// ------------------------------------------------------------------ Alg. 2
+// T(b) in picoseconds from the integer profile (appendix, continuity P:49).
+static __int128 tb_ps(const DispatchCfg& c, int64_t b) {
+  const __int128 base = (__int128)c.t0_ns * 1000;
+  if (b < c.b_star) return base + (__int128)c.k0_ps * b;
+  return base + (__int128)c.k0_ps * c.b_star + (__int128)c.k1_ps * (b - c.b_star);
+}
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Eq. 2: PTL(BS) * L * ceil(M / BS), BS memory-capped.
+static __int128 eq2(const DispatchCfg& c, int64_t members, int64_t L, int64_t instances, int64_t pbar) {
+  if (members <= 0) return 0;
+  const int64_t M = cdiv(members, instances);
+  const int64_t by_mem = c.pool_pages / cdiv(pbar + L - 1, c.page);
+  int64_t bs = std::min<int64_t>({M, (int64_t)c.B, by_mem});
+  if (bs < 1) bs = 1;
+  return tb_ps(c, bs) * L * cdiv(M, bs);
+}
+
+// nearest-rank percentile (ceil(q n)-th order statistic)
+static int64_t pct(std::vector<int64_t> v, int q) {
+  const int64_t n = (int64_t)v.size();
+  int64_t k = cdiv((int64_t)q * n, 100);
+  if (k < 1) k = 1;
+  std::nth_element(v.begin(), v.begin() + (k - 1), v.end());
+  return v[k - 1];
+}
+
+int dispatch_alg2(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P, const int32_t* hint,
+                  int32_t* instance) {
+  if (n <= 0) return 0;
+  std::vector<int32_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  if (c.policy == 2) {
+    // "prompts are typically assigned randomly": seeded permutation, round robin
+    uint64_t s = c.seed ? c.seed : 1;
+    for (int i = n - 1; i > 0; --i) {
+      s ^= s << 13, s ^= s >> 7, s ^= s << 17;
+      std::swap(order[i], order[(int)(s % (uint64_t)(i + 1))]);
+    }
+    for (int j = 0; j < n; ++j) instance[order[j]] = j % c.N;
+    return 0;
+  }
+  // Sort(P, L, descending), ties by id
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    if (hint[a] != hint[b]) return hint[a] > hint[b];
+    return ids[a] < ids[b];
+  });
+  if (c.policy == 1 || c.N == 1) {
+    for (int j = 0; j < n; ++j) instance[order[j]] = j % c.N;
+    return 0;
+  }
+  int64_t n_tail = c.tail_ceil ? cdiv((int64_t)c.alpha_pct * n, 100) : ((int64_t)c.alpha_pct * n) / 100;
+  n_tail = std::min<int64_t>(n_tail, n);
+  const int64_t n_reg = n - n_tail;
+  std::vector<int64_t> D(hint, hint + n);
+  const int64_t L_alpha = pct(D, 90), L_r = pct(D, 50);
+  int64_t sumP = 0;
+  for (int i = 0; i < n; ++i) sumP += P[i];
+  const int64_t pbar = cdiv(sumP, n);
+  int n_l;
+  if (n_tail == 0) {
+    n_l = 0;
+  } else if (n_reg == 0) {
+    n_l = c.N;
+  } else {
+    __int128 best = 0;
+    n_l = -1;
+    for (int nl = 1; nl < c.N; ++nl) {
+      const __int128 a = eq2(c, n_tail, L_alpha, nl, pbar);
+      const __int128 r = eq2(c, n_reg, L_r, c.N - nl, pbar);
+      const __int128 tot = c.score_max ? (a > r ? a : r) : a + r;
+      if (n_l < 0 || tot < best) best = tot, n_l = nl;
+    }
+  }
+  for (int j = 0; j < n; ++j) {
+    const int32_t i = order[j];
+    if (n_l == c.N || (n_l > 0 && j < n_tail))
+      instance[i] = j % n_l;
+    else {
+      const int64_t jr = n_l == 0 ? j : j - n_tail;
+      instance[i] = n_l + (int32_t)(jr % (c.N - n_l));
+    }
+  }
+  return n_l;
+}
+
+// ------------------------------------------------------------------ T(b) fit
+// Least squares on the hinge basis [1, b, (b - b*)+] for every measured b* with
+// >= 2 distinct points at or below and >= 1 above; minimum SSE wins, ties ->
+// smaller b*.  3x3 normal equations solved by Cramer's rule.
+static double det3(const double m[3][3]) {
+  return m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
+         m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]);
+}
+
+bool fit_tb(int n, const double* b, const double* T, double out[5], int64_t* b_star, int64_t prof[4]) {
+  std::vector<double> xs(b, b + n);
+  std::sort(xs.begin(), xs.end());
+  xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
+  bool have = false;
+  double best_sse = 0, bt0 = 0, bk0 = 0, bdk = 0, bbs = 0;
+  for (size_t ci = 0; ci < xs.size(); ++ci) {
+    const double bs = xs[ci];
+    const size_t left = ci + 1, right = xs.size() - ci - 1;
+    if (left < 2 || right < 1) continue;
+    double G[3][3] = {{0}}, r[3] = {0};
+    for (int i = 0; i < n; ++i) {
+      const double f[3] = {1.0, b[i], b[i] > bs ? b[i] - bs : 0.0};
+      for (int a = 0; a < 3; ++a) {
+        r[a] += f[a] * T[i];
+        for (int c = 0; c < 3; ++c) G[a][c] += f[a] * f[c];
+      }
+    }
+    const double D = det3(G);
+    if (std::fabs(D) < 1e-300) continue;
+    double beta[3];
+    for (int k = 0; k < 3; ++k) {
+      double Mk[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) Mk[a][c] = c == k ? r[a] : G[a][c];
+      beta[k] = det3(Mk) / D;
+    }
+    double sse = 0;
+    for (int i = 0; i < n; ++i) {
+      const double e = T[i] - beta[0] - beta[1] * b[i] - beta[2] * (b[i] > bs ? b[i] - bs : 0.0);
+      sse += e * e;
+    }
+    if (!have || sse < best_sse) {
+      have = true;
+      best_sse = sse, bt0 = beta[0], bk0 = beta[1], bdk = beta[2], bbs = bs;
+    }
+  }
+  if (!have) return false;
+  const double k1 = bk0 + bdk;
+  out[0] = bt0, out[1] = bk0, out[2] = k1, out[3] = bt0 + (bk0 - k1) * bbs, out[4] = best_sse;
+  *b_star = (int64_t)bbs;
+  prof[0] = std::llround(bt0), prof[1] = std::llround(bk0 * 1000.0), prof[2] = (int64_t)bbs,
+  prof[3] = std::llround(k1 * 1000.0);
+  return true;
+}
+
+}  // namespace sgs

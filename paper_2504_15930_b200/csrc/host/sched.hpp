@@ -1,0 +1,98 @@
+// Host-side control plane of one generation instance: paged-KV page
+// allocator, longest-first continuous-batching scheduler, Alg. 2 dispatcher
+// and the T(b) fit.  Pure C++ (no CUDA); the engine consumes IterPlan.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sgs {
+
+// ------------------------------------------------------------------ pages
+// Lowest-free-index page allocator over a two-level bitmap (R4).
+class PageAllocator {
+ public:
+  void reset(int64_t n_pages);
+  int64_t alloc();  // -1 when empty
+  void free(int64_t p);
+  int64_t n_free() const { return n_free_; }
+  int64_t capacity() const { return n_; }
+
+ private:
+  int64_t n_ = 0, n_free_ = 0;
+  std::vector<uint64_t> words_;    // bit = 1: page free
+  std::vector<uint64_t> summary_;  // bit = 1: word has a free page
+};
+
+// ------------------------------------------------------------------ samples
+struct Sample {
+  uint64_t id;
+  int32_t P, d, hint;
+  int32_t batch;
+  int64_t tok_off;  // offset of the prompt in the token store
+  // runtime
+  int32_t slot = -1;
+  int32_t produced = 0;
+  int64_t admit_iter = -1, finish_iter = -1;
+  std::vector<int32_t> pages;
+};
+
+struct IterPlan {
+  int64_t t = 0;
+  std::vector<int32_t> admitted;         // sample indices, admission order
+  std::vector<int32_t> running;          // sample indices decoding this iteration, ascending slot
+  std::vector<int32_t> completed;        // sample indices, ascending id
+  std::vector<int32_t> bt_deltas;        // (slot, page_idx, page) triples in allocation order
+  std::vector<int32_t> alloc_log, free_log;
+  int64_t sumctx = 0;
+  int32_t b = 0;
+};
+
+class Scheduler {
+ public:
+  void init(int max_batch, int page, int64_t n_pages);
+  // Append one RL batch (already restricted to this instance).
+  void submit(std::vector<Sample>&& batch);
+  bool idle() const { return active_ == 0 && qhead_ == queue_.size(); }
+  // Build the next iteration; returns false when idle (no iteration counted).
+  bool plan(IterPlan* p);
+  int64_t iterations() const { return t_; }
+  int64_t queued() const { return (int64_t)(queue_.size() - qhead_); }
+  int32_t active() const { return active_; }
+  std::vector<Sample>& samples() { return samples_; }
+  const std::vector<Sample>& samples() const { return samples_; }
+  int page() const { return page_; }
+  int64_t pool_pages() const { return pages_.capacity(); }
+  // trace (DESIGN.md §5 format)
+  std::vector<int64_t> trace_iters;
+  bool tracing = true;
+  void sample_trace(std::vector<int64_t>* out) const;
+
+ private:
+  int B_ = 0, page_ = 16;
+  PageAllocator pages_;
+  std::vector<Sample> samples_;   // all samples ever submitted (index = handle-local)
+  std::vector<int32_t> queue_;    // sample indices in admission order (FIFO by batch, LF within)
+  size_t qhead_ = 0;
+  std::vector<int32_t> slot_of_;  // slot -> sample index or -1
+  int64_t reserved_ = 0;
+  int32_t active_ = 0;
+  int64_t t_ = 0;
+};
+
+// ------------------------------------------------------------------ dispatch (Alg. 2)
+struct DispatchCfg {
+  int N, B, page;
+  int64_t pool_pages;
+  int64_t t0_ns, k0_ps, b_star, k1_ps;
+  int alpha_pct, score_max, tail_ceil, policy;  // policy: 0 skew, 1 round robin, 2 random
+  uint64_t seed;
+};
+// instance[i] for each sample i; returns N_l.
+int dispatch_alg2(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P, const int32_t* hint,
+                  int32_t* instance);
+
+// ------------------------------------------------------------------ T(b) fit
+bool fit_tb(int n, const double* b, const double* T_ns, double out[5], int64_t* b_star, int64_t prof[4]);
+
+}  // namespace sgs

@@ -1,0 +1,348 @@
+// a8 / K1+K2: paged GQA decode attention with split-K over KV pages.
+//
+//   o_h = softmax(q_h K^T / sqrt(hd)) V     over the ctx cached tokens of a sample
+//
+// Decode is memory-bandwidth bound (§2.2); every byte of the KV
+// cache is read once per layer.  One CTA = 4 warps handles one work item
+// (sample row, kv head, page range).  Each warp streams its own pages
+// (page, page+4, ...) through a private 3-stage shared-memory ring with 1-D
+// bulk copies (TMA unit, completion on an mbarrier): one page-head = K and V
+// of 16 tokens = 8 KB contiguous (hd = 128).  The g query heads of the group
+// are the M = 16 rows of mma.sync.m16n8k16 (rows >= g are zero): S = Q K^T in
+// bf16 with fp32 accumulation (ldmatrix from the XOR-swizzled page rows, bank
+// conflict free), online softmax in fp32 with exp2 and quad shuffles, then
+// O += P V with P in fp16 (V converted bf16 -> fp16 in registers) so the
+// softmax weights keep 11 mantissa bits (the 1e-3 target).
+// The 4 warps merge their (m, l, O) in shared memory; items that cover a
+// whole row write o directly, split items write fp32 partials that the
+// combine kernel merges with the log-sum-exp rule
+//   o = sum_j 2^(m_j - M) O_j / sum_j 2^(m_j - M) l_j.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sgs {
+
+constexpr int ATTN_WARPS = 4;
+constexpr int ATTN_STAGES = 3;
+constexpr int PAGE_T = 16;
+
+template <int HD>
+__global__ void __launch_bounds__(128, 2)
+    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv,
+                       const int32_t* __restrict__ bt, const int32_t* __restrict__ ctx,
+                       const AttnItem* __restrict__ items, int n_items, int nq, int nkv, int max_pages,
+                       float scale_log2, void* __restrict__ out, int out_fp32, float* __restrict__ part_o,
+                       float* __restrict__ part_ml) {
+  constexpr int RC = HD / 8;                 // 16-byte chunks per row
+  constexpr int HALF = PAGE_T * HD * 2;      // K (or V) bytes of one page-head
+  constexpr int STAGE = 2 * HALF;
+  constexpr int NT = HD / 8;                 // n8 tiles of the output
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bars[ATTN_WARPS][ATTN_STAGES];
+
+  if ((int)blockIdx.x >= n_items) return;
+  const AttnItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = nq / nkv;
+  const int L = ctx[it.row];
+  const int32_t* btr = bt + (size_t)it.row * max_pages;
+  uint8_t* my = smem + (size_t)warp * ATTN_STAGES * STAGE;
+
+  if (lane == 0) {
+    for (int s = 0; s < ATTN_STAGES; ++s) mbar_init(&bars[warp][s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int npages = it.p1 - it.p0;
+  const int n_my = npages > warp ? (npages - warp + ATTN_WARPS - 1) / ATTN_WARPS : 0;
+  auto issue = [&](int i) {
+    const int page = btr[it.p0 + warp + ATTN_WARPS * i];
+    const __nv_bfloat16* src = kv + ((size_t)page * nkv + it.kvh) * (size_t)(2 * PAGE_T * HD);
+    uint64_t* b = &bars[warp][i % ATTN_STAGES];
+    mbar_expect_tx(b, STAGE);
+    bulk_g2s(my + (size_t)(i % ATTN_STAGES) * STAGE, src, STAGE, b);
+  };
+  if (lane == 0)
+    for (int i = 0; i < n_my && i < ATTN_STAGES; ++i) issue(i);
+
+  // q fragments (A operand, rows = heads of the group)
+  const int r0 = lane >> 2, r1 = r0 + 8, cq = 2 * (lane & 3);
+  uint32_t qa[HD / 16][4];
+  {
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(q + ((size_t)it.row * nq + (size_t)it.kvh * g) * HD);
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      qa[kk][0] = r0 < g ? qrow[(r0 * HD + 16 * kk + cq) >> 1] : 0u;
+      qa[kk][1] = r1 < g ? qrow[(r1 * HD + 16 * kk + cq) >> 1] : 0u;
+      qa[kk][2] = r0 < g ? qrow[(r0 * HD + 16 * kk + 8 + cq) >> 1] : 0u;
+      qa[kk][3] = r1 < g ? qrow[(r1 * HD + 16 * kk + 8 + cq) >> 1] : 0u;
+    }
+  }
+  float o[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  // per-lane ldmatrix coordinates
+  const int ktok = ((lane >> 4) << 3) + (lane & 7);  // K: matrices (t0-7,lo)(t0-7,hi)(t8-15,lo)(t8-15,hi)
+  const int kchk = (lane >> 3) & 1;
+  const int vtok = (((lane >> 3) & 1) << 3) + (lane & 7);  // V: (t0-7,c)(t8-15,c)(t0-7,c+1)(t8-15,c+1)
+  const int vchk = lane >> 4;
+
+  for (int i = 0; i < n_my; ++i) {
+    const int s = i % ATTN_STAGES;
+    mbar_wait(&bars[warp][s], (i / ATTN_STAGES) & 1);
+    const uint32_t kbase = smem_u32(my + (size_t)s * STAGE);
+    const uint32_t vbase = kbase + HALF;
+    const int tok0 = (it.p0 + warp + ATTN_WARPS * i) * PAGE_T;
+
+    float sc[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int ch = 2 * kk + kchk;
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(b0, b1, b2, b3, kbase + ktok * (HD * 2) + ((ch ^ kv_swz(ktok, RC)) << 4));
+      mma_bf16_16816(sc[0], qa[kk], b0, b1);
+      mma_bf16_16816(sc[1], qa[kk], b2, b3);
+    }
+    // mask tokens beyond the context (only the last page is partial)
+    if (tok0 + PAGE_T > L) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (tok0 + 8 * t + cq + (e & 1) >= L) sc[t][e] = -INFINITY;
+    }
+    // online softmax (base 2, scores pre-scaled by log2(e)/sqrt(hd))
+    float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])) * scale_log2;
+    float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3])) * scale_log2;
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float a0 = exp2f(m0 - mn0), a1 = exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    uint32_t pa[4];
+    {
+      float p[2][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        p[t][0] = exp2f(fmaf(sc[t][0], scale_log2, -mn0));
+        p[t][1] = exp2f(fmaf(sc[t][1], scale_log2, -mn0));
+        p[t][2] = exp2f(fmaf(sc[t][2], scale_log2, -mn1));
+        p[t][3] = exp2f(fmaf(sc[t][3], scale_log2, -mn1));
+      }
+      pa[0] = pack_f16x2(p[0][0], p[0][1]);
+      pa[1] = pack_f16x2(p[0][2], p[0][3]);
+      pa[2] = pack_f16x2(p[1][0], p[1][1]);
+      pa[3] = pack_f16x2(p[1][2], p[1][3]);
+      // l accumulates the fp16-rounded weights actually used by the PV product
+      const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&pa[0]));
+      const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&pa[1]));
+      const float2 f2 = __half22float2(*reinterpret_cast<__half2*>(&pa[2]));
+      const float2 f3 = __half22float2(*reinterpret_cast<__half2*>(&pa[3]));
+      l0 = l0 * a0 + (f0.x + f0.y + f2.x + f2.y);
+      l1 = l1 * a1 + (f1.x + f1.y + f3.x + f3.y);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      o[nt][0] *= a0;
+      o[nt][1] *= a0;
+      o[nt][2] *= a1;
+      o[nt][3] *= a1;
+    }
+#pragma unroll
+    for (int nn = 0; nn < HD / 16; ++nn) {
+      const int ch = 2 * nn + vchk;
+      uint32_t v0, v1, v2, v3;
+      ldmatrix_x4_trans(v0, v1, v2, v3, vbase + vtok * (HD * 2) + ((ch ^ kv_swz(vtok, RC)) << 4));
+      mma_f16_16816(o[2 * nn], pa, bf16x2_to_f16x2(v0), bf16x2_to_f16x2(v1));
+      mma_f16_16816(o[2 * nn + 1], pa, bf16x2_to_f16x2(v2), bf16x2_to_f16x2(v3));
+    }
+    __syncwarp();
+    if (lane == 0 && i + ATTN_STAGES < n_my) {
+      fence_proxy_async_smem();
+      issue(i + ATTN_STAGES);
+    }
+  }
+  // quad-reduce the partial row sums
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+
+  // ---- merge the 4 warps through shared memory (stage buffers are idle now)
+  __syncthreads();
+  float* sO = reinterpret_cast<float*>(smem);                 // [4][16][HD]
+  float* sM = sO + ATTN_WARPS * 16 * HD;                       // [4][16]
+  float* sL = sM + ATTN_WARPS * 16;                            // [4][16]
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    sO[(warp * 16 + r0) * HD + 8 * nt + cq] = o[nt][0];
+    sO[(warp * 16 + r0) * HD + 8 * nt + cq + 1] = o[nt][1];
+    sO[(warp * 16 + r1) * HD + 8 * nt + cq] = o[nt][2];
+    sO[(warp * 16 + r1) * HD + 8 * nt + cq + 1] = o[nt][3];
+  }
+  if ((lane & 3) == 0) {
+    sM[warp * 16 + r0] = m0;
+    sM[warp * 16 + r1] = m1;
+    sL[warp * 16 + r0] = l0;
+    sL[warp * 16 + r1] = l1;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < g * HD; idx += blockDim.x) {
+    const int r = idx / HD, e = idx % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < ATTN_WARPS; ++w) M = fmaxf(M, sM[w * 16 + r]);
+    float so = 0.f, sl = 0.f;
+#pragma unroll
+    for (int w = 0; w < ATTN_WARPS; ++w) {
+      const float f = exp2f(sM[w * 16 + r] - M);  // empty warps: 2^-inf = 0
+      so += f * sO[(w * 16 + r) * HD + e];
+      sl += f * sL[w * 16 + r];
+    }
+    if (it.part < 0) {
+      const size_t oi = ((size_t)it.row * nq + (size_t)it.kvh * g + r) * HD + e;
+      const float v = so / sl;
+      if (out_fp32)
+        reinterpret_cast<float*>(out)[oi] = v;
+      else
+        reinterpret_cast<__nv_bfloat16*>(out)[oi] = __float2bfloat16_rn(v);
+    } else {
+      part_o[((size_t)it.part * g + r) * HD + e] = so;
+      if (e == 0) {
+        part_ml[((size_t)it.part * g + r) * 2 + 0] = M;
+        part_ml[((size_t)it.part * g + r) * 2 + 1] = sl;
+      }
+    }
+  }
+}
+
+__global__ void attn_combine_kernel(const AttnComb* __restrict__ combs, int n_combs, int nq, int nkv, int hd,
+                                    const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                    void* __restrict__ out, int out_fp32) {
+  if ((int)blockIdx.x >= n_combs) return;
+  const AttnComb c = combs[blockIdx.x];
+  const int g = nq / nkv;
+  for (int idx = threadIdx.x; idx < g * hd; idx += blockDim.x) {
+    const int r = idx / hd, e = idx % hd;
+    float M = -INFINITY;
+    for (int j = 0; j < c.nparts; ++j) M = fmaxf(M, part_ml[((size_t)(c.part0 + j) * g + r) * 2]);
+    float so = 0.f, sl = 0.f;
+    for (int j = 0; j < c.nparts; ++j) {
+      const size_t pj = (size_t)(c.part0 + j) * g + r;
+      const float f = exp2f(part_ml[pj * 2] - M);
+      so += f * part_o[pj * hd + e];
+      sl += f * part_ml[pj * 2 + 1];
+    }
+    const size_t oi = ((size_t)c.row * nq + (size_t)c.kvh * g + r) * hd + e;
+    const float v = so / sl;
+    if (out_fp32)
+      reinterpret_cast<float*>(out)[oi] = v;
+    else
+      reinterpret_cast<__nv_bfloat16*>(out)[oi] = __float2bfloat16_rn(v);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, AttnPlan* plan) {
+  plan->items.clear();
+  plan->combs.clear();
+  plan->n_parts = 0;
+  int64_t total = 0;
+  for (int i = 0; i < b; ++i) total += (int64_t)((ctx[i] + page - 1) / page) * nkv;
+  int chunk = split_pages;
+  if (chunk <= 0) {
+    // aim for ~2 waves of 2 CTAs per SM (148 SMs); at least one page per warp
+    const int64_t target = 2 * 2 * 148;
+    chunk = (int)std::max<int64_t>(ATTN_WARPS, (total + target - 1) / target);
+  }
+  for (int i = 0; i < b; ++i) {
+    const int np = (ctx[i] + page - 1) / page;
+    if (np == 0) continue;
+    const int nch = (np + chunk - 1) / chunk;
+    for (int h = 0; h < nkv; ++h) {
+      if (nch == 1) {
+        plan->items.push_back(AttnItem{i, h, 0, np, -1});
+        continue;
+      }
+      const int part0 = plan->n_parts;
+      for (int c = 0; c < nch; ++c) {
+        const int p0 = (int)((int64_t)np * c / nch), p1 = (int)((int64_t)np * (c + 1) / nch);
+        plan->items.push_back(AttnItem{i, h, p0, p1, plan->n_parts++});
+      }
+      plan->combs.push_back(AttnComb{i, h, part0, nch});
+    }
+  }
+  // longest items first (tail balance)
+  std::stable_sort(plan->items.begin(), plan->items.end(),
+                   [](const AttnItem& a, const AttnItem& c) { return (a.p1 - a.p0) > (c.p1 - c.p0); });
+}
+
+int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd) {
+  return (int64_t)max_items * sizeof(AttnItem) + (int64_t)max_items * sizeof(AttnComb) +
+         (int64_t)max_parts * g * (hd + 2) * sizeof(float) + 1024;
+}
+
+template <int HD>
+static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx,
+                                 const AttnItem* items, int n_items, int nq, int nkv, int max_pages, void* out,
+                                 int out_fp32, float* part_o, float* part_ml, cudaStream_t stream) {
+  constexpr int STAGE = 2 * PAGE_T * HD * 2;
+  const size_t ring = (size_t)ATTN_WARPS * ATTN_STAGES * STAGE;
+  const size_t merge = (size_t)ATTN_WARPS * 16 * (HD + 2) * sizeof(float);
+  const size_t smem = ring > merge ? ring : merge;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = true;
+  }
+  const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
+  attn_decode_kernel<HD><<<n_items, 128, smem, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx, items,
+      n_items, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const AttnItem* items,
+                        int n_items, const AttnComb* combs, int n_combs, int nq, int nkv, int hd, int page,
+                        int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
+                        cudaStream_t stream) {
+  if (page != PAGE_T) return cudaErrorInvalidValue;
+  if (nq % nkv != 0 || nq / nkv > 16) return cudaErrorInvalidValue;
+  if (n_items <= 0) return cudaSuccess;
+  cudaError_t e;
+  switch (hd) {
+    case 32:
+      e = launch_decode<32>(q, kv, bt, ctx, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
+                            stream);
+      break;
+    case 64:
+      e = launch_decode<64>(q, kv, bt, ctx, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
+                            stream);
+      break;
+    case 128:
+      e = launch_decode<128>(q, kv, bt, ctx, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o,
+                             part_ml, stream);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  if (n_combs > 0) {
+    attn_combine_kernel<<<n_combs, 128, 0, stream>>>(combs, n_combs, nq, nkv, hd, part_o, part_ml, out, out_fp32);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace sgs

@@ -1,0 +1,293 @@
+// Small HBM/latency-bound kernels of the iteration (SURVEY §8a rows a5, a6,
+// a7, a10 epilogue, a13, K11):
+//   rmsnorm      y = bf16(x / sqrt(mean(x^2) + eps) * w)          (fp32 math)
+//   rope_append  NeoX rotate-half RoPE on q,k (+bias) at each row's position,
+//                q -> bf16 buffer, k/v -> paged KV pool (XOR-swizzled rows)
+//   embed        h = float(E[token])
+//   silu_mul     m = bf16(SiLU(g) * u)
+//   argmax_rows  greedy sampling, lowest index on ties
+//   hash_init    counter-based bf16 weight generator
+//   checksum     sum_i bits16(w_i) * (2i+1) mod 2^64
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sgs {
+
+// ------------------------------------------------------------------ RMSNorm
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+                               __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ rows, int d, float eps) {
+  const int t = blockIdx.x;
+  const int src = rows ? rows[t] : t;
+  const float* xr = x + (size_t)src * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + i);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)d + eps);
+  __nv_bfloat16* yr = y + (size_t)t * d;
+  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + i);
+    const uint2 wb = *reinterpret_cast<const uint2*>(w + i);
+    const float w0 = __uint_as_float(wb.x << 16), w1 = __uint_as_float(wb.x & 0xffff0000u);
+    const float w2 = __uint_as_float(wb.y << 16), w3 = __uint_as_float(wb.y & 0xffff0000u);
+    uint2 o;
+    o.x = pack_bf16x2(v.x * r * w0, v.y * r * w1);
+    o.y = pack_bf16x2(v.z * r * w2, v.w * r * w3);
+    *reinterpret_cast<uint2*>(yr + i) = o;
+  }
+}
+
+cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows, int T, int d, float eps,
+                    cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  if (d % 4) return cudaErrorInvalidValue;
+  int threads = d >= 1024 ? 256 : 128;
+  rmsnorm_kernel<<<T, threads, 0, stream>>>(x, reinterpret_cast<const __nv_bfloat16*>(w),
+                                             reinterpret_cast<__nv_bfloat16*>(y), rows, d, eps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ RoPE + KV append
+// One block per row.  Pair index j in [0, (nq+2nkv) * hd/2): head = j / half,
+// i = j % half.  q/k heads rotate (x_i, x_{i+half}); v heads copy.
+__global__ void rope_append_kernel(const float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
+                                   const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+                                   const int32_t* __restrict__ bt, int max_pages, const float* __restrict__ cs,
+                                   __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv,
+                                   __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out, int nq,
+                                   int nkv, int hd, int page) {
+  const int t = blockIdx.x;
+  const int half = hd >> 1;
+  const int nh = nq + 2 * nkv;
+  const int ps = pos[t];
+  const float* row = qkv + (size_t)t * nh * hd;
+  const float* c = cs + (size_t)ps * half * 2;
+  const int rc = hd / 8;
+  int pg = -1, r = ps % page;
+  if (kv) pg = bt[(size_t)slot[t] * max_pages + ps / page];
+  for (int j = threadIdx.x; j < nh * half; j += blockDim.x) {
+    const int hh = j / half, i = j % half;
+    float x1 = row[hh * hd + i], x2 = row[hh * hd + i + half];
+    if (bias) {
+      x1 += __bfloat162float(bias[hh * hd + i]);
+      x2 += __bfloat162float(bias[hh * hd + i + half]);
+    }
+    float y1 = x1, y2 = x2;
+    if (hh < nq + nkv) {
+      const float co = c[2 * i], si = c[2 * i + 1];
+      y1 = x1 * co - x2 * si;
+      y2 = x2 * co + x1 * si;
+    }
+    const __nv_bfloat16 b1 = __float2bfloat16_rn(y1), b2 = __float2bfloat16_rn(y2);
+    if (hh < nq) {
+      q_out[((size_t)t * nq + hh) * hd + i] = b1;
+      q_out[((size_t)t * nq + hh) * hd + i + half] = b2;
+    } else {
+      const int isv = hh >= nq + nkv;
+      const int kvh = isv ? hh - nq - nkv : hh - nq;
+      if (kv) {
+        __nv_bfloat16* base = kv + (((size_t)pg * nkv + kvh) * 2 + isv) * (size_t)page * hd + (size_t)r * hd;
+        const int e1 = i, e2 = i + half;
+        base[(((e1 >> 3) ^ kv_swz(r, rc)) << 3) + (e1 & 7)] = b1;
+        base[(((e2 >> 3) ^ kv_swz(r, rc)) << 3) + (e2 & 7)] = b2;
+      }
+      __nv_bfloat16* cont = isv ? v_out : k_out;
+      if (cont) {
+        cont[((size_t)t * nkv + kvh) * hd + i] = b1;
+        cont[((size_t)t * nkv + kvh) * hd + i + half] = b2;
+      }
+    }
+  }
+}
+
+cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
+                        const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
+                        void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  rope_append_kernel<<<T, 256, 0, stream>>>(
+      qkv, reinterpret_cast<const __nv_bfloat16*>(bias), pos, slot, block_table, max_pages, cos_sin,
+      reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(kv),
+      reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), nq, nkv, hd, page);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ embedding gather
+__global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tokens,
+                             const int32_t* __restrict__ slots, const int32_t* __restrict__ last_tok,
+                             float* __restrict__ h, int d) {
+  const int t = blockIdx.x;
+  const int tok = slots ? last_tok[slots[t]] : tokens[t];
+  const __nv_bfloat16* e = E + (size_t)tok * d;
+  float* o = h + (size_t)t * d;
+  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(e + i);
+    *reinterpret_cast<float2*>(o + i) = make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+  }
+}
+
+cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, const int32_t* last_tok, float* h,
+                  int T, int d, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  embed_kernel<<<T, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(E), tokens, slots, last_tok, h, d);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ SwiGLU
+__global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ m, int f) {
+  const int t = blockIdx.y;
+  const float* g = gu + (size_t)t * 2 * f;
+  const float* u = g + f;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i < f; i += gridDim.x * blockDim.x * 2) {
+    const float2 gv = *reinterpret_cast<const float2*>(g + i);
+    const float2 uv = *reinterpret_cast<const float2*>(u + i);
+    const float s0 = gv.x / (1.f + __expf(-gv.x)), s1 = gv.y / (1.f + __expf(-gv.y));
+    *reinterpret_cast<uint32_t*>(m + (size_t)t * f + i) = pack_bf16x2(s0 * uv.x, s1 * uv.y);
+  }
+}
+
+cudaError_t silu_mul(const float* gu, void* m, int T, int f, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  int bx = (f / 2 + 255) / 256;
+  if (bx > 16) bx = 16;
+  silu_mul_kernel<<<dim3(bx, T), 256, 0, stream>>>(gu, reinterpret_cast<__nv_bfloat16*>(m), f);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ greedy sampler
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V, int32_t* ids,
+                                                      const int32_t* __restrict__ slot,
+                                                      const int32_t* __restrict__ tok_idx, int32_t* last_tok,
+                                                      int32_t* out_hist, int max_gen) {
+  const int r = blockIdx.x;
+  const float* x = logits + (size_t)r * V;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x * 4; i < V; i += blockDim.x * 4) {
+    if (i + 3 < V) {
+      const float4 v = *reinterpret_cast<const float4*>(x + i);
+      if (v.x > bv) bv = v.x, bi = i;
+      if (v.y > bv) bv = v.y, bi = i + 1;
+      if (v.z > bv) bv = v.z, bi = i + 2;
+      if (v.w > bv) bv = v.w, bi = i + 3;
+    } else {
+      for (int j = i; j < V; ++j)
+        if (x[j] > bv) bv = x[j], bi = j;
+    }
+  }
+  // (value desc, index asc) reduction
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = bv, si[threadIdx.x >> 5] = bi;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    bv = threadIdx.x < nw ? sv[threadIdx.x] : -INFINITY;
+    bi = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
+    }
+    if (threadIdx.x == 0) {
+      if (bi == 0x7fffffff) bi = 0;
+      if (ids) ids[r] = bi;
+      if (slot) {
+        const int s = slot[r];
+        last_tok[s] = bi;
+        out_hist[(size_t)s * max_gen + tok_idx[r]] = bi;
+      }
+    }
+  }
+}
+
+cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, const int32_t* slot,
+                        const int32_t* tok_idx, int32_t* last_tok, int32_t* out_hist, int max_gen,
+                        cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (V % 4) return cudaErrorInvalidValue;
+  argmax_kernel<<<rows, 1024, 0, stream>>>(logits, V, ids, slot, tok_idx, last_tok, out_hist, max_gen);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ weights
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, int64_t n, int is_norm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = splitmix64(key + (uint64_t)i);
+    const int32_t m = (int32_t)(h >> 40) - (1 << 23);
+    const float u = (float)m * (1.0f / 8388608.0f);
+    const float v = is_norm ? __fadd_rn(1.0f, __fmul_rn(u, 0.125f)) : __fmul_rn(u, 0.034641016f);
+    dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
+cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream) {
+  // key = splitmix64(seed ^ tensor_id * C): computed on the host, same constant as DESIGN.md §3
+  uint64_t z = seed ^ (tensor_id * 0xD1B54A32D192ED03ull);
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const uint64_t key = z ^ (z >> 31);
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  hash_init_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<__nv_bfloat16*>(dst), key, n, is_norm);
+  return cudaGetLastError();
+}
+
+__global__ void checksum_kernel(const uint16_t* __restrict__ src, int64_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += (unsigned long long)src[i] * (unsigned long long)(2 * i + 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  checksum_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint16_t*>(src), n, out_dev);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ block-table deltas
+__global__ void bt_delta_kernel(int32_t* bt, int max_pages, const int32_t* __restrict__ d, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) bt[(size_t)d[3 * i] * max_pages + d[3 * i + 1]] = d[3 * i + 2];
+}
+
+cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bt_delta_kernel<<<(n + 255) / 256, 256, 0, stream>>>(block_table, max_pages, deltas, n);
+  return cudaGetLastError();
+}
+
+}  // namespace sgs

@@ -1,0 +1,225 @@
+// K3/K4: bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+//   C[t, n] (+)= sum_k X[t, k] * W[n, k]        (the projections / MLP / LM head,
+//                                               SURVEY §8a rows a7, a9-a12)
+//
+// Swap-AB: the weight tile (128 output features x 64 K) is the UMMA "A"
+// operand (M = 128) and the token tile (BN tokens x 64 K) is "B" (N = BN,
+// 16..256), so the same kernel serves decode (b <= 256 tokens: weight
+// streaming, one N tile, HBM bound) and prefill (thousands of tokens,
+// tensor bound).  Accumulators live in TMEM; one elected thread issues TMA
+// loads into a multi-stage shared-memory ring, one elected thread issues
+// tcgen05.mma, four epilogue warps read TMEM (tcgen05.ld) and write fp32
+// rows of C (coalesced: lane = output feature).  Split-K over gridDim.z with
+// fp32 red.add when mode == 1.
+#include <cstdio>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sgs {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;
+constexpr int GEMM_SMEM_BUDGET = 200 * 1024;
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                        float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
+                        int chunks_per_split, int mode, int tmem_cols) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int b_bytes = BN * GEMM_BK * 2;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)stages * GEMM_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)stages * b_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* tmem_full = empty + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * GEMM_BM;
+  const int n0 = blockIdx.y * BN;
+  const int kc0 = blockIdx.z * chunks_per_split;
+  const int kc1 = min(kc0 + chunks_per_split, k_chunks_total);
+  const int nk = kc1 - kc0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmX);
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % stages;
+      if (i >= stages) mbar_wait(&empty[s], ((i / stages) - 1) & 1);
+      mbar_expect_tx(&full[s], GEMM_A_BYTES + b_bytes);
+      tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
+      tma_load_2d(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread)
+    const uint32_t idesc = umma_idesc_bf16(GEMM_BM, BN);
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % stages;
+      mbar_wait(&full[s], (i / stages) & 1);
+      tc_fence_after();
+      const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * GEMM_A_BYTES));
+      const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_bytes));
+#pragma unroll
+      for (int k = 0; k < GEMM_BK / 16; ++k)  // K = 16 per MMA: advance 32 B inside the swizzle atom
+        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tmem_full);
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> global (lane = output feature)
+    const int e = warp - 4;
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int n = m0 + 32 * e + lane;
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)c, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = n0 + c + j;
+        if (t < T) {
+          float* p = C + (size_t)t * ldc + n;
+          const float v = __uint_as_float(r[j]);
+          if (mode == 0)
+            *p = v;
+          else if (mode == 1)
+            atomicAdd(p, v);
+          else
+            *p += v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] tensor, box [box_rows, 64] with 128-byte swizzle.
+static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)GEMM_BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct TmapKey {
+  const void* p;
+  int64_t rows, cols;
+  int box;
+  bool operator==(const TmapKey& o) const { return p == o.p && rows == o.rows && cols == o.cols && box == o.box; }
+};
+struct TmapKeyHash {
+  size_t operator()(const TmapKey& k) const {
+    return std::hash<const void*>()(k.p) ^ (size_t)(k.rows * 1315423911u) ^ (size_t)(k.cols * 2654435761u) ^
+           (size_t)k.box;
+  }
+};
+
+static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  static std::mutex mu;
+  static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
+  TmapKey k{ptr, rows, cols, box_rows};
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(k);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (!make_tmap(out, ptr, rows, cols, box_rows)) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(k, *out);
+  return true;
+}
+
+int gemm_auto_splits(int N, int K, int T) {
+  const int bn = T >= 256 ? 256 : ((T + 15) / 16) * 16;
+  const int tiles = (N / GEMM_BM) * ((T + bn - 1) / bn);
+  const int kc = K / GEMM_BK;
+  if (tiles >= 120) return 1;
+  int s = 148 / tiles;
+  s = s < 1 ? 1 : s;
+  int maxs = kc / 4 > 0 ? kc / 4 : 1;  // keep >= 4 K chunks per split
+  return s > maxs ? maxs : s;
+}
+
+cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
+                      cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  if (N % GEMM_BM != 0 || K % GEMM_BK != 0) return cudaErrorInvalidValue;
+  const int BN = T >= 256 ? 256 : ((T + 15) / 16) * 16;
+  const int kc = K / GEMM_BK;
+  if (splits <= 0) splits = mode == 1 ? gemm_auto_splits(N, K, T) : 1;
+  if (splits > 1 && mode != 1) return cudaErrorInvalidValue;
+  const int per = (kc + splits - 1) / splits;
+  splits = (kc + per - 1) / per;  // every split has >= 1 chunk
+  CUtensorMap tw, tx;
+  if (!cached_tmap(&tw, W, N, K, GEMM_BM)) return cudaErrorInvalidValue;
+  if (!cached_tmap(&tx, X, T, K, BN)) return cudaErrorInvalidValue;
+  const int stage_bytes = GEMM_A_BYTES + BN * GEMM_BK * 2;
+  int stages = GEMM_SMEM_BUDGET / stage_bytes;
+  if (stages > 12) stages = 12;
+  if (stages > kc) stages = kc < 2 ? 2 : kc;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
+  const int tmem_cols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  dim3 grid(N / GEMM_BM, (T + BN - 1) / BN, splits);
+  gemm_bf16_tc_kernel<<<grid, 256, smem, stream>>>(tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols);
+  return cudaGetLastError();
+}
+
+}  // namespace sgs

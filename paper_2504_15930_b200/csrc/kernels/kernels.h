@@ -1,0 +1,58 @@
+// Host-side launchers of the sm_100a kernels (internal to libsgs).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace sgs {
+
+// ---- GEMM (gemm.cu): C[t, n] (+)= X[t, :] . W[n, :]; mode 0 store, 1 atomic add, 2 add
+cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
+                      cudaStream_t stream);
+int gemm_auto_splits(int N, int K, int T);
+
+// ---- decode attention (attention.cu)
+struct AttnItem {
+  int32_t row, kvh, p0, p1, part;  // part < 0: the item covers the whole row -> final output
+};
+struct AttnComb {
+  int32_t row, kvh, part0, nparts;
+};
+struct AttnPlan {
+  std::vector<AttnItem> items;
+  std::vector<AttnComb> combs;
+  int n_parts = 0;
+};
+// Split-K plan over pages: rows with more than `chunk` pages are split.
+void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, AttnPlan* plan);
+int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
+// items/combs are device arrays (already copied); part buffers in workspace.
+cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
+                        const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
+                        int hd, int page, int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
+                        cudaStream_t stream);
+
+// ---- prefill attention (prefill_attn.cu): causal within each prompt.
+// q [T, nq, hd], k/v [T, nkv, hd] contiguous bf16; prompt p spans rows
+// [offs[p], offs[p+1]).  out bf16 [T, nq, hd].
+cudaError_t attn_prefill(const void* q, const void* k, const void* v, const int32_t* offs, const int32_t* qblocks,
+                         int n_qblocks, int nq, int nkv, int hd, void* out, cudaStream_t stream);
+
+// ---- elementwise (elementwise.cu)
+cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows, int T, int d, float eps,
+                    cudaStream_t stream);
+cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
+                        const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
+                        void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream);
+cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, const int32_t* last_tok, float* h,
+                  int T, int d, cudaStream_t stream);
+cudaError_t silu_mul(const float* gu, void* m, int T, int f, cudaStream_t stream);
+cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, const int32_t* slot,
+                        const int32_t* tok_idx, int32_t* last_tok, int32_t* out_hist, int max_gen,
+                        cudaStream_t stream);
+cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream);
+cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream);
+cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream);
+
+}  // namespace sgs

@@ -1,0 +1,201 @@
+"""GPU parity of the sm_100a kernels (through the C-ABI) against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workload
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sgs():
+    assert torch.cuda.is_available(), "the -m gpu tests need a B200"
+    import paper_2504_15930_b200 as m
+    m.lib()
+    return m
+
+
+def _bf(shape, seed, scale=1.0):
+    return workload.random_bf16(shape, seed, scale)
+
+
+# ------------------------------------------------------------------ GEMM (K3/K4)
+@pytest.mark.parametrize("N,K,T,mode,splits", [
+    (256, 128, 5, 0, 1),          # tiny QKV, decode
+    (4608, 3584, 1, 1, 4),        # 7B QKV, b = 1, split-K with red.add
+    (4608, 3584, 37, 1, 0),       # ragged b, automatic splits
+    (3584, 18944, 256, 2, 1),     # 7B down at b = 256 (+= residual)
+    (1024, 512, 1000, 0, 1),      # prefill-shaped: several N tiles + ragged tail
+    (152064 // 16, 3584, 200, 0, 1),
+])
+def test_gemm_vs_fp64(sgs, N, K, T, mode, splits):
+    W = _bf((N, K), 1, 0.02).cuda()
+    X = _bf((T, K), 2, 1.0).cuda()
+    C0 = torch.randn(T, N, device="cuda") if mode == 2 else torch.zeros(T, N, device="cuda")
+    C = C0.clone()
+    sgs.op_gemm(W, X, C, mode=mode, splits=splits)
+    torch.cuda.synchronize()
+    ref = X.double().cpu() @ W.double().cpu().T
+    if mode == 2:
+        ref = ref + C0.double().cpu()
+    bound = 1e-5 * (X.double().abs().cpu() @ W.double().abs().cpu().T) + 1e-6
+    err = (C.double().cpu() - ref).abs()
+    assert (err <= bound).all(), float((err / bound).max())
+
+
+# ------------------------------------------------------------------ decode attention (K1/K2)
+def _attn_case(b, nq, nkv, hd, ctxs, seed, n_pages=None):
+    page = 16
+    npg = [(c + page - 1) // page for c in ctxs]
+    maxp = max(npg)
+    total = sum(npg)
+    n_pages = n_pages or total + 7
+    K = _bf((n_pages, nkv, page, hd), seed)
+    V = _bf((n_pages, nkv, page, hd), seed + 1)
+    perm = torch.randperm(n_pages, generator=torch.Generator().manual_seed(seed))[:total]
+    bt = torch.zeros(b, maxp, dtype=torch.int32)
+    o = 0
+    for i, n in enumerate(npg):
+        bt[i, :n] = perm[o:o + n].to(torch.int32)
+        o += n
+    q = _bf((b, nq, hd), seed + 2)
+    return q, K, V, bt, torch.tensor(ctxs, dtype=torch.int32)
+
+
+def _oracle_rows(q, K, V, bt, ctx, rows):
+    page = K.shape[2]
+    out = {}
+    for i in rows:
+        c = int(ctx[i])
+        pages = bt[i, :(c + page - 1) // page].long()
+        Kl = K[pages].permute(0, 2, 1, 3).reshape(-1, K.shape[1], K.shape[3])[:c]
+        Vl = V[pages].permute(0, 2, 1, 3).reshape(-1, V.shape[1], V.shape[3])[:c]
+        out[i] = oracle.attention(q[i].float().numpy(), Kl.float().numpy(), Vl.float().numpy())
+    return out
+
+
+def _rel_err(got, ref):
+    # per (row, head): ||o - ref||_inf / ||ref||_inf  (north_star: 1e-3, fp32 output)
+    return np.abs(got - ref).max(axis=-1) / np.abs(ref).max(axis=-1)
+
+
+@pytest.mark.parametrize("nq,nkv,hd,ctxs", [
+    (4, 2, 32, [1, 15, 16, 17, 255, 272]),            # tiny
+    (28, 4, 128, [1, 16, 33, 500, 1024, 4097]),       # 7B (g = 7)
+    (40, 8, 128, [7, 300, 2048, 8704]),               # 14B/32B (g = 5)
+])
+@pytest.mark.parametrize("split", [0, 1, 3])
+def test_decode_attention_vs_fp64(sgs, nq, nkv, hd, ctxs, split):
+    b = len(ctxs)
+    q, K, V, bt, ctx = _attn_case(b, nq, nkv, hd, ctxs, seed=hd + len(ctxs) + split)
+    pool = sgs.kv_pack(K, V).cuda()
+    out = torch.zeros(b, nq, hd, dtype=torch.float32, device="cuda")
+    sgs.op_decode_attention(q.cuda(), pool, bt.cuda(), ctx.cuda(), out, split_pages=split)
+    torch.cuda.synchronize()
+    ref = _oracle_rows(q, K, V, bt, ctx, range(b))
+    got = out.cpu().numpy()
+    for i in range(b):
+        err = _rel_err(got[i], ref[i])
+        assert err.max() <= 1e-3, (i, ctxs[i], float(err.max()))
+    # bf16 output mode = the fp32 result rounded once
+    outb = torch.zeros(b, nq, hd, dtype=torch.bfloat16, device="cuda")
+    sgs.op_decode_attention(q.cuda(), pool, bt.cuda(), ctx.cuda(), outb, split_pages=split)
+    torch.cuda.synchronize()
+    assert torch.equal(outb.cpu(), out.cpu().to(torch.bfloat16))
+
+
+def test_decode_attention_special_cases(sgs):
+    nq, nkv, hd = 28, 4, 128
+    # ctx = 1 -> o = v0 exactly; identical keys -> mean(V)
+    q, K, V, bt, ctx = _attn_case(2, nq, nkv, hd, [1, 640], seed=5)
+    Ksame = K.clone()
+    key = _bf((nkv, hd), 77)
+    for p in bt[1, :40].long():
+        Ksame[p] = key[:, None, :].expand(nkv, 16, hd)
+    pool = sgs.kv_pack(Ksame, V).cuda()
+    out = torch.zeros(2, nq, hd, dtype=torch.float32, device="cuda")
+    sgs.op_decode_attention(q.cuda(), pool, bt.cuda(), ctx.cuda(), out)
+    torch.cuda.synchronize()
+    v0 = V[bt[0, 0].long(), :, 0, :].float()
+    assert torch.equal(out[0].cpu(), v0.repeat_interleave(nq // nkv, 0))
+    Vl = V[bt[1, :40].long()].permute(0, 2, 1, 3).reshape(-1, nkv, hd).double()
+    mean = Vl.mean(0).repeat_interleave(nq // nkv, 0)
+    assert ((out[1].cpu().double() - mean).abs().max() / mean.abs().max()) < 1e-3
+
+
+def test_decode_attention_full_size_sampled(sgs):
+    # 7B launch configuration of the bench: b = 256 rows, long-tail contexts up to 8.7K;
+    # sampled rows are checked one by one against the fp64 oracle
+    rng = np.random.default_rng(3)
+    ctxs = np.clip(np.rint(rng.lognormal(np.log(1500), 1.0, 256)), 1, 8704).astype(int).tolist()
+    q, K, V, bt, ctx = _attn_case(256, 28, 4, 128, ctxs, seed=11)
+    pool = sgs.kv_pack(K, V).cuda()
+    out = torch.zeros(256, 28, 128, dtype=torch.float32, device="cuda")
+    sgs.op_decode_attention(q.cuda(), pool, bt.cuda(), ctx.cuda(), out)
+    torch.cuda.synchronize()
+    rows = [int(np.argmax(ctxs)), int(np.argmin(ctxs))] + rng.choice(256, 10, replace=False).tolist()
+    ref = _oracle_rows(q, K, V, bt, ctx, rows)
+    got = out.cpu().numpy()
+    for i in rows:
+        assert _rel_err(got[i], ref[i]).max() <= 1e-3, i
+
+
+# ------------------------------------------------------------------ RMSNorm, RoPE+append, argmax
+def test_rmsnorm_vs_oracle(sgs):
+    for T, d in [(3, 128), (37, 3584), (5, 5120)]:
+        x = torch.randn(T, d, generator=torch.Generator().manual_seed(d)) * 3
+        w = torch.from_numpy(oracle.gen_tensor(3, 10, d, is_norm=True)).to(torch.bfloat16)
+        y = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+        sgs.op_rmsnorm(x.cuda(), w.cuda(), y, 1e-6)
+        torch.cuda.synchronize()
+        ref = oracle.rmsnorm(x.double().numpy(), w.float().numpy(), 1e-6)
+        got = y.float().cpu().numpy()
+        # both round once to bf16; fp32 vs fp64 may straddle a rounding boundary: <= 1 ulp
+        assert (np.abs(got - ref) <= np.abs(ref) * 2 ** -7 + 1e-30).all()
+        assert (got == ref).mean() > 0.97
+
+
+def test_rope_append_vs_oracle(sgs):
+    nq, nkv, hd, page = 28, 4, 128, 16
+    T = 9
+    theta = 1e6
+    qkv = torch.randn(T, (nq + 2 * nkv) * hd, generator=torch.Generator().manual_seed(1))
+    bias = _bf(((nq + 2 * nkv) * hd,), 2, 0.02)
+    pos = torch.tensor([0, 1, 15, 16, 17, 100, 4095, 8191, 31], dtype=torch.int32)
+    slot = torch.tensor([0, 1, 2, 3, 4, 5, 6, 7, 8], dtype=torch.int32)
+    maxp = 8192 // page + 1
+    bt = torch.arange(T * maxp, dtype=torch.int32).reshape(T, maxp) % 1000
+    bt = torch.stack([torch.randperm(1000, generator=torch.Generator().manual_seed(i))[:maxp] for i in range(T)]).int()
+    cs = torch.from_numpy(sgs.rope_table(8192 + 1, hd, theta))
+    kv = torch.zeros(1000, nkv, 2, page, hd, dtype=torch.bfloat16, device="cuda")
+    qo = torch.empty(T, nq, hd, dtype=torch.bfloat16, device="cuda")
+    sgs.op_rope_append(qkv.cuda(), bias.cuda(), pos.cuda(), slot.cuda(), bt.cuda(), cs.cuda(), qo, kv, nq, nkv, hd)
+    torch.cuda.synchronize()
+    Kl, Vl = sgs.kv_unpack(kv.cpu())
+    x = qkv.double() + bias.double()
+    for t in range(T):
+        p = int(pos[t])
+        pg = int(bt[t, p // page])
+        for h in range(nq + 2 * nkv):
+            v = x[t, h * hd:(h + 1) * hd].numpy()
+            ref = oracle.rope(v, p, theta) if h < nq + nkv else v
+            if h < nq:
+                got = qo[t, h].float().cpu().numpy()
+            elif h < nq + nkv:
+                got = Kl[pg, h - nq, p % page].float().numpy()
+            else:
+                got = Vl[pg, h - nq - nkv, p % page].float().numpy()
+            refb = torch.from_numpy(ref).float().to(torch.bfloat16).float().numpy()
+            # fp32 angles from an fp64 table vs fp64: at most one bf16 ulp apart
+            assert (np.abs(got - refb) <= np.abs(refb) * 2 ** -7 + 1e-6).all(), (t, h)
+
+
+def test_argmax_vs_oracle(sgs):
+    rng = np.random.default_rng(0)
+    x = rng.integers(-20, 20, size=(33, 152064)).astype(np.float32)  # many ties
+    ids = torch.empty(33, dtype=torch.int32, device="cuda")
+    sgs.op_argmax(torch.from_numpy(x).cuda(), ids)
+    torch.cuda.synchronize()
+    assert ids.cpu().tolist() == [oracle.argmax(r) for r in x]

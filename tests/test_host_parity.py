@@ -1,0 +1,169 @@
+"""CPU parity of the product's host control plane (null-device mode of libsgs)
+against the oracle: schedules, block tables, emitted order, dispatch and the
+T(b) fit must agree bit for bit (north_star)."""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+from paper_2504_15930_b200 import Instance, dispatch_plan, fit_profile
+
+PROF = (20000, 500, 128, 2000)
+
+
+def run_null(tr, B, page, pool, N=1, rank=0, batches=None, shape="qwen2.5-7b", **kw):
+    inst = Instance(workload.MODELS[shape], B, 40000, device=None, page_size=page, n_pages=pool,
+                    n_instances=N, instance_rank=rank, profile=PROF, **kw)
+    comps = []
+    if batches is None:
+        inst.submit_trace(tr)
+        comps = inst.run()
+    else:
+        # batches: list of (trace, submit_after_iterations)
+        it = 0
+        pending = list(batches)
+        while True:
+            while pending and pending[0][1] <= it:
+                inst.submit_trace(pending.pop(0)[0])
+            q, a = inst.pending()
+            if q == 0 and a == 0 and not pending:
+                break
+            if q == 0 and a == 0:
+                inst.submit_trace(pending.pop(0)[0])
+                continue
+            comps.extend(inst.step())
+            it += 1
+    return inst, comps
+
+
+def oracle_trace(tr, B, page, pool, batch=None, arrival=None):
+    return oracle.sched_sim(tr.ids, tr.prompt_len, tr.forced_len, tr.hint, B, page, pool, batch=batch,
+                            arrival_after=arrival)
+
+
+def assert_same(inst, o):
+    got_it = inst.trace(0)
+    got_s = inst.trace(1)
+    assert np.array_equal(got_it, o["iter_blob"])
+    assert np.array_equal(got_s, o["sample_blob"])
+
+
+@pytest.mark.parametrize("cfg,pool", [("c1_tiny", 2000), ("c1_tiny", 40), ("c2_7b", 171_000), ("c2_7b", 20_000)])
+def test_schedule_bit_exact_config_traces(cfg, pool):
+    c = workload.CONFIGS[cfg]
+    tr = workload.config_trace(c)
+    inst, comps = run_null(tr, c.max_batch, c.page_size, pool)
+    o = oracle_trace(tr, c.max_batch, c.page_size, pool)
+    assert_same(inst, o)
+    # emitted order: by finish iteration, ascending id within an iteration
+    order = [x["id"] for x in comps]
+    exp = [i for it in o["iters"] for i in it["completed"]]
+    assert order == exp
+    assert all(len(x["tokens"]) == int(tr.forced_len[x["id"]]) for x in comps)
+
+
+def test_schedule_noisy_hints_and_ragged_prompts():
+    tr = workload.make_trace(200, 40, 60, 1.2, 900, 512, seed=9, hint_noise=0.6, prompt_len_jitter=30)
+    inst, _ = run_null(tr, 24, 16, 500)
+    assert_same(inst, oracle_trace(tr, 24, 16, 500))
+
+
+def test_schedule_edge_cases():
+    # single sample d=1; B=1; all equal lengths; pool exactly one sample
+    for (n, P, d, B, pool) in [(1, 1, 1, 4, 10), (5, 3, 7, 1, 100), (9, 16, 16, 3, 100), (4, 20, 13, 4, 3)]:
+        ids = np.arange(n)
+        tr = workload.Trace(ids, np.full(n, P), np.full(n, d), np.full(n, d),
+                            np.zeros(n * P, np.int32), np.arange(n + 1) * P)
+        inst, comps = run_null(tr, B, 16, pool)
+        assert_same(inst, oracle_trace(tr, B, 16, pool))
+        assert len(comps) == n
+
+
+def test_schedule_multi_batch_fifo():
+    a = workload.make_trace(30, 8, 20, 1.0, 120, 512, seed=3)
+    b = workload.make_trace(30, 8, 20, 1.0, 120, 512, seed=4, id_base=1000)
+    inst, _ = run_null(None, 8, 16, 300, batches=[(a, 0), (b, 25)])
+    ids = np.concatenate([a.ids, b.ids])
+    cat = lambda f: np.concatenate([getattr(a, f), getattr(b, f)])
+    tr = workload.Trace(ids, cat("prompt_len"), cat("forced_len"), cat("hint"), np.zeros(1, np.int32), None)
+    o = oracle_trace(tr, 8, 16, 300, batch=np.array([0] * 30 + [1] * 30), arrival=np.array([0] * 30 + [25] * 30))
+    assert_same(inst, o)
+
+
+def test_capacity_and_validation_errors():
+    from paper_2504_15930_b200 import SgsError
+    inst = Instance(workload.MODELS["tiny"], 4, 100, device=None, n_pages=5)
+    tr = workload.make_trace(3, 8, 10, 0.0, 10, 512, seed=1)
+    with pytest.raises(SgsError) as e:  # hint 0
+        inst.submit(tr.ids, tr.tokens, tr.offsets, np.zeros(3), tr.forced_len)
+    assert e.value.code == -1
+    with pytest.raises(SgsError) as e:  # P + d - 1 > max_ctx
+        inst.submit(tr.ids, tr.tokens, tr.offsets, tr.hint, np.full(3, 200))
+    assert e.value.code == -4
+    with pytest.raises(SgsError) as e:  # token out of range
+        inst.submit(tr.ids, np.full_like(tr.tokens, 999), tr.offsets, tr.hint, tr.forced_len)
+    assert e.value.code == -1
+    assert inst.submit_trace(tr) == 3
+    with pytest.raises(SgsError):  # duplicate id
+        inst.submit_trace(tr)
+    assert inst.step() == [] or True
+    with pytest.raises(SgsError) as e:  # update while busy
+        inst.update_weights(0)
+    assert e.value.code == -3
+    inst.run()
+    assert inst.step() == []  # idle: no iteration counted
+    n_it = len(oracle.parse_iter_blob(inst.trace(0)))
+    inst.update_weights(0)
+    assert inst.weight_version() == 1
+    assert len(oracle.parse_iter_blob(inst.trace(0))) == n_it
+
+
+def test_dispatch_bit_exact_vs_oracle():
+    rng = np.random.default_rng(11)
+    for trial in range(300):
+        n = int(rng.integers(1, 120))
+        N = int(rng.integers(1, 9))
+        ids = rng.permutation(5000)[:n].astype(np.uint64)
+        hint = rng.integers(1, 20000, size=n)
+        P = rng.integers(1, 700, size=n)
+        B = int(rng.integers(1, 300))
+        pool = int(rng.integers(50, 100000))
+        prof = (int(rng.integers(100, 9000)), int(rng.integers(1, 200)) * 1000, int(rng.integers(1, 400)),
+                int(rng.integers(200, 900)) * 1000)
+        alpha = int(rng.integers(0, 101))
+        score = int(rng.integers(0, 2))
+        tc = int(rng.integers(0, 2))
+        got, nl = dispatch_plan(ids, P, hint, N, B, 16, pool, prof, alpha, score, tc)
+        exp = oracle.dispatch(ids.astype(np.int64), P, hint, N, B, 16, pool, prof, alpha, score, tc)
+        assert np.array_equal(got, exp["instance"]), trial
+        if N > 1:
+            assert nl == exp["n_l"]
+
+
+def test_submit_keeps_dispatched_share():
+    tr = workload.config_trace("c3_14b_4", n=256)
+    N, pool = 4, 50_000
+    exp = oracle.dispatch(tr.ids, tr.prompt_len, tr.hint, N, 256, 16, pool, PROF)["instance"]
+    seen = []
+    for r in range(N):
+        inst, comps = run_null(tr, 256, 16, pool, N=N, rank=r)
+        mine = sorted(x["id"] for x in comps)
+        assert mine == sorted(tr.ids[exp == r].tolist())
+        sub = tr.subset(np.flatnonzero(exp == r))
+        assert_same(inst, oracle_trace(sub, 256, 16, pool))
+        seen += mine
+    assert sorted(seen) == tr.ids.tolist()
+
+
+def test_fit_matches_oracle():
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        t0, k0, k1 = rng.uniform(500, 5000), rng.uniform(0.5, 20), rng.uniform(25, 80)
+        bs = int(rng.choice([32, 64, 128, 192, 256]))
+        b = np.array([1, 2, 4, 8, 16, 32, 64, 96, 128, 160, 192, 224, 256, 320, 384, 512, 768, 1024], float)
+        T = np.where(b < bs, t0 + k0 * b, t0 + k0 * bs + k1 * (b - bs)) * (1 + rng.uniform(-0.02, 0.02, b.size))
+        g, o = fit_profile(b, T), oracle.tb_fit(b, T)
+        assert g["profile"][2] == o["b_star"]
+        for k in ("t0", "k0", "k1", "t1"):
+            assert abs(g[k] - o[k]) <= 1e-6 * max(1.0, abs(o[k]))
+        assert g["profile"] == o["profile"]

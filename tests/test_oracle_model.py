@@ -198,3 +198,37 @@ def test_top_p_limits():
         counts[oracle.sample_top_p(x, 1.0, 1.0, 7, s, 3)] += 1
     top = np.argsort(-p)[:5]
     assert np.all(np.abs(counts[top] / n - p[top]) < 5 * np.sqrt(p[top] / n) + 1e-3)
+
+
+def test_rmsnorm_closed_forms():
+    d = 64
+    w = oracle.gen_tensor(1, 99, d, is_norm=True)
+    # constant row c: x / sqrt(c^2 + eps) -> sign(c) * w (up to eps), exactly bf16(w) for eps = 0
+    for c in (3.0, -0.25):
+        y = oracle.rmsnorm(np.full((1, d), c), w, 0.0)
+        assert np.array_equal(y[0], np.sign(c) * w.astype(np.float64))
+    # scale invariance and library routine (torch rms_norm in fp64, then bf16)
+    x = np.random.default_rng(0).standard_normal((5, d)) * 7
+    y1, y2 = oracle.rmsnorm(x, w, 1e-6), oracle.rmsnorm(x * 1000, w, 1e-6 * 1e6)
+    assert np.array_equal(y1, y2)
+    ref = torch.nn.functional.rms_norm(torch.from_numpy(x), (d,), torch.from_numpy(w).double(), eps=1e-6)
+    ref = ref.float().to(torch.bfloat16).double().numpy()
+    assert (np.abs(y1 - ref) <= np.abs(ref) * 2 ** -8).all()
+
+
+def test_rope_invariants():
+    hd, theta = 128, 1e6
+    rng = np.random.default_rng(2)
+    q, k = rng.standard_normal(hd), rng.standard_normal(hd)
+    assert np.array_equal(oracle.rope(q, 0, theta), q)            # position 0 = identity
+    for p in (1, 37, 9000, 32767):                                 # rotation: norm preserved per pair
+        r = oracle.rope(q, p, theta)
+        half = hd // 2
+        assert np.allclose(r[:half] ** 2 + r[half:] ** 2, q[:half] ** 2 + q[half:] ** 2, rtol=1e-12)
+    # relative position: <R_m q, R_n k> depends only on m - n
+    dots = [oracle.rope(q, m, theta) @ oracle.rope(k, m - 5, theta) for m in (5, 100, 7777)]
+    assert np.allclose(dots, dots[0], rtol=1e-9)
+    # first pair rotates by exactly pos radians (inv_freq_0 = 1)
+    e = np.zeros(hd); e[0] = 1.0
+    r = oracle.rope(e, 3, theta)
+    assert abs(r[0] - np.cos(3)) < 1e-15 and abs(r[hd // 2] - np.sin(3)) < 1e-15
