@@ -1,0 +1,300 @@
+"""bench.py — generated tokens/s and RL-batch completion time of the Stream
+Generation Service hot path (StreamRL, arXiv 2504.15930) on B200.
+
+One step = one RL batch through every hot-path row: submit +
+Alg. 2 dispatch, longest-first continuous batching (prefill + paged decode)
+until every sample has streamed out, then the weight sync (NCCL broadcast from
+rank 0 = the trainer proxy; a version bump at N = 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_7b] [--impl reference]
+N > 1: torchrun, one rank per GPU; weak scaling (512 prompts per GPU, the
+whole N*512-prompt batch is submitted on every rank and Alg. 2 keeps each
+rank's share; no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workload  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["_source"] = "measured"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["_source"] = "fallback"
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ reference arm (the CPU oracle)
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    import oracle
+    cfg = workload.CONFIGS[args.config]
+    shape = workload.MODELS[cfg.model]
+    res = cpu_oracle_sample(shape, steps=args.steps, warmup=args.warmup)
+    line = {"metric": "generated_tokens_per_s", "value": res["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: {cfg.model}-shaped, {cfg.n_prompts} prompts x {cfg.prompt_len}"},
+            "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"], "kind": "oracle",
+                             "sample": res["sample"]},
+            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_oracle_sample(shape, steps=1, warmup=0, T=8):
+    """Time the oracle decoder (as it stands) on a bounded sample of the workload:
+    T positions of one sample through layer subsets of the full model, extrapolated
+    to all layers (t_full = t_lmhead + L * (t_1layer - t_lmhead))."""
+    import dataclasses
+    import oracle
+    toks = np.random.default_rng(0).integers(0, shape.vocab, size=T).astype(np.int32)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        oracle.decoder_forward(dataclasses.replace(shape, n_layers=0), 1, toks, T - 1)
+        t1 = time.perf_counter()
+        oracle.decoder_forward(dataclasses.replace(shape, n_layers=1), 1, toks, T - 1)
+        t2 = time.perf_counter()
+        if i >= warmup:
+            t_lm, t_layer = t1 - t0, (t2 - t1) - (t1 - t0)
+            times.append(t_lm + shape.n_layers * max(t_layer, 0.0))
+    t_full = statistics.median(times)
+    return {"value": T / t_full, "ms_per_step": 1e3 * t_full, "cores": os.cpu_count(),
+            "sample": f"{T} teacher-forced positions of one sample; 0- and 1-layer {shape.name} runs timed, "
+                      f"extrapolated to {shape.n_layers} layers (fp64, OpenMP, weights regenerated per call)"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2_7b")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prompts-per-gpu", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2504_15930_b200 as sgs
+
+    world, rank, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    cfg = workload.CONFIGS[args.config]
+    shape = workload.MODELS[cfg.model]
+    per_gpu = args.prompts_per_gpu or cfg.n_prompts
+    n_total = per_gpu * world
+    max_ctx = cfg.prompt_len + cfg.max_out
+
+    inst = sgs.Instance(shape, cfg.max_batch, max_ctx, device=local, n_instances=world, instance_rank=rank,
+                        weight_seed=cfg.seed, flags=sgs.sgs.F_KERNEL_TIMING)
+    if world > 1:
+        uid = [sgs.comm_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(uid, src=0)
+        inst.comm_init(uid[0], rank, world)
+
+    def make_batch(step):
+        # a fresh RL batch per step: same length distribution, new ids and prompts
+        return workload.make_trace(n_total, cfg.prompt_len, cfg.median_out, cfg.sigma, cfg.max_out, shape.vocab,
+                                   seed=cfg.seed + 1000 * step, id_base=step * 1_000_000)
+
+    stream = inst.stream
+
+    def one_step(step):
+        tr = make_batch(step)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = inst.kernel_launches()
+        io0 = inst.io_bytes()
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        mine = inst.submit_trace(tr)
+        comps = inst.run()
+        # weight sync at the RL-step boundary: rank 0 is the trainer proxy
+        if rank == 0:
+            inst.load_weights_seed(cfg.seed + step + 1)
+        inst.update_weights(0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        io1 = inst.io_bytes()
+        gen_tokens = int(sum(len(c["tokens"]) for c in comps))
+        assert len(comps) == mine
+        prompt_bytes = int(tr.tokens.nbytes)
+        return dict(dev_s=ev0.elapsed_time(ev1) / 1e3, wall_s=wall, tokens=gen_tokens, samples=len(comps),
+                    launches=inst.kernel_launches() - launches0,
+                    h2d=io1[0] - io0[0] + prompt_bytes, d2h=io1[1] - io0[1])
+
+    for w in range(args.warmup):
+        one_step(w)
+    for cls in range(3):
+        inst.kernel_stats(cls, reset=True)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    results = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            results.append(one_step(args.warmup + k))
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+
+    dev_s = sum(r["dev_s"] for r in results)
+    wall_s = sum(r["wall_s"] for r in results)
+    tokens = sum(r["tokens"] for r in results)
+    stats = {cls: inst.kernel_stats(cls) for cls in range(3)}
+    if pg:
+        t = torch.tensor([dev_s, wall_s, float(tokens)], dtype=torch.float64)
+        mx = t.clone()
+        pg.all_reduce(mx, op=pg.ReduceOp.MAX)
+        sm = t.clone()
+        pg.all_reduce(sm, op=pg.ReduceOp.SUM)
+        dev_s, wall_s, tokens = float(mx[0]), float(mx[1]), int(sm[2])
+    if rank != 0:
+        pg.destroy_process_group()
+        return
+    peaks = load_peaks()
+    # dominant kernel class by device time: 0 decode attention (HBM), 1 GEMMs
+    dom = max((0, 1), key=lambda c: stats[c]["ms"])
+    st = stats[dom]
+    if dom == 0:
+        achieved = st["bytes"] / (st["ms"] / 1e3) / 1e9
+        roof = {"kernel": "decode_attention (K1+K2)", "bound": "hbm", "achieved": round(achieved, 1),
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4)}
+    else:
+        achieved = st["bytes"] / (st["ms"] / 1e3) / 1e9
+        roof = {"kernel": "tcgen05 GEMMs (all shapes)", "bound": "hbm", "achieved": round(achieved, 1),
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4)}
+    roof["traffic"] = None
+    roof["peak_source"] = peaks["_source"]
+    roof["launches"] = st["launches"]
+    roof["share_of_step"] = round(st["ms"] / 1e3 / (sum(r["dev_s"] for r in results)), 4)
+    other = {("decode_attention" if c == 0 else "gemm" if c == 1 else "prefill_attention"):
+             {"ms": round(stats[c]["ms"], 1), "launches": stats[c]["launches"],
+              "GB/s": round(stats[c]["bytes"] / max(stats[c]["ms"], 1e-9) / 1e6, 1),
+              "TFLOP/s": round(stats[c]["flops"] / max(stats[c]["ms"], 1e-9) / 1e9, 1)} for c in range(3)}
+    line = {
+        "metric": "generated_tokens_per_s",
+        "value": round(tokens / dev_s, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dev_s / args.steps, 1),
+        "rl_batch_completion_s": round(dev_s / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg.model}-shaped random-init bf16 decoder, {per_gpu} prompts/GPU "
+                               f"x {cfg.prompt_len} tokens, lognormal(median {cfg.median_out}, sigma {cfg.sigma}) "
+                               f"forced lengths <= {cfg.max_out}, B={cfg.max_batch}, longest-first, Alg. 2 dispatch",
+                   "prompts_total": n_total, "global_batch": n_total, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (weights 15 GB, KV pool > 100 GB)"},
+        "e2e": {"value": round(tokens / wall_s, 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(statistics.mean(r["h2d"] for r in results)),
+                "d2h_bytes_per_step": int(statistics.mean(r["d2h"] for r in results))},
+        "gpu_launches": int(sum(r["launches"] for r in results)),
+        "roofline": roof,
+        "kernels": other,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        cb = cpu_oracle_sample(shape)
+        line["cpu_baseline"] = {"value": round(cb["value"], 4), "unit": "tokens/s", "cores": cb["cores"],
+                                "kind": "oracle", "sample": cb["sample"]}
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -62,7 +62,8 @@ enum { SGS_SCORE_SUM = 0, SGS_SCORE_MAX = 1 };
 enum { SGS_SAMPLE_GREEDY = 0, SGS_SAMPLE_TOP_P = 1 };
 enum {
   SGS_F_KEEP_LOGITS = 1,     /* keep fp32 logits of the last iteration (teacher-forcing tests) */
-  SGS_F_NO_GRAPHS = 2        /* launch the decode iteration eagerly (no CUDA graphs) */
+  SGS_F_NO_GRAPHS = 2,       /* launch the decode iteration eagerly (no CUDA graphs) */
+  SGS_F_KERNEL_TIMING = 4    /* CUDA-event timing per kernel class (sgs_kernel_stats) */
 };
 
 typedef struct {
@@ -170,8 +171,22 @@ sgs_status sgs_trace_clear(sgs_handle* h);
 sgs_status sgs_last_logits(sgs_handle* h, float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap,
                            int32_t* rows);
 
+/* Layer-by-layer parity hook: a standalone prefill forward of one prompt
+ * (tokens host int32 [T], slot 0, idle handle only) that dumps the fp32
+ * residual stream after the embedding and after every residual add into
+ * dump (host, [(2*n_layers+1) x T x d_model]). */
+sgs_status sgs_debug_forward(sgs_handle* h, const int32_t* tokens, int32_t T, float* dump);
+
 /* Device-side timing of the last iteration's kernels (CUDA events), ms. */
 sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms);
+/* Per kernel class (0 decode attention K1+K2, 1 GEMMs, 2 prefill attention),
+ * accumulated with SGS_F_KERNEL_TIMING: device ms (CUDA events on the
+ * launching stream), algorithmic bytes and flops, launches.  reset != 0 clears. */
+sgs_status sgs_kernel_stats(sgs_handle* h, int32_t cls, double* ms, double* bytes, double* flops, int64_t* launches,
+                            int32_t reset);
+/* Host<->device bytes moved by the service calls so far (metadata, prompts, tokens). */
+sgs_status sgs_io_bytes(const sgs_handle* h, int64_t* h2d, int64_t* d2h);
+
 /* Count of kernel launches (or graph launches' kernels) issued so far. */
 sgs_status sgs_kernel_launches(const sgs_handle* h, int64_t* n);
 
@@ -223,6 +238,15 @@ sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t*
                               void* q_out, void* kv, int32_t T, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
                               void* stream);
 sgs_status sgs_rope_table(float* host_out, int32_t max_pos, int32_t hd, double theta);
+
+/* a4/K10: causal prefill attention.  q device bf16 [T, nq, hd]; k, v device
+ * bf16 [T, nkv, hd] (contiguous, not paged); prompt p spans rows
+ * [offs[p], offs[p+1]) (offs device int32 [n_prompts+1]); out bf16 [T, nq, hd]. */
+sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
+                                    int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out, void* stream);
+
+/* a10 epilogue: m[t, i] = bf16(SiLU(gu[t, i]) * gu[t, f + i]); gu fp32 [T, 2f], m bf16 [T, f]. */
+sgs_status sgs_op_silu_mul(const float* gu, void* m, int32_t T, int32_t f, void* stream);
 
 /* K9 greedy: ids[r] = argmax_v logits[r, v] (lowest index on ties). */
 sgs_status sgs_op_argmax(const float* logits, int32_t rows, int32_t V, int32_t* ids, void* stream);

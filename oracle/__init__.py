@@ -90,6 +90,8 @@ def _declare(L):
     L.oracle_decoder_forward.argtypes = [P_i32, P_f64, ctypes.c_uint64, P_i32, ctypes.c_int32, ctypes.c_int32,
                                          P_f64]
     L.oracle_decoder_forward.restype = ctypes.c_int32
+    L.oracle_decoder_dump.argtypes = [P_i32, P_f64, ctypes.c_uint64, P_i32, ctypes.c_int32, P_f64]
+    L.oracle_decoder_dump.restype = ctypes.c_int32
     L.oracle_rmsnorm.argtypes = [P_f64, P_f32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P_f64]
     L.oracle_rope.argtypes = [P_f64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
     L.oracle_argmax.argtypes = [P_f32, ctypes.c_int64]
@@ -293,6 +295,19 @@ def rope(v, pos: int, theta: float):
     v = np.array(v, np.float64)
     lib().oracle_rope(_p(v, P_f64), len(v), int(pos), theta)
     return v
+
+
+def decoder_dump(shape, seed: int, tokens):
+    """Residual stream after the embedding and after each residual add: [2L+1, T, d] float64."""
+    toks = np.ascontiguousarray(tokens, np.int32)
+    T = len(toks)
+    ci = np.array([shape.n_layers, shape.d_model, shape.n_q_heads, shape.n_kv_heads, shape.head_dim,
+                   shape.d_ffn, shape.vocab], np.int32)
+    cd = np.array([shape.rms_eps, shape.rope_theta], np.float64)
+    out = np.zeros((2 * shape.n_layers + 1, T, shape.d_model), np.float64)
+    if lib().oracle_decoder_dump(_p(ci, P_i32), _p(cd, P_f64), seed, _p(toks, P_i32), T, _p(out, P_f64)) != 0:
+        raise RuntimeError(lib().oracle_last_error().decode())
+    return out
 
 
 def argmax(x) -> int:

@@ -147,6 +147,20 @@ int32_t oracle_decoder_forward(const int32_t* cfg_i, const double* cfg_d, uint64
   }
 }
 
+// residual stream after the embedding and after every residual add: dump [(2L+1) x T x d]
+int32_t oracle_decoder_dump(const int32_t* cfg_i, const double* cfg_d, uint64_t seed, const int32_t* tokens,
+                            int32_t T, double* dump) {
+  try {
+    ModelCfg c{cfg_i[0], cfg_i[1], cfg_i[2], cfg_i[3], cfg_i[4], cfg_i[5], cfg_i[6], cfg_d[0], cfg_d[1]};
+    std::vector<double> logits((size_t)c.vocab);
+    decoder_forward(c, seed, tokens, T, T - 1, logits.data(), dump);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // y = bf16(x / sqrt(mean(x^2) + eps) * w), rows of x [T x d]
 void oracle_rmsnorm(const double* x, const float* w, int32_t T, int32_t d, double eps, double* y) {
   std::vector<double> h(x, x + (size_t)T * d), out;

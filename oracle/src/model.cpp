@@ -165,8 +165,14 @@ void rope(double* v, int hd, int pos, double theta) {
 }
 
 void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, int T, int first_row,
-                     double* logits) {
+                     double* logits, double* dump) {
   const int d = c.d, hd = c.hd, nq = c.nq, nkv = c.nkv;
+  // dump (optional): residual stream h [T x d] after the embedding and after
+  // each attention / MLP residual add -> (2 L + 1) blocks
+  int n_dump = 0;
+  auto save = [&](const std::vector<double>& h) {
+    if (dump) std::memcpy(dump + (size_t)(n_dump++) * T * d, h.data(), sizeof(double) * (size_t)T * d);
+  };
   std::vector<double> h((size_t)T * d);
   {
     // embedding rows (weights are bf16 values)
@@ -174,6 +180,7 @@ void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, in
       for (int i = 0; i < d; ++i)
         h[(size_t)t * d + i] = weight_value(seed, 0, (uint64_t)tokens[t] * d + i, 0);
   }
+  save(h);
   std::vector<double> x, q, k, v, y, g, u;
   for (int l = 0; l < c.n_layers; ++l) {
     const uint64_t b = 16 + 16 * (uint64_t)l;
@@ -215,6 +222,7 @@ void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, in
       matmul(o, T, nq * hd, Wo, d, y);
       for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
     }
+    save(h);
     auto wn2 = tensor(seed, b + 11, d, 1);
     rmsnorm_bf16(h, T, d, wn2, c.eps, x);
     {
@@ -234,6 +242,7 @@ void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, in
       matmul(g, T, c.ffn, Wd, d, y);
       for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
     }
+    save(h);
   }
   auto wf = tensor(seed, 2, d, 1);
   const int R = T - first_row;

@@ -110,7 +110,7 @@ void rmsnorm_bf16(const std::vector<double>& h, int T, int d, const std::vector<
                   std::vector<double>& x);
 void rope(double* v, int hd, int pos, double theta);
 void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, int T, int first_row,
-                     double* logits /* [(T-first_row) x vocab] */);
+                     double* logits /* [(T-first_row) x vocab] */, double* dump = nullptr);
 
 int32_t argmax_lowest(const float* x, int64_t n);
 void philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

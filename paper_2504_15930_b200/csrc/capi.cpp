@@ -119,9 +119,33 @@ sgs_status sgs_last_logits(sgs_handle* h, float* logits, uint64_t* ids, int32_t*
   return h->eng.last_logits(logits, ids, tok_idx, cap, rows);
 }
 
+sgs_status sgs_debug_forward(sgs_handle* h, const int32_t* tokens, int32_t T, float* dump) {
+  if (!h || !tokens || !dump) return SGS_E_INVAL;
+  return h->eng.debug_forward(tokens, T, dump);
+}
+
 sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms) {
   if (!h || !ms) return SGS_E_INVAL;
   *ms = h->eng.last_ms;
+  return SGS_OK;
+}
+
+sgs_status sgs_kernel_stats(sgs_handle* h, int32_t cls, double* ms, double* bytes, double* flops, int64_t* launches,
+                            int32_t reset) {
+  if (!h || cls < 0 || cls > 3) return SGS_E_INVAL;
+  auto& E = h->eng;
+  if (ms) *ms = E.kstat_ms[cls];
+  if (bytes) *bytes = E.kstat_bytes[cls];
+  if (flops) *flops = E.kstat_flops[cls];
+  if (launches) *launches = E.kstat_n[cls];
+  if (reset) E.kstat_ms[cls] = E.kstat_bytes[cls] = E.kstat_flops[cls] = 0, E.kstat_n[cls] = 0;
+  return SGS_OK;
+}
+
+sgs_status sgs_io_bytes(const sgs_handle* h, int64_t* h2d, int64_t* d2h) {
+  if (!h) return SGS_E_INVAL;
+  if (h2d) *h2d = h->eng.h2d_bytes;
+  if (d2h) *d2h = h->eng.d2h_bytes;
   return SGS_OK;
 }
 
@@ -192,7 +216,7 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
       cudaMemcpyAsync(d_combs, plan.combs.data(), plan.combs.size() * sizeof(sgs::AttnComb), cudaMemcpyHostToDevice,
                       st) != cudaSuccess)
     return SGS_E_CUDA;
-  cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, d_items, (int)plan.items.size(), d_combs,
+  cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, nullptr, d_items, (int)plan.items.size(), d_combs,
                                    (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, out_fp32,
                                    part_o, part_ml, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host plan vectors die here
@@ -219,6 +243,34 @@ sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t*
   if (!qkv || !pos || !cos_sin || !q_out || T < 0) return SGS_E_INVAL;
   return cuda_status(sgs::rope_append(qkv, bias, pos, slot, block_table, max_pages_per_seq, cos_sin, q_out, kv,
                                       nullptr, nullptr, T, nq, nkv, hd, page, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
+                                    int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out, void* stream) {
+  if (!q || !k || !v || !offs || !out || n_prompts < 0 || nq <= 0 || nkv <= 0 || nq % nkv) return SGS_E_INVAL;
+  if (n_prompts == 0) return SGS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<int32_t> ho(n_prompts + 1);
+  if (cudaMemcpyAsync(ho.data(), offs, ho.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return SGS_E_CUDA;
+  std::vector<int32_t> qb;
+  for (int p = 0; p < n_prompts; ++p)
+    for (int b = 0; b < (ho[p + 1] - ho[p] + 63) / 64; ++b) qb.push_back(p), qb.push_back(b);
+  if (qb.empty()) return SGS_OK;
+  int32_t* d_qb = nullptr;
+  if (cudaMallocAsync(&d_qb, qb.size() * 4, st) != cudaSuccess) return SGS_E_CUDA;
+  cudaError_t e = cudaMemcpyAsync(d_qb, qb.data(), qb.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = sgs::attn_prefill(q, k, v, offs, d_qb, (int)qb.size() / 2, nq, nkv, hd, out, st);
+  cudaFreeAsync(d_qb, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_status(e);
+}
+
+sgs_status sgs_op_silu_mul(const float* gu, void* m, int32_t T, int32_t f, void* stream) {
+  if (!gu || !m || T < 0 || f <= 0 || f % 2) return SGS_E_INVAL;
+  return cuda_status(sgs::silu_mul(gu, m, T, f, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 sgs_status sgs_op_argmax(const float* logits, int32_t rows, int32_t V, int32_t* ids, void* stream) {

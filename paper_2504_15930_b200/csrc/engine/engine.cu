@@ -385,9 +385,53 @@ sgs_status Engine::step(sgs_completion* out, int32_t cap, int32_t* n_out) {
   return SGS_OK;
 }
 
+cudaEvent_t Engine::next_event() {
+  if (ev_used_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_used_++];
+}
+
+void Engine::ktic(KRec* r, int cls) {
+  r->cls = -1;
+  if (!(e_.flags & SGS_F_KERNEL_TIMING)) return;
+  r->cls = cls;
+  r->a = next_event();
+  r->b = next_event();
+  cudaEventRecord(r->a, st_);
+}
+
+void Engine::ktoc(KRec* r, double bytes, double flops) {
+  if (r->cls < 0) return;
+  cudaEventRecord(r->b, st_);
+  r->bytes = bytes;
+  r->flops = flops;
+  krec_.push_back(*r);
+}
+
+// after a stream synchronize: fold the iteration's kernel timings into the stats
+cudaError_t Engine::kflush() {
+  for (const KRec& r : krec_) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess) return e;
+    kstat_ms[r.cls] += ms;
+    kstat_bytes[r.cls] += r.bytes;
+    kstat_flops[r.cls] += r.flops;
+    kstat_n[r.cls] += 1;
+  }
+  krec_.clear();
+  ev_used_ = 0;
+  return cudaSuccess;
+}
+
 cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate) {
   const int splits = gemm_auto_splits(N, K, T);
   cudaError_t e;
+  KRec kr;
+  ktic(&kr, 1);
   if (splits > 1) {
     if (!accumulate) {
       e = cudaMemsetAsync(C, 0, (size_t)T * N * 4, st_);
@@ -397,6 +441,8 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
   } else {
     e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_);
   }
+  // algorithmic bytes: weights + activations in + fp32 out (read-modify-write when accumulating)
+  ktoc(&kr, 2.0 * N * K + 2.0 * T * K + (accumulate ? 8.0 : 4.0) * T * N, 2.0 * N * K * T);
   ++launches;
   return e;
 }
@@ -503,6 +549,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_);
   CK(cudaEventRecord(ev0_, st_), "event");
   CK(cudaMemcpyAsync(meta_dev_, meta_host_, meta.size() * 4, cudaMemcpyHostToDevice, st_), "meta H2D");
+  h2d_bytes += (int64_t)meta.size() * 4;
   CK(apply_bt_deltas(bt_, L_.max_pages, MD + o_bt, n_bt, st_), "bt deltas");
   ++launches;
 
@@ -522,6 +569,12 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     const AttnComb* d_combs = reinterpret_cast<const AttnComb*>(MD + o_combs);
     float* part_o = reinterpret_cast<float*>(attn_ws_);
     float* part_ml = part_o + (size_t)std::max(ap.n_parts, 1) * (nq / nkv) * hd;
+    // algorithmic bytes of one decode-attention launch: every cached K and V
+    // element once + q in + o out; flops = 4 nq hd sum(ctx)
+    double sum_ctx = 0;
+    for (int32_t c : dctx) sum_ctx += c;
+    const double attn_bytes = sum_ctx * nkv * hd * 2 * 2 + (double)b * nq * hd * 2 * 2;
+    const double attn_flops = 4.0 * nq * hd * sum_ctx;
     CK(embed(embed_, nullptr, d_slot, last_tok_, h_, b, d, st_), "embed");
     ++launches;
     for (int l = 0; l < m_.n_layers; ++l) {
@@ -531,9 +584,12 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
       CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, b, nq,
                      nkv, hd, e_.page_size, st_),
          "rope_append");
-      CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_items, (int)ap.items.size(), d_combs, (int)ap.combs.size(), nq,
+      KRec kr;
+      ktic(&kr, 0);
+      CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_slot, d_items, (int)ap.items.size(), d_combs, (int)ap.combs.size(), nq,
                      nkv, hd, e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, st_),
          "attn_decode");
+      ktoc(&kr, attn_bytes, attn_flops);
       CK(gemm(Ly.wo, ao_, h_, d, nq * hd, b, true), "gemm o");
       CK(rmsnorm(h_, Ly.n2, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm2");
       CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, b, false), "gemm gate_up");
@@ -562,6 +618,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
        "tokens D2H");
     toff.push_back(off);
     off += s.d;
+    d2h_bytes += (int64_t)s.d * 4;
   }
   const int rows = row_base + n_run;
   if (e_.flags & SGS_F_KEEP_LOGITS) {
@@ -577,6 +634,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   CK(cudaEventRecord(ev1_, st_), "event");
   CK(cudaStreamSynchronize(st_), "iteration sync");
   CK(cudaEventElapsedTime(&last_ms, ev0_, ev1_), "elapsed");
+  CK(kflush(), "kernel timing");
   for (size_t k = 0; k < plan.completed.size(); ++k) {
     const Sample& s = S[plan.completed[k]];
     Completion c{s.id, s.slot, s.admit_iter, s.finish_iter, version,
@@ -590,13 +648,19 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
 sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, const int32_t* d_tokens,
                                  const int32_t* d_pos, const int32_t* d_slot, const int32_t* d_offs,
                                  const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
-                                 const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T) {
+                                 const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump) {
   const int d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn,
             V = m_.vocab;
   const int qkvN = (nq + 2 * nkv) * hd;
   const int np = (int)idx.size();
   CK(embed(embed_, d_tokens, nullptr, nullptr, h_, T, d, st_), "embed");
   ++launches;
+  int n_dump = 0;
+  auto save = [&]() -> cudaError_t {
+    if (!dump) return cudaSuccess;
+    return cudaMemcpyAsync(dump + (size_t)(n_dump++) * T * d, h_, (size_t)T * d * 4, cudaMemcpyDeviceToHost, st_);
+  };
+  CK(save(), "dump");
   for (int l = 0; l < m_.n_layers; ++l) {
     const Layer& Ly = layers_[l];
     CK(rmsnorm(h_, Ly.n1, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm1");
@@ -604,12 +668,17 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, kc_, vc_, T, nq, nkv, hd,
                    e_.page_size, st_),
        "rope_append");
+    KRec kr;
+    ktic(&kr, 2);
     CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
+    ktoc(&kr, 0.0, 0.0);
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
+    CK(save(), "dump");
     CK(rmsnorm(h_, Ly.n2, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm2");
     CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, T, false), "gemm gate_up");
     CK(silu_mul(gu_, mm_, T, f, st_), "silu");
     CK(gemm(Ly.wd, mm_, h_, d, f, T, true), "gemm down");
+    CK(save(), "dump");
     launches += 5;
   }
   CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
@@ -617,6 +686,44 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
   CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
   CK(argmax_rows(lg, np, V, nullptr, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, st_), "argmax");
   launches += 2;
+  return SGS_OK;
+}
+
+// Standalone prefill forward of one prompt in slot 0 (idle handle only) with
+// the residual stream dumped after the embedding and every residual add.
+sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump) {
+  if (null_ || !sched.idle()) {
+    err = "debug_forward needs a device handle with nothing in flight";
+    return SGS_E_STATE;
+  }
+  const int np = (T + e_.page_size - 1) / e_.page_size;
+  if (T < 1 || T > e_.max_prefill_tokens || np > n_pages_ || np > L_.max_pages) {
+    err = "debug_forward: prompt too long";
+    return SGS_E_INVAL;
+  }
+  std::vector<int32_t> meta;
+  for (int k = 0; k < np; ++k) meta.insert(meta.end(), {0, k, k});
+  const size_t o_tok = meta.size();
+  meta.insert(meta.end(), tokens, tokens + T);
+  const size_t o_pos = meta.size();
+  for (int j = 0; j < T; ++j) meta.push_back(j);
+  const size_t o_slot = meta.size();
+  for (int j = 0; j < T; ++j) meta.push_back(0);
+  const size_t o_offs = meta.size();
+  meta.push_back(0), meta.push_back(T);
+  const size_t o_qb = meta.size();
+  for (int b = 0; b < (T + 63) / 64; ++b) meta.push_back(0), meta.push_back(b);
+  const size_t o_last = meta.size();
+  meta.push_back(T - 1), meta.push_back(0), meta.push_back(0);  // last row, pf slot, pf tok
+  std::memcpy(meta_host_, meta.data(), meta.size() * 4);
+  const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_);
+  CK(cudaMemcpyAsync(meta_dev_, meta_host_, meta.size() * 4, cudaMemcpyHostToDevice, st_), "meta");
+  CK(apply_bt_deltas(bt_, L_.max_pages, MD, np, st_), "bt");
+  std::vector<int32_t> idx(1, 0);
+  sgs_status s = prefill_chunk(idx, 0, MD + o_tok, MD + o_pos, MD + o_slot, MD + o_offs, MD + o_qb, (T + 63) / 64,
+                               MD + o_last, MD + o_last + 1, MD + o_last + 2, T, dump);
+  if (s != SGS_OK) return s;
+  CK(cudaStreamSynchronize(st_), "debug sync");
   return SGS_OK;
 }
 

@@ -51,6 +51,7 @@ class Engine {
   sgs_status comm_init(const uint8_t id[128], int rank, int world);
   sgs_status update_weights(int root);
   sgs_status last_logits(float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap, int32_t* rows);
+  sgs_status debug_forward(const int32_t* tokens, int32_t T, float* dump);
 
   static sgs_status layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64_t n_pages, ArenaLayout* L);
 
@@ -58,6 +59,10 @@ class Engine {
   bool poisoned = false;
   Scheduler sched;
   float last_ms = 0.f;
+  // kernel-class timing (SGS_F_KERNEL_TIMING) and I/O accounting
+  double kstat_ms[4] = {0}, kstat_bytes[4] = {0}, kstat_flops[4] = {0};
+  int64_t kstat_n[4] = {0};
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
   int64_t launches = 0;
   int32_t version = 0;
 
@@ -67,9 +72,21 @@ class Engine {
   sgs_status prefill_chunk(const std::vector<int32_t>& idx, int row_base, const int32_t* d_tokens,
                            const int32_t* d_pos, const int32_t* d_slot, const int32_t* d_offs,
                            const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
-                           const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T);
+                           const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump = nullptr);
   cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
   void build_tensor_table();
+  struct KRec {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes, flops;
+  };
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_used_ = 0;
+  std::vector<KRec> krec_;
+  cudaEvent_t next_event();
+  void ktic(KRec* r, int cls);
+  void ktoc(KRec* r, double bytes, double flops);
+  cudaError_t kflush();
 
   sgs_model_cfg m_{};
   sgs_engine_cfg e_{};

@@ -33,7 +33,8 @@ template <int HD>
 __global__ void __launch_bounds__(128, 2)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv,
                        const int32_t* __restrict__ bt, const int32_t* __restrict__ ctx,
-                       const AttnItem* __restrict__ items, int n_items, int nq, int nkv, int max_pages,
+                       const int32_t* __restrict__ row_slot, const AttnItem* __restrict__ items, int n_items,
+                       int nq, int nkv, int max_pages,
                        float scale_log2, void* __restrict__ out, int out_fp32, float* __restrict__ part_o,
                        float* __restrict__ part_ml) {
   constexpr int RC = HD / 8;                 // 16-byte chunks per row
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(128, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = nq / nkv;
   const int L = ctx[it.row];
-  const int32_t* btr = bt + (size_t)it.row * max_pages;
+  const int32_t* btr = bt + (size_t)(row_slot ? row_slot[it.row] : it.row) * max_pages;
   uint8_t* my = smem + (size_t)warp * ATTN_STAGES * STAGE;
 
   if (lane == 0) {
@@ -130,7 +131,8 @@ __global__ void __launch_bounds__(128, 2)
     const float a0 = exp2f(m0 - mn0), a1 = exp2f(m1 - mn1);
     m0 = mn0;
     m1 = mn1;
-    uint32_t pa[4];
+    // P = P_hi + P_lo (two fp16 parts) so the softmax weights keep ~22 bits
+    uint32_t pa[4], pl[4];
     {
       float p[2][4];
 #pragma unroll
@@ -140,17 +142,12 @@ __global__ void __launch_bounds__(128, 2)
         p[t][2] = exp2f(fmaf(sc[t][2], scale_log2, -mn1));
         p[t][3] = exp2f(fmaf(sc[t][3], scale_log2, -mn1));
       }
-      pa[0] = pack_f16x2(p[0][0], p[0][1]);
-      pa[1] = pack_f16x2(p[0][2], p[0][3]);
-      pa[2] = pack_f16x2(p[1][0], p[1][1]);
-      pa[3] = pack_f16x2(p[1][2], p[1][3]);
-      // l accumulates the fp16-rounded weights actually used by the PV product
-      const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&pa[0]));
-      const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&pa[1]));
-      const float2 f2 = __half22float2(*reinterpret_cast<__half2*>(&pa[2]));
-      const float2 f3 = __half22float2(*reinterpret_cast<__half2*>(&pa[3]));
-      l0 = l0 * a0 + (f0.x + f0.y + f2.x + f2.y);
-      l1 = l1 * a1 + (f1.x + f1.y + f3.x + f3.y);
+      split_f16x2(p[0][0], p[0][1], pa[0], pl[0]);
+      split_f16x2(p[0][2], p[0][3], pa[1], pl[1]);
+      split_f16x2(p[1][0], p[1][1], pa[2], pl[2]);
+      split_f16x2(p[1][2], p[1][3], pa[3], pl[3]);
+      l0 = l0 * a0 + ((p[0][0] + p[0][1]) + (p[1][0] + p[1][1]));
+      l1 = l1 * a1 + ((p[0][2] + p[0][3]) + (p[1][2] + p[1][3]));
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -164,8 +161,12 @@ __global__ void __launch_bounds__(128, 2)
       const int ch = 2 * nn + vchk;
       uint32_t v0, v1, v2, v3;
       ldmatrix_x4_trans(v0, v1, v2, v3, vbase + vtok * (HD * 2) + ((ch ^ kv_swz(vtok, RC)) << 4));
-      mma_f16_16816(o[2 * nn], pa, bf16x2_to_f16x2(v0), bf16x2_to_f16x2(v1));
-      mma_f16_16816(o[2 * nn + 1], pa, bf16x2_to_f16x2(v2), bf16x2_to_f16x2(v3));
+      const uint32_t h0 = bf16x2_to_f16x2(v0), h1 = bf16x2_to_f16x2(v1);
+      const uint32_t h2 = bf16x2_to_f16x2(v2), h3 = bf16x2_to_f16x2(v3);
+      mma_f16_16816(o[2 * nn], pa, h0, h1);
+      mma_f16_16816(o[2 * nn], pl, h0, h1);
+      mma_f16_16816(o[2 * nn + 1], pa, h2, h3);
+      mma_f16_16816(o[2 * nn + 1], pl, h2, h3);
     }
     __syncwarp();
     if (lane == 0 && i + ATTN_STAGES < n_my) {
@@ -295,7 +296,7 @@ int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd) {
 
 template <int HD>
 static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx,
-                                 const AttnItem* items, int n_items, int nq, int nkv, int max_pages, void* out,
+                                 const int32_t* row_slot, const AttnItem* items, int n_items, int nq, int nkv, int max_pages, void* out,
                                  int out_fp32, float* part_o, float* part_ml, cudaStream_t stream) {
   constexpr int STAGE = 2 * PAGE_T * HD * 2;
   const size_t ring = (size_t)ATTN_WARPS * ATTN_STAGES * STAGE;
@@ -308,12 +309,13 @@ static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* b
   }
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
   attn_decode_kernel<HD><<<n_items, 128, smem, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx, items,
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx, row_slot, items,
       n_items, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
   return cudaGetLastError();
 }
 
-cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const AttnItem* items,
+cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const int32_t* row_slot,
+                        const AttnItem* items,
                         int n_items, const AttnComb* combs, int n_combs, int nq, int nkv, int hd, int page,
                         int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
                         cudaStream_t stream) {
@@ -323,15 +325,15 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const 
   cudaError_t e;
   switch (hd) {
     case 32:
-      e = launch_decode<32>(q, kv, bt, ctx, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
+      e = launch_decode<32>(q, kv, bt, ctx, row_slot, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
                             stream);
       break;
     case 64:
-      e = launch_decode<64>(q, kv, bt, ctx, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
+      e = launch_decode<64>(q, kv, bt, ctx, row_slot, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
                             stream);
       break;
     case 128:
-      e = launch_decode<128>(q, kv, bt, ctx, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o,
+      e = launch_decode<128>(q, kv, bt, ctx, row_slot, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o,
                              part_ml, stream);
       break;
     default:

@@ -29,7 +29,7 @@ constexpr int GEMM_SMEM_BUDGET = 200 * 1024;
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
-                        int chunks_per_split, int mode, int tmem_cols) {
+                        int chunks_per_split, int mode, int tmem_cols, int n_acc, int acc_stride) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b_bytes = BN * GEMM_BK * 2;
@@ -82,8 +82,13 @@ __global__ void __launch_bounds__(256, 1)
       const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * GEMM_A_BYTES));
       const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_bytes));
 #pragma unroll
+      // k-chunk i accumulates into TMEM accumulator i % n_acc: the tensor-core
+      // fp32 accumulation truncates, so short chains + an IEEE fp32 sum of the
+      // accumulators in the epilogue keep the error at fp32-GEMM level.
+      const uint32_t d = tmem + (uint32_t)((i % n_acc) * acc_stride);
+#pragma unroll
       for (int k = 0; k < GEMM_BK / 16; ++k)  // K = 16 per MMA: advance 32 B inside the swizzle atom
-        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+        umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
       umma_commit(&empty[s]);
     }
     umma_commit(tmem_full);
@@ -93,16 +98,29 @@ __global__ void __launch_bounds__(256, 1)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const int n = m0 + 32 * e + lane;
+    const int used = nk < n_acc ? nk : n_acc;
     for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)c, r);
-      tmem_wait_ld();
+      float acc[16];
+      {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(r[j]);
+      }
+      for (int a = 1; a < used; ++a) {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(a * acc_stride + c), r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[j]);
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int t = n0 + c + j;
         if (t < T) {
           float* p = C + (size_t)t * ldc + n;
-          const float v = __uint_as_float(r[j]);
+          const float v = acc[j];
           if (mode == 0)
             *p = v;
           else if (mode == 1)
@@ -211,14 +229,22 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (stages > 12) stages = 12;
   if (stages > kc) stages = kc < 2 ? 2 : kc;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
-  const int tmem_cols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // accumulator interleave: as many TMEM accumulators as fit (<= 8), each 32-column aligned
+  const int acc_stride = (BN + 31) / 32 * 32;
+  int n_acc = 512 / acc_stride;
+  if (n_acc > 8) n_acc = 8;
+  if (n_acc > per) n_acc = per;
+  if (n_acc < 1) n_acc = 1;
+  int tmem_cols = 32;
+  while (tmem_cols < n_acc * acc_stride) tmem_cols <<= 1;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   dim3 grid(N / GEMM_BM, (T + BN - 1) / BN, splits);
-  gemm_bf16_tc_kernel<<<grid, 256, smem, stream>>>(tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols);
+  gemm_bf16_tc_kernel<<<grid, 256, smem, stream>>>(tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols, n_acc,
+                                                             acc_stride);
   return cudaGetLastError();
 }
 

@@ -28,8 +28,9 @@ struct AttnPlan {
 void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, AttnPlan* plan);
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
 // items/combs are device arrays (already copied); part buffers in workspace.
+// block_table rows are indexed by row_slot[row] (NULL: by row); ctx is per row.
 cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
-                        const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
+                        const int32_t* row_slot, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
                         int hd, int page, int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
                         cudaStream_t stream);
 

@@ -109,17 +109,13 @@ __global__ void __launch_bounds__(128)
         pp[t][2] = mn1 == -INFINITY ? 0.f : exp2f(fmaf(sc[t][2], scale_log2, -mn1));
         pp[t][3] = mn1 == -INFINITY ? 0.f : exp2f(fmaf(sc[t][3], scale_log2, -mn1));
       }
-      uint32_t pa[4];
-      pa[0] = pack_f16x2(pp[0][0], pp[0][1]);
-      pa[1] = pack_f16x2(pp[0][2], pp[0][3]);
-      pa[2] = pack_f16x2(pp[1][0], pp[1][1]);
-      pa[3] = pack_f16x2(pp[1][2], pp[1][3]);
-      const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&pa[0]));
-      const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&pa[1]));
-      const float2 f2 = __half22float2(*reinterpret_cast<__half2*>(&pa[2]));
-      const float2 f3 = __half22float2(*reinterpret_cast<__half2*>(&pa[3]));
-      l0 = l0 * a0 + (f0.x + f0.y + f2.x + f2.y);
-      l1 = l1 * a1 + (f1.x + f1.y + f3.x + f3.y);
+      uint32_t pa[4], pl[4];  // P = P_hi + P_lo in fp16 (~22 significant bits)
+      split_f16x2(pp[0][0], pp[0][1], pa[0], pl[0]);
+      split_f16x2(pp[0][2], pp[0][3], pa[1], pl[1]);
+      split_f16x2(pp[1][0], pp[1][1], pa[2], pl[2]);
+      split_f16x2(pp[1][2], pp[1][3], pa[3], pl[3]);
+      l0 = l0 * a0 + ((pp[0][0] + pp[0][1]) + (pp[1][0] + pp[1][1]));
+      l1 = l1 * a1 + ((pp[0][2] + pp[0][3]) + (pp[1][2] + pp[1][3]));
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         o[nt][0] *= a0;
@@ -133,8 +129,12 @@ __global__ void __launch_bounds__(128)
         const int ch = 2 * nn + vchk;
         uint32_t v0, v1, v2, v3;
         ldmatrix_x4_trans(v0, v1, v2, v3, vbase + vr * (HD * 2) + ((ch ^ kv_swz(vr, RC)) << 4));
-        mma_f16_16816(o[2 * nn], pa, bf16x2_to_f16x2(v0), bf16x2_to_f16x2(v1));
-        mma_f16_16816(o[2 * nn + 1], pa, bf16x2_to_f16x2(v2), bf16x2_to_f16x2(v3));
+        const uint32_t h0 = bf16x2_to_f16x2(v0), h1 = bf16x2_to_f16x2(v1);
+        const uint32_t h2 = bf16x2_to_f16x2(v2), h3 = bf16x2_to_f16x2(v3);
+        mma_f16_16816(o[2 * nn], pa, h0, h1);
+        mma_f16_16816(o[2 * nn], pl, h0, h1);
+        mma_f16_16816(o[2 * nn + 1], pa, h2, h3);
+        mma_f16_16816(o[2 * nn + 1], pl, h2, h3);
       }
     }
   }

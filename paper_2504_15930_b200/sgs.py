@@ -17,6 +17,7 @@ STATUS = {0: "SGS_OK", -1: "SGS_E_INVAL", -2: "SGS_E_NOMEM", -3: "SGS_E_STATE", 
 DISPATCH = {"skew": 0, "round_robin": 1, "random": 2}
 F_KEEP_LOGITS = 1
 F_NO_GRAPHS = 2
+F_KERNEL_TIMING = 4
 
 # every symbol include/sgs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
@@ -25,7 +26,7 @@ EXPORTS = [
     "sgs_weight_version", "sgs_trace", "sgs_trace_clear", "sgs_last_logits", "sgs_last_iter_ms",
     "sgs_kernel_launches", "sgs_fit_profile", "sgs_dispatch_plan", "sgs_attn_workspace_bytes",
     "sgs_op_decode_attention", "sgs_op_gemm", "sgs_op_rmsnorm", "sgs_op_rope_append", "sgs_rope_table",
-    "sgs_op_argmax",
+    "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
 ]
 
 
@@ -115,6 +116,11 @@ def _declare(L):
     L.sgs_op_rope_append.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
     L.sgs_rope_table.argtypes = [P(ctypes.c_float), i32, i32, ctypes.c_double]
     L.sgs_op_argmax.argtypes = [vp, i32, i32, vp, vp]
+    L.sgs_kernel_stats.argtypes = [vp, i32, P(ctypes.c_double), P(ctypes.c_double), P(ctypes.c_double), P(i64), i32]
+    L.sgs_io_bytes.argtypes = [vp, P(i64), P(i64)]
+    L.sgs_op_silu_mul.argtypes = [vp, vp, i32, i32, vp]
+    L.sgs_debug_forward.argtypes = [vp, P(i32), i32, P(ctypes.c_float)]
+    L.sgs_op_prefill_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
     for name in EXPORTS:
         f = getattr(L, name)
         if name not in ("sgs_destroy", "sgs_last_error", "sgs_attn_workspace_bytes"):
@@ -300,10 +306,29 @@ class Instance:
                                      ctypes.byref(rows)), self.h)
         return lg, ids, tk
 
+    def debug_forward(self, tokens) -> np.ndarray:
+        """Residual stream after the embedding and each residual add: [2L+1, T, d] fp32."""
+        toks = np.ascontiguousarray(tokens, np.int32)
+        out = np.zeros((2 * self.shape.n_layers + 1, len(toks), self.shape.d_model), np.float32)
+        _check(lib().sgs_debug_forward(self.h, _i32p(toks), len(toks),
+                                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))), self.h)
+        return out
+
     def last_iter_ms(self) -> float:
         v = ctypes.c_float()
         _check(lib().sgs_last_iter_ms(self.h, ctypes.byref(v)), self.h)
         return v.value
+
+    def kernel_stats(self, cls: int, reset: bool = False):
+        ms, by, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(lib().sgs_kernel_stats(self.h, cls, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(fl),
+                                      ctypes.byref(n), int(reset)), self.h)
+        return dict(ms=ms.value, bytes=by.value, flops=fl.value, launches=n.value)
+
+    def io_bytes(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().sgs_io_bytes(self.h, ctypes.byref(a), ctypes.byref(b)), self.h)
+        return a.value, b.value
 
     def kernel_launches(self) -> int:
         v = ctypes.c_int64()
@@ -380,9 +405,21 @@ def op_rope_append(qkv, bias, pos, slot, block_table, cos_sin, q_out, kv, nq, nk
                                     _ptr(cos_sin), _ptr(q_out), _ptr(kv), T, nq, nkv, hd, page, _cur_stream(qkv)))
 
 
+def op_silu_mul(gu, m):
+    T, f = m.shape
+    _check(lib().sgs_op_silu_mul(_ptr(gu), _ptr(m), T, f, _cur_stream(gu)))
+
+
 def op_argmax(logits, ids):
     rows, V = logits.shape
     _check(lib().sgs_op_argmax(_ptr(logits), rows, V, _ptr(ids), _cur_stream(logits)))
+
+
+def op_prefill_attention(q, k, v, offs, out):
+    T, nq, hd = q.shape
+    nkv = k.shape[1]
+    _check(lib().sgs_op_prefill_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(offs), offs.numel() - 1, nq, nkv, hd,
+                                          _ptr(out), _cur_stream(q)))
 
 
 def op_decode_attention(q, kv, block_table, ctx, out, page=16, split_pages=0, workspace=None):

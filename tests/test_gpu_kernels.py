@@ -28,7 +28,7 @@ def _bf(shape, seed, scale=1.0):
     (4608, 3584, 37, 1, 0),       # ragged b, automatic splits
     (3584, 18944, 256, 2, 1),     # 7B down at b = 256 (+= residual)
     (1024, 512, 1000, 0, 1),      # prefill-shaped: several N tiles + ragged tail
-    (152064 // 16, 3584, 200, 0, 1),
+    (9472, 3584, 200, 0, 1),      # 74 N tiles (half-wave of 148 SMs)
 ])
 def test_gemm_vs_fp64(sgs, N, K, T, mode, splits):
     W = _bf((N, K), 1, 0.02).cuda()
@@ -199,3 +199,24 @@ def test_argmax_vs_oracle(sgs):
     sgs.op_argmax(torch.from_numpy(x).cuda(), ids)
     torch.cuda.synchronize()
     assert ids.cpu().tolist() == [oracle.argmax(r) for r in x]
+
+
+@pytest.mark.parametrize("nq,nkv,hd,lens", [(4, 2, 32, [16, 1, 40, 129]), (28, 4, 128, [512, 70, 1, 200])])
+def test_prefill_attention_vs_fp64(sgs, nq, nkv, hd, lens):
+    T = sum(lens)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    q, k, v = _bf((T, nq, hd), 1), _bf((T, nkv, hd), 2), _bf((T, nkv, hd), 3)
+    out = torch.zeros(T, nq, hd, dtype=torch.bfloat16, device="cuda")
+    sgs.op_prefill_attention(q.cuda(), k.cuda(), v.cuda(), torch.from_numpy(offs).cuda(), out)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    rng = np.random.default_rng(0)
+    for p, L in enumerate(lens):
+        for t in sorted(set([0, L - 1] + rng.integers(0, L, 6).tolist())):
+            r = offs[p] + t
+            ref = oracle.attention(q[r].float().numpy(), k[offs[p]:r + 1].float().numpy(),
+                                   v[offs[p]:r + 1].float().numpy())
+            refb = torch.from_numpy(ref).float().to(torch.bfloat16).float().numpy()
+            # bf16 output: within 1e-3 relative of the fp64 result plus one bf16 rounding
+            err = np.abs(got[r] - ref).max(-1) / np.abs(ref).max(-1)
+            assert err.max() <= 1e-3 + 2 ** -8, (p, t, float(err.max()))
