@@ -151,6 +151,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--prompts-per-gpu", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--max-out", type=int, default=None, help="cap forced lengths (profiling runs only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -168,6 +169,9 @@ def main():
         dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
         pg = dist
     cfg = workload.CONFIGS[args.config]
+    if args.max_out:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, max_out=args.max_out, median_out=min(cfg.median_out, args.max_out // 4))
     shape = workload.MODELS[cfg.model]
     per_gpu = args.prompts_per_gpu or cfg.n_prompts
     n_total = per_gpu * world

@@ -64,7 +64,9 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->off_hist = take(B * (int64_t)(e.max_ctx + 1) * 4);
   // per-iteration metadata: bt deltas, prefill tokens/pos/slot, decode rows, attention work lists
   const int64_t max_items = 2 * 2 * 148 + 2 * B * nkv + 64;
-  L->meta_bytes = align_up(4 * (3 * (B * max_pages + B) + 3 * tmax + 8 * B + 2 * (tmax / 64 + B) + 16 * B) +
+  // prefill tokens of one iteration: up to B admitted prompts of <= min(max_ctx, prefill chunk) tokens
+  const int64_t adm_tok = B * std::min<int64_t>(e.max_ctx, pf);
+  L->meta_bytes = align_up(4 * (3 * (B * max_pages + B) + 3 * adm_tok + 8 * B + 2 * (adm_tok / 64 + 2 * B) + 16 * B) +
                                max_items * (int64_t)(sizeof(AttnItem) + sizeof(AttnComb)) + 4096,
                            256);
   L->off_meta = take(L->meta_bytes);

@@ -228,25 +228,60 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-__global__ void attn_combine_kernel(const AttnComb* __restrict__ combs, int n_combs, int nq, int nkv, int hd,
-                                    const float* __restrict__ part_o, const float* __restrict__ part_ml,
-                                    void* __restrict__ out, int out_fp32) {
+constexpr int ATTN_MAX_PARTS = 64;  // the planner never splits a (row, kv head) into more parts
+
+// LSE merge of the split-K partials of one (row, kv head): the per-part
+// weights 2^(m_j - M) and the denominator are computed once per row into
+// shared memory (one warp per query row), then every output element sums its
+// column over the parts with independent, coalesced loads.
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __restrict__ combs, int n_combs, int nq,
+                                                           int nkv, int hd, const float* __restrict__ part_o,
+                                                           const float* __restrict__ part_ml,
+                                                           void* __restrict__ out, int out_fp32) {
   if ((int)blockIdx.x >= n_combs) return;
+  __shared__ float w[16][ATTN_MAX_PARTS];
+  __shared__ float inv_l[16];
   const AttnComb c = combs[blockIdx.x];
   const int g = nq / nkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < g; r += blockDim.x >> 5) {
+    float m[2], l[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int j = lane + 32 * k;
+      const bool ok = j < c.nparts;
+      const size_t pj = ((size_t)(c.part0 + (ok ? j : 0)) * g + r) * 2;
+      m[k] = ok ? part_ml[pj] : -INFINITY;
+      l[k] = ok ? part_ml[pj + 1] : 0.f;
+    }
+    const float M = warp_max(fmaxf(m[0], m[1]));
+    float L = 0.f;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int j = lane + 32 * k;
+      const float f = j < c.nparts ? exp2f(m[k] - M) : 0.f;
+      if (j < ATTN_MAX_PARTS) w[r][j] = f;
+      L += f * l[k];
+    }
+    L = warp_sum(L);
+    if (lane == 0) inv_l[r] = 1.f / L;
+  }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < g * hd; idx += blockDim.x) {
     const int r = idx / hd, e = idx % hd;
-    float M = -INFINITY;
-    for (int j = 0; j < c.nparts; ++j) M = fmaxf(M, part_ml[((size_t)(c.part0 + j) * g + r) * 2]);
-    float so = 0.f, sl = 0.f;
-    for (int j = 0; j < c.nparts; ++j) {
-      const size_t pj = (size_t)(c.part0 + j) * g + r;
-      const float f = exp2f(part_ml[pj * 2] - M);
-      so += f * part_o[pj * hd + e];
-      sl += f * part_ml[pj * 2 + 1];
+    const float* po = part_o + ((size_t)c.part0 * g + r) * hd + e;
+    const size_t stride = (size_t)g * hd;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int j = 0;
+    for (; j + 4 <= c.nparts; j += 4) {
+      s0 += w[r][j] * po[j * stride];
+      s1 += w[r][j + 1] * po[(j + 1) * stride];
+      s2 += w[r][j + 2] * po[(j + 2) * stride];
+      s3 += w[r][j + 3] * po[(j + 3) * stride];
     }
+    for (; j < c.nparts; ++j) s0 += w[r][j] * po[j * stride];
+    const float v = ((s0 + s1) + (s2 + s3)) * inv_l[r];
     const size_t oi = ((size_t)c.row * nq + (size_t)c.kvh * g + r) * hd + e;
-    const float v = so / sl;
     if (out_fp32)
       reinterpret_cast<float*>(out)[oi] = v;
     else
@@ -263,14 +298,15 @@ void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, At
   for (int i = 0; i < b; ++i) total += (int64_t)((ctx[i] + page - 1) / page) * nkv;
   int chunk = split_pages;
   if (chunk <= 0) {
-    // aim for ~2 waves of 2 CTAs per SM (148 SMs); at least one page per warp
-    const int64_t target = 2 * 2 * 148;
-    chunk = (int)std::max<int64_t>(ATTN_WARPS, (total + target - 1) / target);
+    // about one wave of 2 CTAs per SM (148 SMs), at least two pages per warp
+    const int64_t target = 2 * 148;
+    chunk = (int)std::max<int64_t>(2 * ATTN_WARPS, (total + target - 1) / target);
   }
   for (int i = 0; i < b; ++i) {
     const int np = (ctx[i] + page - 1) / page;
     if (np == 0) continue;
-    const int nch = (np + chunk - 1) / chunk;
+    int nch = (np + chunk - 1) / chunk;
+    if (nch > ATTN_MAX_PARTS) nch = ATTN_MAX_PARTS;
     for (int h = 0; h < nkv; ++h) {
       if (nch == 1) {
         plan->items.push_back(AttnItem{i, h, 0, np, -1});

@@ -24,7 +24,9 @@ struct AttnPlan {
   std::vector<AttnComb> combs;
   int n_parts = 0;
 };
-// Split-K plan over pages: rows with more than `chunk` pages are split.
+// Split-K plan over pages: rows with more than `chunk` pages are split (at
+// most 64 parts per row and kv head).  The item count is bounded by
+// 2*148 + 2*b*nkv (+ the split_pages override).
 void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, AttnPlan* plan);
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
 // items/combs are device arrays (already copied); part buffers in workspace.
