@@ -216,7 +216,7 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
       cudaMemcpyAsync(d_combs, plan.combs.data(), plan.combs.size() * sizeof(sgs::AttnComb), cudaMemcpyHostToDevice,
                       st) != cudaSuccess)
     return SGS_E_CUDA;
-  cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, nullptr, d_items, (int)plan.items.size(), d_combs,
+  cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, nullptr, nullptr, d_items, (int)plan.items.size(), d_combs,
                                    (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, out_fp32,
                                    part_o, part_ml, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host plan vectors die here

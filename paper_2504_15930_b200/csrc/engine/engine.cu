@@ -57,17 +57,23 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->off_ao = take(tmax * nq * hd * 2);
   L->off_gu = take(tmax * 2 * f * 4);
   L->off_mm = take(tmax * f * 2);
-  L->off_logits = take(B * V * 4);
+  // decode rows [0, Bpad) (CUDA-graph buckets pad to 16), prefill rows after them
+  const int64_t Bpad = (B + 15) / 16 * 16;
+  L->off_logits = take((Bpad + B) * V * 4);
   L->off_rope = take((int64_t)(e.max_ctx + 1) * (hd / 2) * 2 * 4);
   L->off_bt = take(B * max_pages * 4);
   L->off_last = take(B * 4);
   L->off_hist = take(B * (int64_t)(e.max_ctx + 1) * 4);
   // per-iteration metadata: bt deltas, prefill tokens/pos/slot, decode rows, attention work lists
-  const int64_t max_items = 2 * 2 * 148 + 2 * B * nkv + 64;
+  // attention work list bound of attn_plan: 2*148 + b*nkv (+ slack)
+  const int64_t max_items = 2 * 148 + Bpad * nkv + 64;
+  // fixed decode region (graph-replayable): counts[4] | slot,pos,ctx,tok [Bpad] | combs | items
+  L->meta_dec_bytes = align_up(4 * (4 + 4 * Bpad) + max_items * (int64_t)(sizeof(AttnItem) + sizeof(AttnComb)), 256);
   // prefill tokens of one iteration: up to B admitted prompts of <= min(max_ctx, prefill chunk) tokens
   const int64_t adm_tok = B * std::min<int64_t>(e.max_ctx, pf);
-  L->meta_bytes = align_up(4 * (3 * (B * max_pages + B) + 3 * adm_tok + 8 * B + 2 * (adm_tok / 64 + 2 * B) + 16 * B) +
-                               max_items * (int64_t)(sizeof(AttnItem) + sizeof(AttnComb)) + 4096,
+  L->meta_bytes = L->meta_dec_bytes +
+                  align_up(4 * (3 * (B * max_pages + B) + 3 * adm_tok + 8 * B + 2 * (adm_tok / 64 + 2 * B) + 16 * B) +
+                               4096,
                            256);
   L->off_meta = take(L->meta_bytes);
   L->attn_bytes = max_items * (nq / nkv) * (hd + 2) * 4;
@@ -400,32 +406,39 @@ void Engine::ktic(KRec* r, int cls) {
   r->cls = -1;
   if (!(e_.flags & SGS_F_KERNEL_TIMING)) return;
   r->cls = cls;
-  r->a = next_event();
-  r->b = next_event();
-  cudaEventRecord(r->a, st_);
+  if (rec_target_) {  // capturing: events owned by the graph
+    cudaEventCreate(&r->a);
+    cudaEventCreate(&r->b);
+  } else {
+    r->a = next_event();
+    r->b = next_event();
+  }
+  // inside a capture the record must be an external event-record node to be replayed
+  cudaEventRecordWithFlags(r->a, st_, rec_target_ ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 
-void Engine::ktoc(KRec* r, double bytes, double flops) {
+void Engine::ktoc(KRec* r, double bfix, double brow, double frow, int rows) {
   if (r->cls < 0) return;
-  cudaEventRecord(r->b, st_);
-  r->bytes = bytes;
-  r->flops = flops;
-  krec_.push_back(*r);
+  cudaEventRecordWithFlags(r->b, st_, rec_target_ ? cudaEventRecordExternal : cudaEventRecordDefault);
+  r->bfix = bfix;
+  r->brow = brow;
+  r->frow = frow;
+  r->rows = rec_target_ ? -1 : rows;
+  (rec_target_ ? *rec_target_ : krec_).push_back(*r);
 }
 
-// after a stream synchronize: fold the iteration's kernel timings into the stats
-cudaError_t Engine::kflush() {
-  for (const KRec& r : krec_) {
+// after a stream synchronize: fold kernel timings into the stats
+cudaError_t Engine::kflush(const std::vector<KRec>& recs, int rows) {
+  for (const KRec& r : recs) {
     float ms = 0.f;
     cudaError_t e = cudaEventElapsedTime(&ms, r.a, r.b);
     if (e != cudaSuccess) return e;
+    const int n = r.rows < 0 ? rows : r.rows;
     kstat_ms[r.cls] += ms;
-    kstat_bytes[r.cls] += r.bytes;
-    kstat_flops[r.cls] += r.flops;
+    kstat_bytes[r.cls] += r.bfix < 0 ? cur_attn_bytes_ : r.bfix + r.brow * n;
+    kstat_flops[r.cls] += r.bfix < 0 ? cur_attn_flops_ : r.frow * n;
     kstat_n[r.cls] += 1;
   }
-  krec_.clear();
-  ev_used_ = 0;
   return cudaSuccess;
 }
 
@@ -443,8 +456,8 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
   } else {
     e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_);
   }
-  // algorithmic bytes: weights + activations in + fp32 out (read-modify-write when accumulating)
-  ktoc(&kr, 2.0 * N * K + 2.0 * T * K + (accumulate ? 8.0 : 4.0) * T * N, 2.0 * N * K * T);
+  // algorithmic bytes: weights + per row activations in + fp32 out (read-modify-write when accumulating)
+  ktoc(&kr, 2.0 * N * K, 2.0 * K + (accumulate ? 8.0 : 4.0) * N, 2.0 * N * K, T);
   ++launches;
   return e;
 }
@@ -518,40 +531,55 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     c.row_base = row_base;
     row_base += (int)c.idx.size();
   }
-  // decode rows (ascending slot)
-  std::vector<int32_t> dslot, dpos, dctx, dtok;
-  for (int32_t i : plan.running) {
-    const Sample& s = S[i];
-    const int j = s.produced - 1;  // tokens generated before this iteration (plan already counted this one)
-    dslot.push_back(s.slot);
-    dpos.push_back(s.P + j - 1);
-    dctx.push_back(s.P + j);
-    dtok.push_back(j);
+  // ---------------- decode rows (ascending slot) -> fixed region at the start of the metadata
+  const int Bpad = (e_.max_batch + 15) / 16 * 16;
+  const int Bk = (n_run + 15) / 16 * 16;  // CUDA-graph bucket; rows [n_run, Bk) are inert (slot -1)
+  int32_t* D = reinterpret_cast<int32_t*>(meta_host_);
+  int32_t *dslot = D + 4, *dpos = dslot + Bpad, *dctx = dpos + Bpad, *dtok = dctx + Bpad;
+  for (int r = 0; r < Bk; ++r) {
+    if (r < n_run) {
+      const Sample& s = S[plan.running[r]];
+      const int j = s.produced - 1;  // tokens generated before this iteration (plan already counted this one)
+      dslot[r] = s.slot, dpos[r] = s.P + j - 1, dctx[r] = s.P + j, dtok[r] = j;
+    } else {
+      dslot[r] = -1, dpos[r] = 0, dctx[r] = 1, dtok[r] = 0;
+    }
   }
-  const size_t o_dslot = put(dslot.data(), dslot.size());
-  const size_t o_dpos = put(dpos.data(), dpos.size());
-  const size_t o_dctx = put(dctx.data(), dctx.size());
-  const size_t o_dtok = put(dtok.data(), dtok.size());
   AttnPlan ap;
-  attn_plan(dctx.data(), n_run, nkv, e_.page_size, 0, &ap);
+  attn_plan(dctx, n_run, nkv, e_.page_size, 0, &ap);
   if ((int)ap.items.size() > L_.max_items || ap.n_parts > L_.max_items) {
     err = "attention work list exceeds workspace";
     poisoned = true;
     return SGS_E_NOMEM;
   }
-  while (meta.size() % 4) meta.push_back(0);
-  const size_t o_items = put(reinterpret_cast<const int32_t*>(ap.items.data()), ap.items.size() * 5);
-  const size_t o_combs = put(reinterpret_cast<const int32_t*>(ap.combs.data()), ap.combs.size() * 4);
-  if ((int64_t)meta.size() * 4 > L_.meta_bytes) {
+  D[0] = (int32_t)ap.items.size(), D[1] = (int32_t)ap.combs.size(), D[2] = n_run, D[3] = 0;
+  AttnComb* hcombs = reinterpret_cast<AttnComb*>(D + 4 + 4 * Bpad);
+  AttnItem* hitems = reinterpret_cast<AttnItem*>(hcombs + L_.max_items);
+  std::memcpy(hcombs, ap.combs.data(), ap.combs.size() * sizeof(AttnComb));
+  std::memcpy(hitems, ap.items.data(), ap.items.size() * sizeof(AttnItem));
+  const size_t dec_used = (uint8_t*)(hitems + ap.items.size()) - meta_host_;
+  {
+    double sum_ctx = 0;
+    for (int r = 0; r < n_run; ++r) sum_ctx += dctx[r];
+    // algorithmic bytes of one decode-attention launch: every cached K and V
+    // element once + q in + o out (SURVEY §8d); flops = 4 nq hd sum(ctx)
+    cur_attn_bytes_ = sum_ctx * nkv * hd * 2 * 2 + (double)n_run * nq * hd * 2 * 2;
+    cur_attn_flops_ = 4.0 * nq * hd * sum_ctx;
+  }
+  if ((int64_t)meta.size() * 4 > L_.meta_bytes - L_.meta_dec_bytes) {
     err = "iteration metadata exceeds the staging buffer";
     poisoned = true;
     return SGS_E_NOMEM;
   }
-  std::memcpy(meta_host_, meta.data(), meta.size() * 4);
-  const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_);
+  std::memcpy(meta_host_ + L_.meta_dec_bytes, meta.data(), meta.size() * 4);
+  const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_ + L_.meta_dec_bytes);
   CK(cudaEventRecord(ev0_, st_), "event");
-  CK(cudaMemcpyAsync(meta_dev_, meta_host_, meta.size() * 4, cudaMemcpyHostToDevice, st_), "meta H2D");
-  h2d_bytes += (int64_t)meta.size() * 4;
+  if (n_run > 0) CK(cudaMemcpyAsync(meta_dev_, meta_host_, dec_used, cudaMemcpyHostToDevice, st_), "meta H2D");
+  if (!meta.empty())
+    CK(cudaMemcpyAsync(meta_dev_ + L_.meta_dec_bytes, meta_host_ + L_.meta_dec_bytes, meta.size() * 4,
+                       cudaMemcpyHostToDevice, st_),
+       "meta H2D");
+  h2d_bytes += (int64_t)meta.size() * 4 + (n_run > 0 ? (int64_t)dec_used : 0);
   CK(apply_bt_deltas(bt_, L_.max_pages, MD + o_bt, n_bt, st_), "bt deltas");
   ++launches;
 
@@ -561,49 +589,10 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
                                  MD + c.o_qb, c.nqb, MD + c.o_last, MD + c.o_pfslot, MD + c.o_pftok, c.T);
     if (s != SGS_OK) return s;
   }
-  // ---------------- decode
+  // ---------------- decode (graph replay per bucket)
   if (n_run > 0) {
-    const int b = n_run;
-    const int32_t* d_slot = MD + o_dslot;
-    const int32_t* d_pos = MD + o_dpos;
-    const int32_t* d_ctx = MD + o_dctx;
-    const AttnItem* d_items = reinterpret_cast<const AttnItem*>(MD + o_items);
-    const AttnComb* d_combs = reinterpret_cast<const AttnComb*>(MD + o_combs);
-    float* part_o = reinterpret_cast<float*>(attn_ws_);
-    float* part_ml = part_o + (size_t)std::max(ap.n_parts, 1) * (nq / nkv) * hd;
-    // algorithmic bytes of one decode-attention launch: every cached K and V
-    // element once + q in + o out (SURVEY §8d); flops = 4 nq hd sum(ctx)
-    double sum_ctx = 0;
-    for (int32_t c : dctx) sum_ctx += c;
-    const double attn_bytes = sum_ctx * nkv * hd * 2 * 2 + (double)b * nq * hd * 2 * 2;
-    const double attn_flops = 4.0 * nq * hd * sum_ctx;
-    CK(embed(embed_, nullptr, d_slot, last_tok_, h_, b, d, st_), "embed");
-    ++launches;
-    for (int l = 0; l < m_.n_layers; ++l) {
-      const Layer& Ly = layers_[l];
-      CK(rmsnorm(h_, Ly.n1, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm1");
-      CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, b, false), "gemm qkv");
-      CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, b, nq,
-                     nkv, hd, e_.page_size, st_),
-         "rope_append");
-      KRec kr;
-      ktic(&kr, 0);
-      CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_slot, d_items, (int)ap.items.size(), d_combs, (int)ap.combs.size(), nq,
-                     nkv, hd, e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, st_),
-         "attn_decode");
-      ktoc(&kr, attn_bytes, attn_flops);
-      CK(gemm(Ly.wo, ao_, h_, d, nq * hd, b, true), "gemm o");
-      CK(rmsnorm(h_, Ly.n2, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm2");
-      CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, b, false), "gemm gate_up");
-      CK(silu_mul(gu_, mm_, b, f, st_), "silu");
-      CK(gemm(Ly.wd, mm_, h_, d, f, b, true), "gemm down");
-      launches += 5 + (ap.combs.empty() ? 0 : 1);
-    }
-    CK(rmsnorm(h_, nf_, x_, nullptr, b, d, m_.rms_eps, st_), "rmsnorm f");
-    float* lg = logits_ + (size_t)row_base * V;
-    CK(gemm(lm_head_, x_, lg, V, d, b, false), "gemm lm_head");
-    CK(argmax_rows(lg, b, V, nullptr, d_slot, MD + o_dtok, last_tok_, hist_, max_gen_, st_), "argmax");
-    launches += 2;
+    sgs_status s = run_decode(n_run);
+    if (s != SGS_OK) return s;
   }
   // ---------------- completions: D2H of their tokens
   int64_t off = 0;
@@ -625,8 +614,15 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   const int rows = row_base + n_run;
   if (e_.flags & SGS_F_KEEP_LOGITS) {
     kept_logits_.resize((size_t)rows * V);
-    if (rows) CK(cudaMemcpyAsync(kept_logits_.data(), logits_, (size_t)rows * V * 4, cudaMemcpyDeviceToHost, st_),
-                 "logits D2H");
+    // prefill rows live after the Bpad decode rows of the logits buffer
+    if (row_base)
+      CK(cudaMemcpyAsync(kept_logits_.data(), logits_ + (size_t)Bpad * V, (size_t)row_base * V * 4,
+                         cudaMemcpyDeviceToHost, st_),
+         "logits D2H");
+    if (n_run)
+      CK(cudaMemcpyAsync(kept_logits_.data() + (size_t)row_base * V, logits_, (size_t)n_run * V * 4,
+                         cudaMemcpyDeviceToHost, st_),
+         "logits D2H");
     kept_ids_.clear();
     kept_tok_.clear();
     for (auto& c : chunks)
@@ -636,7 +632,13 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   CK(cudaEventRecord(ev1_, st_), "event");
   CK(cudaStreamSynchronize(st_), "iteration sync");
   CK(cudaEventElapsedTime(&last_ms, ev0_, ev1_), "elapsed");
-  CK(kflush(), "kernel timing");
+  CK(kflush(krec_, n_run), "kernel timing");
+  krec_.clear();
+  ev_used_ = 0;
+  if (n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS)) {
+    const DecodeGraph& g = graphs_[(n_run + 15) / 16];
+    if (g.exec) CK(kflush(g.recs, n_run), "kernel timing");
+  }
   for (size_t k = 0; k < plan.completed.size(); ++k) {
     const Sample& s = S[plan.completed[k]];
     Completion c{s.id, s.slot, s.admit_iter, s.finish_iter, version,
@@ -644,6 +646,82 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     ready_.push_back(std::move(c));
   }
   (void)n_adm;
+  return SGS_OK;
+}
+
+// The decode step for a bucket of Bk rows: every pointer is fixed (metadata
+// region at meta_dev_, scratch buffers) and the attention work counts are
+// read on the device, so the same launch sequence can be captured once per
+// bucket and replayed.  Rows >= the real batch carry slot -1 and are inert.
+sgs_status Engine::decode_body(int Bk) {
+  const int d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn,
+            V = m_.vocab;
+  const int qkvN = (nq + 2 * nkv) * hd;
+  const int Bpad = (e_.max_batch + 15) / 16 * 16;
+  const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_);
+  const int32_t* counts = MD;
+  const int32_t* d_slot = MD + 4;
+  const int32_t* d_pos = d_slot + Bpad;
+  const int32_t* d_ctx = d_pos + Bpad;
+  const int32_t* d_tok = d_ctx + Bpad;
+  const AttnComb* d_combs = reinterpret_cast<const AttnComb*>(d_tok + Bpad);
+  const AttnItem* d_items = reinterpret_cast<const AttnItem*>(d_combs + L_.max_items);
+  float* part_o = reinterpret_cast<float*>(attn_ws_);
+  float* part_ml = part_o + (size_t)L_.max_items * (nq / nkv) * hd;
+  const int cap_items = std::min(L_.max_items, 2 * 148 + Bk * nkv + 64);
+  const int cap_combs = Bk * nkv;
+  CK(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), "embed");
+  ++launches;
+  for (int l = 0; l < m_.n_layers; ++l) {
+    const Layer& Ly = layers_[l];
+    CK(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm1");
+    CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false), "gemm qkv");
+    CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, Bk, nq, nkv,
+                   hd, e_.page_size, st_),
+       "rope_append");
+    KRec kr;
+    ktic(&kr, 0);
+    CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_slot, counts, d_items, cap_items, d_combs, cap_combs, nq, nkv, hd,
+                   e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, st_),
+       "attn_decode");
+    ktoc(&kr, -1.0, 0.0, 0.0, 0);
+    CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
+    CK(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm2");
+    CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, Bk, false), "gemm gate_up");
+    CK(silu_mul(gu_, mm_, Bk, f, st_), "silu");
+    CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
+    launches += 6;
+  }
+  CK(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm f");
+  CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
+  CK(argmax_rows(logits_, Bk, V, nullptr, d_slot, d_tok, last_tok_, hist_, max_gen_, st_), "argmax");
+  launches += 2;
+  return SGS_OK;
+}
+
+sgs_status Engine::run_decode(int b) {
+  const int Bk = (b + 15) / 16 * 16;
+  if (e_.flags & SGS_F_NO_GRAPHS) return decode_body(Bk);
+  if (graphs_.empty()) graphs_.resize((e_.max_batch + 15) / 16 + 1);
+  DecodeGraph& g = graphs_[Bk / 16];
+  if (!g.exec) {
+    if (g.uses++ == 0) return decode_body(Bk);  // first use eager: sets kernel attributes, warms caches
+    const int64_t l0 = launches;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "begin capture");
+    rec_target_ = &g.recs;
+    sgs_status s = decode_body(Bk);
+    rec_target_ = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(st_, &graph);
+    if (s != SGS_OK) return s;
+    CK(ce, "end capture");
+    CK(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    g.kernels = launches - l0;
+    launches = l0;
+  }
+  CK(cudaGraphLaunch(g.exec, st_), "graph launch");
+  launches += g.kernels;
   return SGS_OK;
 }
 
@@ -673,7 +751,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     KRec kr;
     ktic(&kr, 2);
     CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
-    ktoc(&kr, 0.0, 0.0);
+    ktoc(&kr, 0.0, 0.0, 0.0, T);
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
     CK(save(), "dump");
     CK(rmsnorm(h_, Ly.n2, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm2");
@@ -684,7 +762,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     launches += 5;
   }
   CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
-  float* lg = logits_ + (size_t)row_base * V;
+  float* lg = logits_ + (size_t)((e_.max_batch + 15) / 16 * 16 + row_base) * V;
   CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
   CK(argmax_rows(lg, np, V, nullptr, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, st_), "argmax");
   launches += 2;

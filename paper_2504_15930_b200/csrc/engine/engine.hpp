@@ -27,7 +27,7 @@ struct ArenaLayout {
   int64_t off_kv = 0, off_h = 0, off_x = 0, off_qkv = 0, off_q = 0, off_kc = 0, off_vc = 0, off_ao = 0,
           off_gu = 0, off_mm = 0, off_logits = 0, off_rope = 0, off_bt = 0, off_last = 0, off_hist = 0,
           off_meta = 0, off_attn = 0, off_cksum = 0;
-  int64_t meta_bytes = 0, attn_bytes = 0;
+  int64_t meta_bytes = 0, attn_bytes = 0, meta_dec_bytes = 0;
   int tmax = 0, max_pages = 0, max_items = 0;
 };
 
@@ -75,18 +75,33 @@ class Engine {
                            const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump = nullptr);
   cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
   void build_tensor_table();
+  // kernel-class timing record: bytes = bfix + brow * rows (bfix < 0: the
+  // iteration's decode-attention bytes/flops), flops = frow * rows
   struct KRec {
     int cls;
     cudaEvent_t a, b;
-    double bytes, flops;
+    double bfix, brow, frow;
+    int rows;  // -1: the decode rows of the flush (graph records)
   };
   std::vector<cudaEvent_t> ev_pool_;
   size_t ev_used_ = 0;
   std::vector<KRec> krec_;
   cudaEvent_t next_event();
   void ktic(KRec* r, int cls);
-  void ktoc(KRec* r, double bytes, double flops);
-  cudaError_t kflush();
+  void ktoc(KRec* r, double bfix, double brow, double frow, int rows);
+  cudaError_t kflush(const std::vector<KRec>& recs, int rows);
+  // decode iteration as a CUDA graph per 16-row bucket (fixed pointers, device-side work counts)
+  struct DecodeGraph {
+    cudaGraphExec_t exec = nullptr;
+    int uses = 0;
+    int64_t kernels = 0;
+    std::vector<KRec> recs;
+  };
+  std::vector<DecodeGraph> graphs_;
+  std::vector<KRec>* rec_target_ = nullptr;  // non-null while capturing
+  double cur_attn_bytes_ = 0, cur_attn_flops_ = 0;
+  sgs_status decode_body(int Bk);
+  sgs_status run_decode(int b);
 
   sgs_model_cfg m_{};
   sgs_engine_cfg e_{};

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(128, 2)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv,
                        const int32_t* __restrict__ bt, const int32_t* __restrict__ ctx,
                        const int32_t* __restrict__ row_slot, const AttnItem* __restrict__ items, int n_items,
+                       const int32_t* __restrict__ counts,
                        int nq, int nkv, int max_pages,
                        float scale_log2, void* __restrict__ out, int out_fp32, float* __restrict__ part_o,
                        float* __restrict__ part_ml) {
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(128, 2)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[ATTN_WARPS][ATTN_STAGES];
 
-  if ((int)blockIdx.x >= n_items) return;
+  if ((int)blockIdx.x >= (counts ? counts[0] : n_items)) return;
   const AttnItem it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = nq / nkv;
@@ -234,11 +235,12 @@ constexpr int ATTN_MAX_PARTS = 64;  // the planner never splits a (row, kv head)
 // weights 2^(m_j - M) and the denominator are computed once per row into
 // shared memory (one warp per query row), then every output element sums its
 // column over the parts with independent, coalesced loads.
-__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __restrict__ combs, int n_combs, int nq,
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __restrict__ combs, int n_combs,
+                                                           const int32_t* __restrict__ counts, int nq,
                                                            int nkv, int hd, const float* __restrict__ part_o,
                                                            const float* __restrict__ part_ml,
                                                            void* __restrict__ out, int out_fp32) {
-  if ((int)blockIdx.x >= n_combs) return;
+  if ((int)blockIdx.x >= (counts ? counts[1] : n_combs)) return;
   __shared__ float w[16][ATTN_MAX_PARTS];
   __shared__ float inv_l[16];
   const AttnComb c = combs[blockIdx.x];
@@ -332,7 +334,8 @@ int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd) {
 
 template <int HD>
 static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx,
-                                 const int32_t* row_slot, const AttnItem* items, int n_items, int nq, int nkv, int max_pages, void* out,
+                                 const int32_t* row_slot, const AttnItem* items, int n_items, const int32_t* counts, int nq,
+                                 int nkv, int max_pages, void* out,
                                  int out_fp32, float* part_o, float* part_ml, cudaStream_t stream) {
   constexpr int STAGE = 2 * PAGE_T * HD * 2;
   const size_t ring = (size_t)ATTN_WARPS * ATTN_STAGES * STAGE;
@@ -346,12 +349,12 @@ static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* b
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
   attn_decode_kernel<HD><<<n_items, 128, smem, stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx, row_slot, items,
-      n_items, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
+      n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
   return cudaGetLastError();
 }
 
 cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const int32_t* row_slot,
-                        const AttnItem* items,
+                        const int32_t* counts, const AttnItem* items,
                         int n_items, const AttnComb* combs, int n_combs, int nq, int nkv, int hd, int page,
                         int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
                         cudaStream_t stream) {
@@ -361,15 +364,15 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const 
   cudaError_t e;
   switch (hd) {
     case 32:
-      e = launch_decode<32>(q, kv, bt, ctx, row_slot, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
+      e = launch_decode<32>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
                             stream);
       break;
     case 64:
-      e = launch_decode<64>(q, kv, bt, ctx, row_slot, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
+      e = launch_decode<64>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
                             stream);
       break;
     case 128:
-      e = launch_decode<128>(q, kv, bt, ctx, row_slot, items, n_items, nq, nkv, max_pages, out, out_fp32, part_o,
+      e = launch_decode<128>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32, part_o,
                              part_ml, stream);
       break;
     default:
@@ -377,7 +380,8 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const 
   }
   if (e != cudaSuccess) return e;
   if (n_combs > 0) {
-    attn_combine_kernel<<<n_combs, 128, 0, stream>>>(combs, n_combs, nq, nkv, hd, part_o, part_ml, out, out_fp32);
+    attn_combine_kernel<<<n_combs, 128, 0, stream>>>(combs, n_combs, counts, nq, nkv, hd, part_o, part_ml, out,
+                                                     out_fp32);
     e = cudaGetLastError();
   }
   return e;

@@ -77,7 +77,8 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, const __nv_bfl
   const float* c = cs + (size_t)ps * half * 2;
   const int rc = hd / 8;
   int pg = -1, r = ps % page;
-  if (kv) pg = bt[(size_t)slot[t] * max_pages + ps / page];
+  const int sl = slot ? slot[t] : -1;
+  if (kv && sl >= 0) pg = bt[(size_t)sl * max_pages + ps / page];
   for (int j = threadIdx.x; j < nh * half; j += blockDim.x) {
     const int hh = j / half, i = j % half;
     float x1 = row[hh * hd + i], x2 = row[hh * hd + i + half];
@@ -98,7 +99,7 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, const __nv_bfl
     } else {
       const int isv = hh >= nq + nkv;
       const int kvh = isv ? hh - nq - nkv : hh - nq;
-      if (kv) {
+      if (pg >= 0) {
         __nv_bfloat16* base = kv + (((size_t)pg * nkv + kvh) * 2 + isv) * (size_t)page * hd + (size_t)r * hd;
         const int e1 = i, e2 = i + half;
         base[(((e1 >> 3) ^ kv_swz(r, rc)) << 3) + (e1 & 7)] = b1;
@@ -129,7 +130,8 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t*
                              const int32_t* __restrict__ slots, const int32_t* __restrict__ last_tok,
                              float* __restrict__ h, int d) {
   const int t = blockIdx.x;
-  const int tok = slots ? last_tok[slots[t]] : tokens[t];
+  const int sl = slots ? slots[t] : 0;
+  const int tok = slots ? (sl >= 0 ? last_tok[sl] : 0) : tokens[t];  // slot -1: padding row
   const __nv_bfloat16* e = E + (size_t)tok * d;
   float* o = h + (size_t)t * d;
   for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
     if (threadIdx.x == 0) {
       if (bi == 0x7fffffff) bi = 0;
       if (ids) ids[r] = bi;
-      if (slot) {
+      if (slot && slot[r] >= 0) {  // slot -1: padding row of a CUDA-graph bucket
         const int s = slot[r];
         last_tok[s] = bi;
         out_hist[(size_t)s * max_gen + tok_idx[r]] = bi;

@@ -31,8 +31,10 @@ void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, At
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
 // items/combs are device arrays (already copied); part buffers in workspace.
 // block_table rows are indexed by row_slot[row] (NULL: by row); ctx is per row.
+// counts (device, optional): {n_items, n_combs} read by the kernels, in which
+// case n_items / n_combs are only the launch capacities (CUDA-graph replay).
 cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
-                        const int32_t* row_slot, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
+                        const int32_t* row_slot, const int32_t* counts, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
                         int hd, int page, int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
                         cudaStream_t stream);
 
