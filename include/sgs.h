@@ -231,8 +231,9 @@ sgs_status sgs_op_rmsnorm(const float* x, const void* w, void* y, int32_t T, int
 
 /* a7/K7: RoPE + KV append.  qkv fp32 [T, (nq+2nkv)*hd] (+ bias bf16),
  * pos int32 [T], slot int32 [T] -> q bf16 [T, nq, hd]; k, v written into the
- * page pool via block_table[slot][pos/page], pos % page.  cos_sin fp32
- * [max_pos, hd/2, 2] from sgs_rope_table. */
+ * page pool via block_table[slot][pos/page], pos % page (slot -1: row skipped).
+ * cos_sin fp32 [max_pos, hd/2, 2] from sgs_rope_table.  qkv is zeroed after it
+ * is read (it is the split-K accumulator of the next QKV GEMM). */
 sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
                               const int32_t* block_table, int32_t max_pages_per_seq, const float* cos_sin,
                               void* q_out, void* kv, int32_t T, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
@@ -245,7 +246,8 @@ sgs_status sgs_rope_table(float* host_out, int32_t max_pos, int32_t hd, double t
 sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
                                     int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out, void* stream);
 
-/* a10 epilogue: m[t, i] = bf16(SiLU(gu[t, i]) * gu[t, f + i]); gu fp32 [T, 2f], m bf16 [T, f]. */
+/* a10 epilogue: m[t, i] = bf16(SiLU(gu[t, i]) * gu[t, f + i]); gu fp32 [T, 2f], m bf16 [T, f].
+ * gu is zeroed after it is read. */
 sgs_status sgs_op_silu_mul(const float* gu, void* m, int32_t T, int32_t f, void* stream);
 
 /* K9 greedy: ids[r] = argmax_v logits[r, v] (lowest index on ties). */

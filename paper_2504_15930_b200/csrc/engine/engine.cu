@@ -230,6 +230,8 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   CK(cudaMemsetAsync(arena_ + L_.off_kv, 0, L_.kv_bytes, st_), "memset kv");
   CK(cudaMemsetAsync(bt_, 0, (size_t)e.max_batch * L_.max_pages * 4, st_), "memset bt");
   CK(cudaMemsetAsync(last_tok_, 0, (size_t)e.max_batch * 4, st_), "memset last");
+  // split-K accumulators (kept zeroed by their consumers) and the residual scratch
+  CK(cudaMemsetAsync(arena_ + L_.off_h, 0, L_.off_mm - L_.off_h, st_), "memset scratch");
   // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
   {
     const int half = m.head_dim / 2;
@@ -404,7 +406,7 @@ cudaEvent_t Engine::next_event() {
 
 void Engine::ktic(KRec* r, int cls) {
   r->cls = -1;
-  if (!(e_.flags & SGS_F_KERNEL_TIMING)) return;
+  if (!timing_now_) return;
   r->cls = cls;
   if (rec_target_) {  // capturing: events owned by the graph
     cudaEventCreate(&r->a);
@@ -448,7 +450,8 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
   KRec kr;
   ktic(&kr, 1);
   if (splits > 1) {
-    if (!accumulate) {
+    // qkv_ and gu_ are kept zeroed by their consumers (rope_append, silu_mul)
+    if (!accumulate && C != qkv_ && C != gu_) {
       e = cudaMemsetAsync(C, 0, (size_t)T * N * 4, st_);
       if (e != cudaSuccess) return e;
     }
@@ -477,6 +480,10 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   const int d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn,
             V = m_.vocab;
   const int qkvN = (nq + 2 * nkv) * hd;
+  (void)qkvN, (void)f, (void)d, (void)n_adm;
+  // per-kernel CUDA events on 1 in kTimingStride iterations: events between
+  // kernels serialise them (no PDL overlap), so the others run untouched
+  timing_now_ = (e_.flags & SGS_F_KERNEL_TIMING) && (timing_iter_++ % kTimingStride == 0);
   // ---------------- stage metadata (host, pinned) -> one H2D copy
   std::vector<int32_t> meta;
   meta.reserve(4096);
@@ -635,9 +642,13 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   CK(kflush(krec_, n_run), "kernel timing");
   krec_.clear();
   ev_used_ = 0;
-  if (n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS)) {
-    const DecodeGraph& g = graphs_[(n_run + 15) / 16];
+  if (n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && timing_now_) {
+    const DecodeGraph& g = graphs_[1][(n_run + 15) / 16];
     if (g.exec) CK(kflush(g.recs, n_run), "kernel timing");
+  }
+  if (timing_now_) {  // slot 3: device time of the sampled iterations (for the kernel shares)
+    kstat_ms[3] += last_ms;
+    kstat_n[3] += 1;
   }
   for (size_t k = 0; k < plan.completed.size(); ++k) {
     const Sample& s = S[plan.completed[k]];
@@ -702,8 +713,9 @@ sgs_status Engine::decode_body(int Bk) {
 sgs_status Engine::run_decode(int b) {
   const int Bk = (b + 15) / 16 * 16;
   if (e_.flags & SGS_F_NO_GRAPHS) return decode_body(Bk);
-  if (graphs_.empty()) graphs_.resize((e_.max_batch + 15) / 16 + 1);
-  DecodeGraph& g = graphs_[Bk / 16];
+  auto& gs = graphs_[timing_now_ ? 1 : 0];
+  if (gs.empty()) gs.resize((e_.max_batch + 15) / 16 + 1);
+  DecodeGraph& g = gs[Bk / 16];
   if (!g.exec) {
     if (g.uses++ == 0) return decode_body(Bk);  // first use eager: sets kernel attributes, warms caches
     const int64_t l0 = launches;

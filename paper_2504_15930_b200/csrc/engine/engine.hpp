@@ -97,7 +97,10 @@ class Engine {
     int64_t kernels = 0;
     std::vector<KRec> recs;
   };
-  std::vector<DecodeGraph> graphs_;
+  std::vector<DecodeGraph> graphs_[2];  // [timed]: variant with event-record nodes
+  bool timing_now_ = false;             // this iteration is a timing sample
+  int64_t timing_iter_ = 0;
+  static constexpr int kTimingStride = 32;  // 1 in 32 iterations carries the per-kernel events
   std::vector<KRec>* rec_target_ = nullptr;  // non-null while capturing
   double cur_attn_bytes_ = 0, cur_attn_flops_ = 0;
   sgs_status decode_body(int Bk);

@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(128, 2)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[ATTN_WARPS][ATTN_STAGES];
 
+  pdl_trigger();
+  pdl_wait();
   if ((int)blockIdx.x >= (counts ? counts[0] : n_items)) return;
   const AttnItem it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,6 +242,8 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __res
                                                            int nkv, int hd, const float* __restrict__ part_o,
                                                            const float* __restrict__ part_ml,
                                                            void* __restrict__ out, int out_fp32) {
+  pdl_trigger();
+  pdl_wait();
   if ((int)blockIdx.x >= (counts ? counts[1] : n_combs)) return;
   __shared__ float w[16][ATTN_MAX_PARTS];
   __shared__ float inv_l[16];
@@ -347,10 +351,9 @@ static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* b
     set = true;
   }
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
-  attn_decode_kernel<HD><<<n_items, 128, smem, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx, row_slot, items,
-      n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
-  return cudaGetLastError();
+  return launch_pdl(attn_decode_kernel<HD>, dim3(n_items), dim3(128), smem, stream,
+                    reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx,
+                    row_slot, items, n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
 }
 
 cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const int32_t* row_slot,
@@ -380,9 +383,8 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const 
   }
   if (e != cudaSuccess) return e;
   if (n_combs > 0) {
-    attn_combine_kernel<<<n_combs, 128, 0, stream>>>(combs, n_combs, counts, nq, nkv, hd, part_o, part_ml, out,
-                                                     out_fp32);
-    e = cudaGetLastError();
+    e = launch_pdl(attn_combine_kernel, dim3(n_combs), dim3(128), 0, stream, combs, n_combs, counts, nq, nkv, hd,
+                   part_o, part_ml, out, out_fp32);
   }
   return e;
 }

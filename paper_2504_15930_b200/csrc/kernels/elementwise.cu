@@ -18,6 +18,8 @@ namespace sgs {
 // ------------------------------------------------------------------ RMSNorm
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                                __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ rows, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int src = rows ? rows[t] : t;
   const float* xr = x + (size_t)src * d;
@@ -55,25 +57,28 @@ cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows,
   if (T <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
   int threads = d >= 1024 ? 256 : 128;
-  rmsnorm_kernel<<<T, threads, 0, stream>>>(x, reinterpret_cast<const __nv_bfloat16*>(w),
-                                             reinterpret_cast<__nv_bfloat16*>(y), rows, d, eps);
-  return cudaGetLastError();
+  return launch_pdl(rmsnorm_kernel, dim3(T), dim3(threads), 0, stream, x, reinterpret_cast<const __nv_bfloat16*>(w),
+                    reinterpret_cast<__nv_bfloat16*>(y), rows, d, eps);
 }
 
 // ------------------------------------------------------------------ RoPE + KV append
 // One block per row.  Pair index j in [0, (nq+2nkv) * hd/2): head = j / half,
-// i = j % half.  q/k heads rotate (x_i, x_{i+half}); v heads copy.
-__global__ void rope_append_kernel(const float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
+// i = j % half.  q/k heads rotate (x_i, x_{i+half}); v heads copy.  The fp32
+// qkv row is zeroed after it is read, so the next split-K QKV GEMM (fp32 red.add)
+// finds a zeroed accumulator without a memset.
+__global__ void rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                    const int32_t* __restrict__ bt, int max_pages, const float* __restrict__ cs,
                                    __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv,
                                    __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out, int nq,
                                    int nkv, int hd, int page) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int half = hd >> 1;
   const int nh = nq + 2 * nkv;
   const int ps = pos[t];
-  const float* row = qkv + (size_t)t * nh * hd;
+  float* row = qkv + (size_t)t * nh * hd;
   const float* c = cs + (size_t)ps * half * 2;
   const int rc = hd / 8;
   int pg = -1, r = ps % page;
@@ -82,6 +87,8 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, const __nv_bfl
   for (int j = threadIdx.x; j < nh * half; j += blockDim.x) {
     const int hh = j / half, i = j % half;
     float x1 = row[hh * hd + i], x2 = row[hh * hd + i + half];
+    row[hh * hd + i] = 0.f;
+    row[hh * hd + i + half] = 0.f;
     if (bias) {
       x1 += __bfloat162float(bias[hh * hd + i]);
       x2 += __bfloat162float(bias[hh * hd + i + half]);
@@ -118,17 +125,19 @@ cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, 
                         const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
                         void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  rope_append_kernel<<<T, 256, 0, stream>>>(
-      qkv, reinterpret_cast<const __nv_bfloat16*>(bias), pos, slot, block_table, max_pages, cos_sin,
-      reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(kv),
-      reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), nq, nkv, hd, page);
-  return cudaGetLastError();
+  return launch_pdl(rope_append_kernel, dim3(T), dim3(256), 0, stream, const_cast<float*>(qkv),
+                    reinterpret_cast<const __nv_bfloat16*>(bias), pos, slot, block_table, max_pages, cos_sin,
+                    reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(kv),
+                    reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), nq, nkv, hd,
+                    page);
 }
 
 // ------------------------------------------------------------------ embedding gather
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tokens,
                              const int32_t* __restrict__ slots, const int32_t* __restrict__ last_tok,
                              float* __restrict__ h, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int sl = slots ? slots[t] : 0;
   const int tok = slots ? (sl >= 0 ? last_tok[sl] : 0) : tokens[t];  // slot -1: padding row
@@ -143,18 +152,22 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t*
 cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, const int32_t* last_tok, float* h,
                   int T, int d, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  embed_kernel<<<T, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(E), tokens, slots, last_tok, h, d);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(T), dim3(128), 0, stream, reinterpret_cast<const __nv_bfloat16*>(E), tokens,
+                    slots, last_tok, h, d);
 }
 
 // ------------------------------------------------------------------ SwiGLU
-__global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ m, int f) {
+__global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restrict__ m, int f) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.y;
-  const float* g = gu + (size_t)t * 2 * f;
-  const float* u = g + f;
+  float* g = gu + (size_t)t * 2 * f;
+  float* u = g + f;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i < f; i += gridDim.x * blockDim.x * 2) {
     const float2 gv = *reinterpret_cast<const float2*>(g + i);
     const float2 uv = *reinterpret_cast<const float2*>(u + i);
+    *reinterpret_cast<float2*>(g + i) = make_float2(0.f, 0.f);  // zeroed for a split-K successor
+    *reinterpret_cast<float2*>(u + i) = make_float2(0.f, 0.f);
     const float s0 = gv.x / (1.f + __expf(-gv.x)), s1 = gv.y / (1.f + __expf(-gv.y));
     *reinterpret_cast<uint32_t*>(m + (size_t)t * f + i) = pack_bf16x2(s0 * uv.x, s1 * uv.y);
   }
@@ -164,8 +177,8 @@ cudaError_t silu_mul(const float* gu, void* m, int T, int f, cudaStream_t stream
   if (T <= 0) return cudaSuccess;
   int bx = (f / 2 + 255) / 256;
   if (bx > 16) bx = 16;
-  silu_mul_kernel<<<dim3(bx, T), 256, 0, stream>>>(gu, reinterpret_cast<__nv_bfloat16*>(m), f);
-  return cudaGetLastError();
+  return launch_pdl(silu_mul_kernel, dim3(bx, T), dim3(256), 0, stream, const_cast<float*>(gu),
+                    reinterpret_cast<__nv_bfloat16*>(m), f);
 }
 
 // ------------------------------------------------------------------ greedy sampler
@@ -173,6 +186,8 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
                                                       const int32_t* __restrict__ slot,
                                                       const int32_t* __restrict__ tok_idx, int32_t* last_tok,
                                                       int32_t* out_hist, int max_gen) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float* x = logits + (size_t)r * V;
   float bv = -INFINITY;
@@ -227,8 +242,8 @@ cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, cons
                         cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (V % 4) return cudaErrorInvalidValue;
-  argmax_kernel<<<rows, 1024, 0, stream>>>(logits, V, ids, slot, tok_idx, last_tok, out_hist, max_gen);
-  return cudaGetLastError();
+  return launch_pdl(argmax_kernel, dim3(rows), dim3(1024), 0, stream, logits, V, ids, slot, tok_idx, last_tok,
+                    out_hist, max_gen);
 }
 
 // ------------------------------------------------------------------ weights

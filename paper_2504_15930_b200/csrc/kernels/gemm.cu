@@ -61,13 +61,24 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  pdl_trigger();
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
-    for (int i = 0; i < nk; ++i) {
+    // The weight tiles do not depend on the previous kernel: fill the ring
+    // with them before waiting for it (overlaps the weight stream with the
+    // predecessor's tail), then load the activation tiles.
+    const int pre = nk < stages ? nk : stages;
+    for (int i = 0; i < pre; ++i) {
+      mbar_expect_tx(&full[i], GEMM_A_BYTES + b_bytes);
+      tma_load_2d(sA + (size_t)i * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[i]);
+    }
+    pdl_wait();
+    for (int i = 0; i < pre; ++i) tma_load_2d(sB + (size_t)i * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[i]);
+    for (int i = pre; i < nk; ++i) {
       const int s = i % stages;
-      if (i >= stages) mbar_wait(&empty[s], ((i / stages) - 1) & 1);
+      mbar_wait(&empty[s], ((i / stages) - 1) & 1);
       mbar_expect_tx(&full[s], GEMM_A_BYTES + b_bytes);
       tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
       tma_load_2d(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[s]);
@@ -95,6 +106,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global (lane = output feature)
     const int e = warp - 4;
+    pdl_wait();  // C may still be read by the predecessor (write-after-read)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const int n = m0 + 32 * e + lane;
@@ -225,13 +237,17 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (!cached_tmap(&tw, W, N, K, GEMM_BM)) return cudaErrorInvalidValue;
   if (!cached_tmap(&tx, X, T, K, BN)) return cudaErrorInvalidValue;
   const int stage_bytes = GEMM_A_BYTES + BN * GEMM_BK * 2;
-  int stages = GEMM_SMEM_BUDGET / stage_bytes;
+  // decode-sized tiles (BN <= 64) use half the shared memory and TMEM so two
+  // CTAs fit on an SM: the next GEMM (PDL) streams its weights while the
+  // current one drains
+  const bool small = BN <= 64;
+  int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
   if (stages > 12) stages = 12;
   if (stages > kc) stages = kc < 2 ? 2 : kc;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
   // accumulator interleave: as many TMEM accumulators as fit (<= 8), each 32-column aligned
   const int acc_stride = (BN + 31) / 32 * 32;
-  int n_acc = 512 / acc_stride;
+  int n_acc = (small ? 256 : 512) / acc_stride;
   if (n_acc > 8) n_acc = 8;
   if (n_acc > per) n_acc = per;
   if (n_acc < 1) n_acc = 1;
@@ -243,9 +259,8 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
     attr_set = true;
   }
   dim3 grid(N / GEMM_BM, (T + BN - 1) / BN, splits);
-  gemm_bf16_tc_kernel<<<grid, 256, smem, stream>>>(tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols, n_acc,
-                                                             acc_stride);
-  return cudaGetLastError();
+  return launch_pdl(gemm_bf16_tc_kernel, grid, dim3(256), smem, stream, tw, tx, C, T, ldc, BN, stages, kc, per, mode,
+                    tmem_cols, n_acc, acc_stride);
 }
 
 }  // namespace sgs
