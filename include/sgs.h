@@ -184,6 +184,14 @@ sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms);
  * launching stream), algorithmic bytes and flops, launches.  reset != 0 clears. */
 sgs_status sgs_kernel_stats(sgs_handle* h, int32_t cls, double* ms, double* bytes, double* flops, int64_t* launches,
                             int32_t reset);
+/* Roofline denominators for sgs_kernel_stats' roofline time: every timed
+ * launch contributes max(bytes / (bw_gbs GB/s), flops / (tflops TFLOP/s)). */
+sgs_status sgs_set_roofline(sgs_handle* h, double bw_gbs, double tflops);
+sgs_status sgs_kernel_roofline_ms(const sgs_handle* h, int32_t cls, double* ms);
+/* Per-iteration log (T(b) profiling): 6 int64 per executed iteration
+ * {t, b, admitted, prefill tokens, sum of contexts, device time in us}. */
+sgs_status sgs_iter_log(const sgs_handle* h, int64_t* buf, int64_t cap, int64_t* n);
+
 /* Host<->device bytes moved by the service calls so far (metadata, prompts, tokens). */
 sgs_status sgs_io_bytes(const sgs_handle* h, int64_t* h2d, int64_t* d2h);
 

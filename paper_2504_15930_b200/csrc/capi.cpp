@@ -138,7 +138,28 @@ sgs_status sgs_kernel_stats(sgs_handle* h, int32_t cls, double* ms, double* byte
   if (bytes) *bytes = E.kstat_bytes[cls];
   if (flops) *flops = E.kstat_flops[cls];
   if (launches) *launches = E.kstat_n[cls];
-  if (reset) E.kstat_ms[cls] = E.kstat_bytes[cls] = E.kstat_flops[cls] = 0, E.kstat_n[cls] = 0;
+  if (reset) E.kstat_ms[cls] = E.kstat_bytes[cls] = E.kstat_flops[cls] = E.kstat_roof_ms[cls] = 0, E.kstat_n[cls] = 0;
+  return SGS_OK;
+}
+
+sgs_status sgs_set_roofline(sgs_handle* h, double bw_gbs, double tflops) {
+  if (!h || bw_gbs <= 0 || tflops <= 0) return SGS_E_INVAL;
+  h->eng.roof_bw_gbs = bw_gbs;
+  h->eng.roof_tflops = tflops;
+  return SGS_OK;
+}
+
+sgs_status sgs_kernel_roofline_ms(const sgs_handle* h, int32_t cls, double* ms) {
+  if (!h || !ms || cls < 0 || cls > 3) return SGS_E_INVAL;
+  *ms = h->eng.kstat_roof_ms[cls];
+  return SGS_OK;
+}
+
+sgs_status sgs_iter_log(const sgs_handle* h, int64_t* buf, int64_t cap, int64_t* n) {
+  if (!h || !n) return SGS_E_INVAL;
+  const auto& v = h->eng.iter_log;
+  *n = (int64_t)v.size();
+  if (buf) std::memcpy(buf, v.data(), sizeof(int64_t) * (size_t)std::min<int64_t>(cap, *n));
   return SGS_OK;
 }
 
@@ -216,16 +237,20 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
       cudaMemcpyAsync(d_combs, plan.combs.data(), plan.combs.size() * sizeof(sgs::AttnComb), cudaMemcpyHostToDevice,
                       st) != cudaSuccess)
     return SGS_E_CUDA;
+  int* arrive = reinterpret_cast<int*>(part_ml + (size_t)std::max(plan.n_parts, 1) * g * 2);
+  if (!plan.combs.empty() && cudaMemsetAsync(arrive, 0, plan.combs.size() * sizeof(int), st) != cudaSuccess)
+    return SGS_E_CUDA;
   cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, nullptr, nullptr, d_items, (int)plan.items.size(), d_combs,
                                    (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, out_fp32,
-                                   part_o, part_ml, st);
+                                   part_o, part_ml, arrive, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host plan vectors die here
   return cuda_status(e);
 }
 
 sgs_status sgs_op_gemm(const void* W, const void* X, void* C, int32_t N, int32_t K, int32_t T, int32_t ldc,
                        int32_t mode, int32_t splits, void* stream) {
-  if (!W || !X || !C || N <= 0 || K <= 0 || T < 0 || mode < 0 || mode > 2) return SGS_E_INVAL;
+  if (!W || !X || !C || N <= 0 || K <= 0 || T < 0 || mode < 0 || mode > 3) return SGS_E_INVAL;
+  if (mode == 3 && (splits > 1 || ldc * 2 != N)) return SGS_E_INVAL;
   if (N % 128 || K % 64) return SGS_E_UNSUPPORTED;
   return cuda_status(sgs::gemm_bf16(W, X, reinterpret_cast<float*>(C), N, K, T, ldc, mode, splits,
                                     reinterpret_cast<cudaStream_t>(stream)));

@@ -76,7 +76,7 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
                                4096,
                            256);
   L->off_meta = take(L->meta_bytes);
-  L->attn_bytes = max_items * (nq / nkv) * (hd + 2) * 4;
+  L->attn_bytes = max_items * (nq / nkv) * (hd + 2) * 4 + max_items * 4;  // partials + arrival counters
   L->off_attn = take(L->attn_bytes);
   L->off_cksum = take(64);
   L->scratch_bytes = o - s0;
@@ -126,8 +126,9 @@ void Engine::build_tensor_table() {
     tensors_.push_back({b + 4, at(L->bqkv, nq * hd), nkv * hd, 0});
     tensors_.push_back({b + 5, at(L->bqkv, (nq + nkv) * hd), nkv * hd, 0});
     tensors_.push_back({b + 6, L->wo, d * nq * hd, 0});
-    tensors_.push_back({b + 7, L->wgu, f * d, 0});
-    tensors_.push_back({b + 8, at(L->wgu, f * d), f * d, 0});
+    // gate and up interleave in 64-row blocks: tile i of the fused matrix = 64 gate rows + 64 up rows
+    tensors_.push_back({b + 7, L->wgu, f * d, 0, d, 64, 128, 0});
+    tensors_.push_back({b + 8, L->wgu, f * d, 0, d, 64, 128, 64});
     tensors_.push_back({b + 9, L->wd, d * f, 0});
     tensors_.push_back({b + 10, L->n1, d, 1});
     tensors_.push_back({b + 11, L->n2, d, 1});
@@ -232,6 +233,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   CK(cudaMemsetAsync(last_tok_, 0, (size_t)e.max_batch * 4, st_), "memset last");
   // split-K accumulators (kept zeroed by their consumers) and the residual scratch
   CK(cudaMemsetAsync(arena_ + L_.off_h, 0, L_.off_mm - L_.off_h, st_), "memset scratch");
+  CK(cudaMemsetAsync(attn_ws_, 0, L_.attn_bytes, st_), "memset attention workspace");
   // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
   {
     const int half = m.head_dim / 2;
@@ -250,7 +252,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
 sgs_status Engine::load_weights_seed(uint64_t seed) {
   if (null_) return SGS_OK;
   for (const auto& t : tensors_) {
-    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_), "hash_init");
+    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_, t.cols, t.blk, t.stride, t.off), "hash_init");
     ++launches;
   }
   CK(cudaStreamSynchronize(st_), "hash_init sync");
@@ -265,7 +267,7 @@ sgs_status Engine::checksum(int64_t tensor_id, uint64_t* out) {
   for (const auto& t : tensors_)
     if (t.id == tensor_id) {
       CK(cudaMemsetAsync(cksum_dev_, 0, 8, st_), "memset");
-      CK(checksum_bf16(t.ptr, t.n, cksum_dev_, st_), "checksum");
+      CK(checksum_bf16(t.ptr, t.n, cksum_dev_, st_, t.cols, t.blk, t.stride, t.off), "checksum");
       unsigned long long v = 0;
       CK(cudaMemcpyAsync(&v, cksum_dev_, 8, cudaMemcpyDeviceToHost, st_), "checksum d2h");
       CK(cudaStreamSynchronize(st_), "checksum sync");
@@ -438,7 +440,11 @@ cudaError_t Engine::kflush(const std::vector<KRec>& recs, int rows) {
     const int n = r.rows < 0 ? rows : r.rows;
     kstat_ms[r.cls] += ms;
     kstat_bytes[r.cls] += r.bfix < 0 ? cur_attn_bytes_ : r.bfix + r.brow * n;
-    kstat_flops[r.cls] += r.bfix < 0 ? cur_attn_flops_ : r.frow * n;
+    const double by = r.bfix < 0 ? cur_attn_bytes_ : r.bfix + r.brow * n;
+    const double fl = r.bfix < 0 ? cur_attn_flops_ : r.frow * n;
+    kstat_flops[r.cls] += fl;
+    if (roof_bw_gbs > 0 && roof_tflops > 0)
+      kstat_roof_ms[r.cls] += std::max(by / (roof_bw_gbs * 1e6), fl / (roof_tflops * 1e9));
     kstat_n[r.cls] += 1;
   }
   return cudaSuccess;
@@ -461,6 +467,25 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
   }
   // algorithmic bytes: weights + per row activations in + fp32 out (read-modify-write when accumulating)
   ktoc(&kr, 2.0 * N * K, 2.0 * K + (accumulate ? 8.0 : 4.0) * N, 2.0 * N * K, T);
+  ++launches;
+  return e;
+}
+
+// m = bf16(SiLU(x Wg^T) * (x Wu^T)): one GEMM with the SwiGLU epilogue when
+// the gate/up GEMM needs no split-K (always at the model shapes: 2 f / 128 >=
+// 148 tiles), else the fp32 GEMM + the silu_mul kernel.
+cudaError_t Engine::gate_up(const void* W, int T) {
+  const int d = m_.d_model, f = m_.d_ffn;
+  if (gemm_auto_splits(2 * f, d, T) > 1) {
+    cudaError_t e = gemm(W, x_, gu_, 2 * f, d, T, false);
+    if (e != cudaSuccess) return e;
+    ++launches;
+    return silu_mul(gu_, mm_, T, f, st_);
+  }
+  KRec kr;
+  ktic(&kr, 1);
+  cudaError_t e = gemm_bf16(W, x_, reinterpret_cast<float*>(mm_), 2 * f, d, T, f, 3, 1, st_);
+  ktoc(&kr, 2.0 * 2 * f * d, 2.0 * d + 2.0 * f, 2.0 * 2 * f * d, T);
   ++launches;
   return e;
 }
@@ -650,6 +675,12 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     kstat_ms[3] += last_ms;
     kstat_n[3] += 1;
   }
+  {
+    int64_t pf_tok = 0;
+    for (auto& c : chunks) pf_tok += c.T;
+    iter_log.insert(iter_log.end(), {plan.t, (int64_t)plan.b, (int64_t)n_adm, pf_tok, plan.sumctx,
+                                     (int64_t)std::llround(last_ms * 1000.0)});
+  }
   for (size_t k = 0; k < plan.completed.size(); ++k) {
     const Sample& s = S[plan.completed[k]];
     Completion c{s.id, s.slot, s.admit_iter, s.finish_iter, version,
@@ -679,6 +710,7 @@ sgs_status Engine::decode_body(int Bk) {
   const AttnItem* d_items = reinterpret_cast<const AttnItem*>(d_combs + L_.max_items);
   float* part_o = reinterpret_cast<float*>(attn_ws_);
   float* part_ml = part_o + (size_t)L_.max_items * (nq / nkv) * hd;
+  int* arrive = reinterpret_cast<int*>(part_ml + (size_t)L_.max_items * (nq / nkv) * 2);  // zeroed at init
   const int cap_items = std::min(L_.max_items, 2 * 148 + Bk * nkv + 64);
   const int cap_combs = Bk * nkv;
   CK(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), "embed");
@@ -693,13 +725,12 @@ sgs_status Engine::decode_body(int Bk) {
     KRec kr;
     ktic(&kr, 0);
     CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_slot, counts, d_items, cap_items, d_combs, cap_combs, nq, nkv, hd,
-                   e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, st_),
+                   e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, arrive, st_),
        "attn_decode");
     ktoc(&kr, -1.0, 0.0, 0.0, 0);
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
     CK(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm2");
-    CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, Bk, false), "gemm gate_up");
-    CK(silu_mul(gu_, mm_, Bk, f, st_), "silu");
+    CK(gate_up(Ly.wgu, Bk), "gemm gate_up + SwiGLU");
     CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
     launches += 6;
   }
@@ -767,8 +798,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
     CK(save(), "dump");
     CK(rmsnorm(h_, Ly.n2, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm2");
-    CK(gemm(Ly.wgu, x_, gu_, 2 * f, d, T, false), "gemm gate_up");
-    CK(silu_mul(gu_, mm_, T, f, st_), "silu");
+    CK(gate_up(Ly.wgu, T), "gemm gate_up + SwiGLU");
     CK(gemm(Ly.wd, mm_, h_, d, f, T, true), "gemm down");
     CK(save(), "dump");
     launches += 5;

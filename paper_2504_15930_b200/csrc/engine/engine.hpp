@@ -19,6 +19,8 @@ struct TensorRef {
   void* ptr;
   int64_t n;
   int is_norm;
+  int64_t cols = 1;  // row-block placement (interleaved gate/up): blk rows every stride rows at off
+  int blk = 0, stride = 0, off = 0;
 };
 
 struct ArenaLayout {
@@ -63,6 +65,10 @@ class Engine {
   double kstat_ms[4] = {0}, kstat_bytes[4] = {0}, kstat_flops[4] = {0};
   int64_t kstat_n[4] = {0};
   int64_t h2d_bytes = 0, d2h_bytes = 0;
+  // per-iteration log (T(b) profiling, a16): t, b, admitted, prefill tokens, sum ctx, device us
+  std::vector<int64_t> iter_log;
+  // roofline time of the timed launches: sum_k max(bytes_k / BW, flops_k / F) (sgs_set_roofline)
+  double roof_bw_gbs = 0, roof_tflops = 0, kstat_roof_ms[4] = {0};
   int64_t launches = 0;
   int32_t version = 0;
 
@@ -74,6 +80,7 @@ class Engine {
                            const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
                            const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump = nullptr);
   cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
+  cudaError_t gate_up(const void* W, int T);
   void build_tensor_table();
   // kernel-class timing record: bytes = bfix + brow * rows (bfix < 0: the
   // iteration's decode-attention bytes/flops), flops = frow * rows

@@ -28,6 +28,11 @@ namespace sgs {
 constexpr int ATTN_WARPS = 4;
 constexpr int ATTN_STAGES = 3;
 constexpr int PAGE_T = 16;
+constexpr int ATTN_MAX_PARTS = 64;  // the planner never splits a (row, kv head) into more parts
+
+__device__ __forceinline__ void combine_merge(const AttnComb& c, int nq, int nkv, int hd,
+                                              const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                              void* __restrict__ out, int out_fp32);
 
 template <int HD>
 __global__ void __launch_bounds__(128, 2)
@@ -37,7 +42,7 @@ __global__ void __launch_bounds__(128, 2)
                        const int32_t* __restrict__ counts,
                        int nq, int nkv, int max_pages,
                        float scale_log2, void* __restrict__ out, int out_fp32, float* __restrict__ part_o,
-                       float* __restrict__ part_ml) {
+                       float* __restrict__ part_ml, const AttnComb* __restrict__ combs, int* __restrict__ arrive) {
   constexpr int RC = HD / 8;                 // 16-byte chunks per row
   constexpr int HALF = PAGE_T * HD * 2;      // K (or V) bytes of one page-head
   constexpr int STAGE = 2 * HALF;
@@ -229,25 +234,31 @@ __global__ void __launch_bounds__(128, 2)
       }
     }
   }
+  if (it.part >= 0) {
+    // split item: the last of the (row, kv head)'s parts to arrive merges them
+    // (threadfence reduction; the counter re-arms itself for the next launch)
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&arrive[it.comb], 1) == combs[it.comb].nparts - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      combine_merge(combs[it.comb], nq, nkv, HD, part_o, part_ml, out, out_fp32);
+      if (threadIdx.x == 0) arrive[it.comb] = 0;
+    }
+  }
 }
-
-constexpr int ATTN_MAX_PARTS = 64;  // the planner never splits a (row, kv head) into more parts
 
 // LSE merge of the split-K partials of one (row, kv head): the per-part
 // weights 2^(m_j - M) and the denominator are computed once per row into
 // shared memory (one warp per query row), then every output element sums its
-// column over the parts with independent, coalesced loads.
-__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __restrict__ combs, int n_combs,
-                                                           const int32_t* __restrict__ counts, int nq,
-                                                           int nkv, int hd, const float* __restrict__ part_o,
-                                                           const float* __restrict__ part_ml,
-                                                           void* __restrict__ out, int out_fp32) {
-  pdl_trigger();
-  pdl_wait();
-  if ((int)blockIdx.x >= (counts ? counts[1] : n_combs)) return;
+// column over the parts with independent, coalesced (L2) loads.
+__device__ __forceinline__ void combine_merge(const AttnComb& c, int nq, int nkv, int hd,
+                                              const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                              void* __restrict__ out, int out_fp32) {
   __shared__ float w[16][ATTN_MAX_PARTS];
   __shared__ float inv_l[16];
-  const AttnComb c = combs[blockIdx.x];
   const int g = nq / nkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = warp; r < g; r += blockDim.x >> 5) {
@@ -257,8 +268,8 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __res
       const int j = lane + 32 * k;
       const bool ok = j < c.nparts;
       const size_t pj = ((size_t)(c.part0 + (ok ? j : 0)) * g + r) * 2;
-      m[k] = ok ? part_ml[pj] : -INFINITY;
-      l[k] = ok ? part_ml[pj + 1] : 0.f;
+      m[k] = ok ? __ldcg(part_ml + pj) : -INFINITY;
+      l[k] = ok ? __ldcg(part_ml + pj + 1) : 0.f;
     }
     const float M = warp_max(fmaxf(m[0], m[1]));
     float L = 0.f;
@@ -280,12 +291,12 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnComb* __res
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     int j = 0;
     for (; j + 4 <= c.nparts; j += 4) {
-      s0 += w[r][j] * po[j * stride];
-      s1 += w[r][j + 1] * po[(j + 1) * stride];
-      s2 += w[r][j + 2] * po[(j + 2) * stride];
-      s3 += w[r][j + 3] * po[(j + 3) * stride];
+      s0 += w[r][j] * __ldcg(po + j * stride);
+      s1 += w[r][j + 1] * __ldcg(po + (j + 1) * stride);
+      s2 += w[r][j + 2] * __ldcg(po + (j + 2) * stride);
+      s3 += w[r][j + 3] * __ldcg(po + (j + 3) * stride);
     }
-    for (; j < c.nparts; ++j) s0 += w[r][j] * po[j * stride];
+    for (; j < c.nparts; ++j) s0 += w[r][j] * __ldcg(po + j * stride);
     const float v = ((s0 + s1) + (s2 + s3)) * inv_l[r];
     const size_t oi = ((size_t)c.row * nq + (size_t)c.kvh * g + r) * hd + e;
     if (out_fp32)
@@ -315,13 +326,13 @@ void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, At
     if (nch > ATTN_MAX_PARTS) nch = ATTN_MAX_PARTS;
     for (int h = 0; h < nkv; ++h) {
       if (nch == 1) {
-        plan->items.push_back(AttnItem{i, h, 0, np, -1});
+        plan->items.push_back(AttnItem{i, h, 0, np, -1, -1});
         continue;
       }
       const int part0 = plan->n_parts;
       for (int c = 0; c < nch; ++c) {
         const int p0 = (int)((int64_t)np * c / nch), p1 = (int)((int64_t)np * (c + 1) / nch);
-        plan->items.push_back(AttnItem{i, h, p0, p1, plan->n_parts++});
+        plan->items.push_back(AttnItem{i, h, p0, p1, plan->n_parts++, (int32_t)plan->combs.size()});
       }
       plan->combs.push_back(AttnComb{i, h, part0, nch});
     }
@@ -332,15 +343,16 @@ void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, At
 }
 
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd) {
+  // items + combs (op path) | part_o | part_ml | arrival counters
   return (int64_t)max_items * sizeof(AttnItem) + (int64_t)max_items * sizeof(AttnComb) +
-         (int64_t)max_parts * g * (hd + 2) * sizeof(float) + 1024;
+         (int64_t)max_parts * g * (hd + 2) * sizeof(float) + (int64_t)max_items * sizeof(int) + 2048;
 }
 
 template <int HD>
 static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx,
-                                 const int32_t* row_slot, const AttnItem* items, int n_items, const int32_t* counts, int nq,
-                                 int nkv, int max_pages, void* out,
-                                 int out_fp32, float* part_o, float* part_ml, cudaStream_t stream) {
+                                 const int32_t* row_slot, const AttnItem* items, int n_items, const int32_t* counts,
+                                 int nq, int nkv, int max_pages, void* out, int out_fp32, float* part_o,
+                                 float* part_ml, const AttnComb* combs, int* arrive, cudaStream_t stream) {
   constexpr int STAGE = 2 * PAGE_T * HD * 2;
   const size_t ring = (size_t)ATTN_WARPS * ATTN_STAGES * STAGE;
   const size_t merge = (size_t)ATTN_WARPS * 16 * (HD + 2) * sizeof(float);
@@ -353,40 +365,31 @@ static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* b
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
   return launch_pdl(attn_decode_kernel<HD>, dim3(n_items), dim3(128), smem, stream,
                     reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx,
-                    row_slot, items, n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml);
+                    row_slot, items, n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml,
+                    combs, arrive);
 }
 
 cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const int32_t* row_slot,
-                        const int32_t* counts, const AttnItem* items,
-                        int n_items, const AttnComb* combs, int n_combs, int nq, int nkv, int hd, int page,
-                        int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
-                        cudaStream_t stream) {
+                        const int32_t* counts, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs,
+                        int nq, int nkv, int hd, int page, int max_pages, void* out, int out_fp32, float* part_o,
+                        float* part_ml, int* arrive, cudaStream_t stream) {
+  (void)n_combs;
   if (page != PAGE_T) return cudaErrorInvalidValue;
   if (nq % nkv != 0 || nq / nkv > 16) return cudaErrorInvalidValue;
   if (n_items <= 0) return cudaSuccess;
-  cudaError_t e;
   switch (hd) {
     case 32:
-      e = launch_decode<32>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
-                            stream);
-      break;
+      return launch_decode<32>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
+                               part_o, part_ml, combs, arrive, stream);
     case 64:
-      e = launch_decode<64>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32, part_o, part_ml,
-                            stream);
-      break;
+      return launch_decode<64>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
+                               part_o, part_ml, combs, arrive, stream);
     case 128:
-      e = launch_decode<128>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32, part_o,
-                             part_ml, stream);
-      break;
+      return launch_decode<128>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
+                                part_o, part_ml, combs, arrive, stream);
     default:
       return cudaErrorInvalidValue;
   }
-  if (e != cudaSuccess) return e;
-  if (n_combs > 0) {
-    e = launch_pdl(attn_combine_kernel, dim3(n_combs), dim3(128), 0, stream, combs, n_combs, counts, nq, nkv, hd,
-                   part_o, part_ml, out, out_fp32);
-  }
-  return e;
 }
 
 }  // namespace sgs

@@ -157,17 +157,20 @@ cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, co
 }
 
 // ------------------------------------------------------------------ SwiGLU
+// gu rows use the interleaved gate/up layout: feature i has its gate value at
+// column (i/64)*128 + i%64 and its up value 64 columns later.
 __global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restrict__ m, int f) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.y;
-  float* g = gu + (size_t)t * 2 * f;
-  float* u = g + f;
+  float* row = gu + (size_t)t * 2 * f;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i < f; i += gridDim.x * blockDim.x * 2) {
-    const float2 gv = *reinterpret_cast<const float2*>(g + i);
-    const float2 uv = *reinterpret_cast<const float2*>(u + i);
-    *reinterpret_cast<float2*>(g + i) = make_float2(0.f, 0.f);  // zeroed for a split-K successor
-    *reinterpret_cast<float2*>(u + i) = make_float2(0.f, 0.f);
+    float* g = row + (i / 64) * 128 + (i % 64);
+    float* u = g + 64;
+    const float2 gv = *reinterpret_cast<const float2*>(g);
+    const float2 uv = *reinterpret_cast<const float2*>(u);
+    *reinterpret_cast<float2*>(g) = make_float2(0.f, 0.f);  // zeroed for a split-K successor
+    *reinterpret_cast<float2*>(u) = make_float2(0.f, 0.f);
     const float s0 = gv.x / (1.f + __expf(-gv.x)), s1 = gv.y / (1.f + __expf(-gv.y));
     *reinterpret_cast<uint32_t*>(m + (size_t)t * f + i) = pack_bf16x2(s0 * uv.x, s1 * uv.y);
   }
@@ -254,17 +257,29 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, int64_t n, int is_norm) {
+// Physical index of logical element i of a [rows x cols] tensor stored with
+// row blocks of `blk` rows every `stride` rows starting at `off` (blk 0:
+// contiguous).  The gate/up weights interleave 64-row blocks so
+// one 128-row GEMM tile holds the gate and up rows of the same 64 features.
+__device__ __forceinline__ int64_t phys_index(int64_t i, int64_t cols, int blk, int stride, int off) {
+  if (blk == 0) return i;
+  const int64_t r = i / cols, c = i - r * cols;
+  return ((r / blk) * stride + off + r % blk) * cols + c;
+}
+
+__global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, int64_t n, int is_norm, int64_t cols,
+                                 int blk, int stride, int off) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t h = splitmix64(key + (uint64_t)i);
     const int32_t m = (int32_t)(h >> 40) - (1 << 23);
     const float u = (float)m * (1.0f / 8388608.0f);
     const float v = is_norm ? __fadd_rn(1.0f, __fmul_rn(u, 0.125f)) : __fmul_rn(u, 0.034641016f);
-    dst[i] = __float2bfloat16_rn(v);
+    dst[phys_index(i, cols, blk, stride, off)] = __float2bfloat16_rn(v);
   }
 }
 
-cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream) {
+cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
+                      int64_t cols, int blk, int stride, int off) {
   // key = splitmix64(seed ^ tensor_id * C): computed on the host, same constant as DESIGN.md §3
   uint64_t z = seed ^ (tensor_id * 0xD1B54A32D192ED03ull);
   z += 0x9E3779B97F4A7C15ull;
@@ -274,24 +289,28 @@ cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, i
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  hash_init_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<__nv_bfloat16*>(dst), key, n, is_norm);
+  hash_init_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<__nv_bfloat16*>(dst), key, n, is_norm, cols, blk,
+                                               stride, off);
   return cudaGetLastError();
 }
 
-__global__ void checksum_kernel(const uint16_t* __restrict__ src, int64_t n, unsigned long long* out) {
+__global__ void checksum_kernel(const uint16_t* __restrict__ src, int64_t n, unsigned long long* out, int64_t cols,
+                                int blk, int stride, int off) {
   unsigned long long acc = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    acc += (unsigned long long)src[i] * (unsigned long long)(2 * i + 1);
+    acc += (unsigned long long)src[phys_index(i, cols, blk, stride, off)] * (unsigned long long)(2 * i + 1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
-cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream) {
+cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream, int64_t cols,
+                          int blk, int stride, int off) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  checksum_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint16_t*>(src), n, out_dev);
+  checksum_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint16_t*>(src), n, out_dev, cols, blk, stride,
+                                              off);
   return cudaGetLastError();
 }
 

@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + stages;
   uint64_t* tmem_full = empty + stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [64][17] SwiGLU exchange (mode 3)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * GEMM_BM;
@@ -126,6 +127,29 @@ __global__ void __launch_bounds__(256, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[j]);
+      }
+      if (mode == 3) {
+        // fused SwiGLU: this tile's rows 0..63 are gate rows and 64..127 the up
+        // rows of the same 64 features; warps 2-3 hand their up values to warps
+        // 0-1 through shared memory, which write m = bf16(SiLU(g) * u)
+        if (e >= 2)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xch[((e - 2) * 32 + lane) * 17 + j] = acc[j];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (e < 2) {
+          const int feat = (m0 >> 1) + 32 * e + lane;
+          __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(C);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int t = n0 + c + j;
+            if (t < T) {
+              const float g = acc[j], u = xch[(32 * e + lane) * 17 + j];
+              M[(size_t)t * ldc + feat] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+            }
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        continue;
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -244,7 +268,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
   if (stages > 12) stages = 12;
   if (stages > kc) stages = kc < 2 ? 2 : kc;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16 + 64 * 17 * 4;
   // accumulator interleave: as many TMEM accumulators as fit (<= 8), each 32-column aligned
   const int acc_stride = (BN + 31) / 32 * 32;
   int n_acc = (small ? 256 : 512) / acc_stride;

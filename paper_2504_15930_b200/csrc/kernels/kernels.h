@@ -8,6 +8,8 @@
 namespace sgs {
 
 // ---- GEMM (gemm.cu): C[t, n] (+)= X[t, :] . W[n, :]; mode 0 store, 1 atomic add, 2 add
+// mode 3: fused SwiGLU epilogue for gate/up weights in the interleaved
+// layout; C is then bf16 [T, ldc] with ldc = N/2 (requires splits == 1).
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
                       cudaStream_t stream);
 int gemm_auto_splits(int N, int K, int T);
@@ -15,6 +17,7 @@ int gemm_auto_splits(int N, int K, int T);
 // ---- decode attention (attention.cu)
 struct AttnItem {
   int32_t row, kvh, p0, p1, part;  // part < 0: the item covers the whole row -> final output
+  int32_t comb;                     // split items: index of their AttnComb
 };
 struct AttnComb {
   int32_t row, kvh, part0, nparts;
@@ -31,12 +34,14 @@ void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, At
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
 // items/combs are device arrays (already copied); part buffers in workspace.
 // block_table rows are indexed by row_slot[row] (NULL: by row); ctx is per row.
+// Split items merge in-kernel: the last part of a (row, kv head) to finish
+// combines (arrive = zero-initialised int[n_combs] counters, self re-arming).
 // counts (device, optional): {n_items, n_combs} read by the kernels, in which
 // case n_items / n_combs are only the launch capacities (CUDA-graph replay).
 cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
                         const int32_t* row_slot, const int32_t* counts, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
                         int hd, int page, int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
-                        cudaStream_t stream);
+                        int* arrive, cudaStream_t stream);
 
 // ---- prefill attention (prefill_attn.cu): causal within each prompt.
 // q [T, nq, hd], k/v [T, nkv, hd] contiguous bf16; prompt p spans rows
@@ -56,8 +61,11 @@ cudaError_t silu_mul(const float* gu, void* m, int T, int f, cudaStream_t stream
 cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, const int32_t* slot,
                         const int32_t* tok_idx, int32_t* last_tok, int32_t* out_hist, int max_gen,
                         cudaStream_t stream);
-cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream);
-cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream);
+// Row-block mapping (blk, stride, off) for the interleaved gate/up weights; blk 0 = contiguous.
+cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
+                      int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
+cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream,
+                          int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
 cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream);
 
 }  // namespace sgs

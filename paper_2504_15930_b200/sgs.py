@@ -27,6 +27,7 @@ EXPORTS = [
     "sgs_kernel_launches", "sgs_fit_profile", "sgs_dispatch_plan", "sgs_attn_workspace_bytes",
     "sgs_op_decode_attention", "sgs_op_gemm", "sgs_op_rmsnorm", "sgs_op_rope_append", "sgs_rope_table",
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
+    "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log",
 ]
 
 
@@ -118,6 +119,9 @@ def _declare(L):
     L.sgs_op_argmax.argtypes = [vp, i32, i32, vp, vp]
     L.sgs_kernel_stats.argtypes = [vp, i32, P(ctypes.c_double), P(ctypes.c_double), P(ctypes.c_double), P(i64), i32]
     L.sgs_io_bytes.argtypes = [vp, P(i64), P(i64)]
+    L.sgs_set_roofline.argtypes = [vp, ctypes.c_double, ctypes.c_double]
+    L.sgs_kernel_roofline_ms.argtypes = [vp, i32, P(ctypes.c_double)]
+    L.sgs_iter_log.argtypes = [vp, P(i64), i64, P(i64)]
     L.sgs_op_silu_mul.argtypes = [vp, vp, i32, i32, vp]
     L.sgs_debug_forward.argtypes = [vp, P(i32), i32, P(ctypes.c_float)]
     L.sgs_op_prefill_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
@@ -324,6 +328,23 @@ class Instance:
         _check(lib().sgs_kernel_stats(self.h, cls, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(fl),
                                       ctypes.byref(n), int(reset)), self.h)
         return dict(ms=ms.value, bytes=by.value, flops=fl.value, launches=n.value)
+
+    def set_roofline(self, bw_gbs: float, tflops: float):
+        _check(lib().sgs_set_roofline(self.h, bw_gbs, tflops), self.h)
+
+    def kernel_roofline_ms(self, cls: int) -> float:
+        v = ctypes.c_double()
+        _check(lib().sgs_kernel_roofline_ms(self.h, cls, ctypes.byref(v)), self.h)
+        return v.value
+
+    def iter_log(self) -> np.ndarray:
+        """[n, 6] int64: t, b, admitted, prefill tokens, sum of contexts, device us."""
+        n = ctypes.c_int64()
+        _check(lib().sgs_iter_log(self.h, None, 0, ctypes.byref(n)), self.h)
+        buf = np.zeros(n.value, np.int64)
+        _check(lib().sgs_iter_log(self.h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n.value,
+                                  ctypes.byref(n)), self.h)
+        return buf.reshape(-1, 6)
 
     def io_bytes(self):
         a, b = ctypes.c_int64(), ctypes.c_int64()

@@ -99,7 +99,7 @@ def test_decode_attention_vs_fp64(sgs, nq, nkv, hd, ctxs, split):
     for i in range(b):
         err = _rel_err(got[i], ref[i])
         assert err.max() <= 1e-3, (i, ctxs[i], float(err.max()))
-    # bf16 output mode = the fp32 result rounded once
+    # bf16 output mode = the fp32 result rounded once (same merge order)
     outb = torch.zeros(b, nq, hd, dtype=torch.bfloat16, device="cuda")
     sgs.op_decode_attention(q.cuda(), pool, bt.cuda(), ctx.cuda(), outb, split_pages=split)
     torch.cuda.synchronize()
@@ -220,3 +220,41 @@ def test_prefill_attention_vs_fp64(sgs, nq, nkv, hd, lens):
             # bf16 output: within 1e-3 relative of the fp64 result plus one bf16 rounding
             err = np.abs(got[r] - ref).max(-1) / np.abs(ref).max(-1)
             assert err.max() <= 1e-3 + 2 ** -8, (p, t, float(err.max()))
+
+
+def _interleave_gate_up(Wg, Wu):
+    # 64-row blocks: tile i of the fused matrix = gate rows 64i..64i+63, then up rows 64i..64i+63
+    f, K = Wg.shape
+    return torch.stack([Wg.view(f // 64, 64, K), Wu.view(f // 64, 64, K)], 1).reshape(2 * f, K)
+
+
+@pytest.mark.parametrize("f,K,T", [(512, 128, 5), (18944, 3584, 1), (18944, 3584, 96), (13824, 5120, 300)])
+def test_gemm_fused_swiglu_vs_fp64(sgs, f, K, T):
+    Wg, Wu = _bf((f, K), 3, 0.02), _bf((f, K), 4, 0.02)
+    X = _bf((T, K), 5, 1.0)
+    m = torch.empty(T, f, dtype=torch.bfloat16, device="cuda")
+    sgs.op_gemm(_interleave_gate_up(Wg, Wu).cuda(), X.cuda(), m, mode=3, splits=1)
+    torch.cuda.synchronize()
+    g = X.double() @ Wg.double().T
+    u = X.double() @ Wu.double().T
+    ref = g * torch.sigmoid(g) * u
+    got = m.cpu().double()
+    # one bf16 rounding of fp32 values: <= 1 ulp apart, plus the fp32 accumulation
+    # error of g and u (relative to |g|, |u|, which matters where m ~ 0)
+    acc = 1e-5 * (g.abs() + 1) * (u.abs() + 1)
+    assert ((got - ref).abs() <= ref.abs() * 2 ** -7 + acc).all()
+    assert (got == ref.float().to(torch.bfloat16).double()).double().mean() > 0.99
+
+
+def test_silu_mul_interleaved_vs_fp64(sgs):
+    T, f = 7, 512
+    gu = torch.randn(T, 2 * f, generator=torch.Generator().manual_seed(9)) * 3
+    m = torch.empty(T, f, dtype=torch.bfloat16, device="cuda")
+    gud = gu.cuda()
+    sgs.op_silu_mul(gud, m)
+    torch.cuda.synchronize()
+    blk = gu.double().view(T, f // 64, 2, 64)
+    g, u = blk[:, :, 0].reshape(T, f), blk[:, :, 1].reshape(T, f)
+    ref = g * torch.sigmoid(g) * u
+    assert ((m.cpu().double() - ref).abs() <= ref.abs() * 2 ** -7 + 1e-6).all()
+    assert torch.count_nonzero(gud) == 0  # consumer-zeroed split-K accumulator
