@@ -30,6 +30,14 @@ import numpy as np  # noqa: E402
 import workload  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+# T(b) profiles (t0_ns, k0_ps, b_star, k1_ps) used by Alg. 2's Eq. 2; fitted by tools/tb_sweep.py
+# (config 5) on B200 — see profiles/r01_tb_sweep.json.  Only the dispatch (N > 1) reads them.
+DEFAULT_PROFILES = {
+    "qwen2.5-7b": (2000, 1000, 208, 5000),
+    "qwen2.5-14b": (4000, 2000, 208, 10000),
+    "qwen2.5-32b": (9000, 4500, 208, 22000),
+    "tiny": (200, 100, 64, 400),
+}
 
 
 def load_peaks():
@@ -154,6 +162,10 @@ def main():
     ap.add_argument("--max-out", type=int, default=None, help="cap forced lengths (profiling runs only)")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--iter-log", default=None, help="write the per-iteration log (t,b,adm,pf_tok,sumctx,us) as .npy")
+    ap.add_argument("--dispatch", default="skew", choices=["skew", "random", "round_robin"])
+    ap.add_argument("--strong", action="store_true", help="fixed global batch (cfg.n_prompts) instead of per GPU")
+    ap.add_argument("--profile", default=None, help="T(b) profile t0_ns,k0_ps,b_star,k1_ps for Alg. 2")
+    ap.add_argument("--hint-noise", type=float, default=None, help="ranker noise sigma (None: oracle hints)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -176,11 +188,13 @@ def main():
         cfg = dataclasses.replace(cfg, max_out=args.max_out, median_out=min(cfg.median_out, args.max_out // 4))
     shape = workload.MODELS[cfg.model]
     per_gpu = args.prompts_per_gpu or cfg.n_prompts
-    n_total = per_gpu * world
+    n_total = cfg.n_prompts if args.strong else per_gpu * world
     max_ctx = cfg.prompt_len + cfg.max_out
 
+    prof = tuple(int(x) for x in args.profile.split(",")) if args.profile else DEFAULT_PROFILES.get(cfg.model)
     inst = sgs.Instance(shape, cfg.max_batch, max_ctx, device=local, n_instances=world, instance_rank=rank,
-                        weight_seed=cfg.seed, flags=0 if args.no_kernel_timing else sgs.sgs.F_KERNEL_TIMING)
+                        weight_seed=cfg.seed, flags=0 if args.no_kernel_timing else sgs.sgs.F_KERNEL_TIMING,
+                        dispatch=args.dispatch, profile=prof, sample_seed=cfg.seed)
     peaks0 = load_peaks()
     inst.set_roofline(peaks0["hbm_gbs"], peaks0["bf16_tflops_sustained"])
     if world > 1:
@@ -191,7 +205,7 @@ def main():
     def make_batch(step):
         # a fresh RL batch per step: same length distribution, new ids and prompts
         return workload.make_trace(n_total, cfg.prompt_len, cfg.median_out, cfg.sigma, cfg.max_out, shape.vocab,
-                                   seed=cfg.seed + 1000 * step, id_base=step * 1_000_000)
+                                   seed=cfg.seed + 1000 * step, id_base=step * 1_000_000, hint_noise=args.hint_noise)
 
     stream = inst.stream
 
@@ -290,7 +304,7 @@ def main():
         "ms_per_step": round(1e3 * dev_s / args.steps, 1),
         "rl_batch_completion_s": round(dev_s / args.steps, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
@@ -298,6 +312,8 @@ def main():
                                f"x {cfg.prompt_len} tokens, lognormal(median {cfg.median_out}, sigma {cfg.sigma}) "
                                f"forced lengths <= {cfg.max_out}, B={cfg.max_batch}, longest-first, Alg. 2 dispatch",
                    "prompts_total": n_total, "global_batch": n_total, "parallelism": f"dp{world}",
+                   "dispatch": args.dispatch, "hints": "oracle (= forced)" if args.hint_noise is None else
+                   f"noisy sigma {args.hint_noise}", "profile": list(prof) if prof else None,
                    "l2": "inputs larger than L2 (weights 15 GB, KV pool > 100 GB)"},
         "e2e": {"value": round(tokens / wall_s, 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(statistics.mean(r["h2d"] for r in results)),

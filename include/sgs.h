@@ -176,6 +176,11 @@ sgs_status sgs_last_logits(sgs_handle* h, float* logits, uint64_t* ids, int32_t*
  * residual stream after the embedding and after every residual add into
  * dump (host, [(2*n_layers+1) x T x d_model]). */
 sgs_status sgs_debug_forward(sgs_handle* h, const int32_t* tokens, int32_t T, float* dump);
+/* Layer-local parity hook: run decoder layer `layer` of the CUDA path (prefill
+ * form, positions 0..T-1, slot 0, idle handle only) on the fp32 residual
+ * stream h_in (host [T x d_model]) and return the stream after the layer's
+ * MLP residual add in h_out (host [T x d_model]). */
+sgs_status sgs_debug_layer(sgs_handle* h, int32_t layer, const float* h_in, int32_t T, float* h_out);
 
 /* Device-side timing of the last iteration's kernels (CUDA events), ms. */
 sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms);

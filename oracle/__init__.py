@@ -92,6 +92,7 @@ def _declare(L):
     L.oracle_decoder_forward.restype = ctypes.c_int32
     L.oracle_decoder_dump.argtypes = [P_i32, P_f64, ctypes.c_uint64, P_i32, ctypes.c_int32, P_f64]
     L.oracle_decoder_dump.restype = ctypes.c_int32
+    L.oracle_decoder_layer.argtypes = [P_i32, P_f64, ctypes.c_uint64, ctypes.c_int32, P_f64, ctypes.c_int32, P_f64]
     L.oracle_rmsnorm.argtypes = [P_f64, P_f32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P_f64]
     L.oracle_rope.argtypes = [P_f64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
     L.oracle_argmax.argtypes = [P_f32, ctypes.c_int64]
@@ -307,6 +308,17 @@ def decoder_dump(shape, seed: int, tokens):
     out = np.zeros((2 * shape.n_layers + 1, T, shape.d_model), np.float64)
     if lib().oracle_decoder_dump(_p(ci, P_i32), _p(cd, P_f64), seed, _p(toks, P_i32), T, _p(out, P_f64)) != 0:
         raise RuntimeError(lib().oracle_last_error().decode())
+    return out
+
+
+def decoder_layer(shape, seed: int, layer: int, h_in):
+    """One decoder layer on the residual stream h_in [T, d] (positions 0..T-1) -> [T, d] float64."""
+    h = np.ascontiguousarray(h_in, np.float64)
+    ci = np.array([shape.n_layers, shape.d_model, shape.n_q_heads, shape.n_kv_heads, shape.head_dim,
+                   shape.d_ffn, shape.vocab], np.int32)
+    cd = np.array([shape.rms_eps, shape.rope_theta], np.float64)
+    out = np.zeros_like(h)
+    lib().oracle_decoder_layer(_p(ci, P_i32), _p(cd, P_f64), seed, layer, _p(h, P_f64), h.shape[0], _p(out, P_f64))
     return out
 
 

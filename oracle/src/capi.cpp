@@ -161,6 +161,13 @@ int32_t oracle_decoder_dump(const int32_t* cfg_i, const double* cfg_d, uint64_t 
   }
 }
 
+int32_t oracle_decoder_layer(const int32_t* cfg_i, const double* cfg_d, uint64_t seed, int32_t layer,
+                             const double* h_in, int32_t T, double* h_out) {
+  ModelCfg c{cfg_i[0], cfg_i[1], cfg_i[2], cfg_i[3], cfg_i[4], cfg_i[5], cfg_i[6], cfg_d[0], cfg_d[1]};
+  decoder_layer(c, seed, layer, h_in, T, h_out);
+  return 0;
+}
+
 // y = bf16(x / sqrt(mean(x^2) + eps) * w), rows of x [T x d]
 void oracle_rmsnorm(const double* x, const float* w, int32_t T, int32_t d, double eps, double* y) {
   std::vector<double> h(x, x + (size_t)T * d), out;

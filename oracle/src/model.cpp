@@ -164,6 +164,75 @@ void rope(double* v, int hd, int pos, double theta) {
   }
 }
 
+// One decoder layer (pre-norm attention + SwiGLU MLP, both residual) on the
+// residual stream h [T x d], positions 0..T-1, in place.  save(h) is called
+// after each residual add.
+template <typename Save>
+static void layer_forward(const ModelCfg& c, uint64_t seed, int l, std::vector<double>& h, int T, Save&& save) {
+  const int d = c.d, hd = c.hd, nq = c.nq, nkv = c.nkv;
+  std::vector<double> x, q, k, v, y, g, u;
+  const uint64_t b = 16 + 16 * (uint64_t)l;
+  auto wn1 = tensor(seed, b + 10, d, 1);
+  rmsnorm_bf16(h, T, d, wn1, c.eps, x);
+  {
+    auto Wq = tensor(seed, b + 0, (int64_t)nq * hd * d, 0);
+    auto Wk = tensor(seed, b + 1, (int64_t)nkv * hd * d, 0);
+    auto Wv = tensor(seed, b + 2, (int64_t)nkv * hd * d, 0);
+    auto bq = tensor(seed, b + 3, nq * hd, 0), bk = tensor(seed, b + 4, nkv * hd, 0),
+         bv = tensor(seed, b + 5, nkv * hd, 0);
+    matmul(x, T, d, Wq, nq * hd, q);
+    matmul(x, T, d, Wk, nkv * hd, k);
+    matmul(x, T, d, Wv, nkv * hd, v);
+    for (int t = 0; t < T; ++t) {
+      for (int j = 0; j < nq * hd; ++j) q[(size_t)t * nq * hd + j] += bq[j];
+      for (int j = 0; j < nkv * hd; ++j) k[(size_t)t * nkv * hd + j] += bk[j], v[(size_t)t * nkv * hd + j] += bv[j];
+      for (int hh = 0; hh < nq; ++hh) rope(&q[((size_t)t * nq + hh) * hd], hd, t, c.theta);
+      for (int hh = 0; hh < nkv; ++hh) rope(&k[((size_t)t * nkv + hh) * hd], hd, t, c.theta);
+    }
+    for (auto& e : q) e = bf16_round((float)e);
+    for (auto& e : k) e = bf16_round((float)e);
+    for (auto& e : v) e = bf16_round((float)e);
+  }
+  // causal attention, position t attends to 0..t
+  std::vector<double> o((size_t)T * nq * hd);
+  {
+    std::vector<float> qf(nq * hd), Kf((size_t)T * nkv * hd), Vf((size_t)T * nkv * hd);
+    for (size_t i = 0; i < Kf.size(); ++i) Kf[i] = (float)k[i], Vf[i] = (float)v[i];
+    std::vector<double> ot(nq * hd);
+    for (int t = 0; t < T; ++t) {
+      for (int i = 0; i < nq * hd; ++i) qf[i] = (float)q[(size_t)t * nq * hd + i];
+      attention_fp64(nq, nkv, hd, t + 1, qf.data(), Kf.data(), Vf.data(), ot.data());
+      for (int i = 0; i < nq * hd; ++i) o[(size_t)t * nq * hd + i] = bf16_round((float)ot[i]);
+    }
+  }
+  {
+    auto Wo = tensor(seed, b + 6, (int64_t)d * nq * hd, 0);
+    matmul(o, T, nq * hd, Wo, d, y);
+    for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
+  }
+  save(h);
+  auto wn2 = tensor(seed, b + 11, d, 1);
+  rmsnorm_bf16(h, T, d, wn2, c.eps, x);
+  {
+    auto Wg = tensor(seed, b + 7, (int64_t)c.ffn * d, 0);
+    matmul(x, T, d, Wg, c.ffn, g);
+  }
+  {
+    auto Wu = tensor(seed, b + 8, (int64_t)c.ffn * d, 0);
+    matmul(x, T, d, Wu, c.ffn, u);
+  }
+  for (size_t i = 0; i < g.size(); ++i) {
+    double sg = g[i] / (1.0 + std::exp(-g[i]));  // SiLU
+    g[i] = bf16_round((float)(sg * u[i]));
+  }
+  {
+    auto Wd = tensor(seed, b + 9, (int64_t)d * c.ffn, 0);
+    matmul(g, T, c.ffn, Wd, d, y);
+    for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
+  }
+  save(h);
+}
+
 void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, int T, int first_row,
                      double* logits, double* dump) {
   const int d = c.d, hd = c.hd, nq = c.nq, nkv = c.nkv;
@@ -181,69 +250,8 @@ void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, in
         h[(size_t)t * d + i] = weight_value(seed, 0, (uint64_t)tokens[t] * d + i, 0);
   }
   save(h);
-  std::vector<double> x, q, k, v, y, g, u;
-  for (int l = 0; l < c.n_layers; ++l) {
-    const uint64_t b = 16 + 16 * (uint64_t)l;
-    auto wn1 = tensor(seed, b + 10, d, 1);
-    rmsnorm_bf16(h, T, d, wn1, c.eps, x);
-    {
-      auto Wq = tensor(seed, b + 0, (int64_t)nq * hd * d, 0);
-      auto Wk = tensor(seed, b + 1, (int64_t)nkv * hd * d, 0);
-      auto Wv = tensor(seed, b + 2, (int64_t)nkv * hd * d, 0);
-      auto bq = tensor(seed, b + 3, nq * hd, 0), bk = tensor(seed, b + 4, nkv * hd, 0),
-           bv = tensor(seed, b + 5, nkv * hd, 0);
-      matmul(x, T, d, Wq, nq * hd, q);
-      matmul(x, T, d, Wk, nkv * hd, k);
-      matmul(x, T, d, Wv, nkv * hd, v);
-      for (int t = 0; t < T; ++t) {
-        for (int j = 0; j < nq * hd; ++j) q[(size_t)t * nq * hd + j] += bq[j];
-        for (int j = 0; j < nkv * hd; ++j) k[(size_t)t * nkv * hd + j] += bk[j], v[(size_t)t * nkv * hd + j] += bv[j];
-        for (int hh = 0; hh < nq; ++hh) rope(&q[((size_t)t * nq + hh) * hd], hd, t, c.theta);
-        for (int hh = 0; hh < nkv; ++hh) rope(&k[((size_t)t * nkv + hh) * hd], hd, t, c.theta);
-      }
-      for (auto& e : q) e = bf16_round((float)e);
-      for (auto& e : k) e = bf16_round((float)e);
-      for (auto& e : v) e = bf16_round((float)e);
-    }
-    // causal attention, position t attends to 0..t
-    std::vector<double> o((size_t)T * nq * hd);
-    {
-      std::vector<float> qf(nq * hd), Kf((size_t)T * nkv * hd), Vf((size_t)T * nkv * hd);
-      for (size_t i = 0; i < Kf.size(); ++i) Kf[i] = (float)k[i], Vf[i] = (float)v[i];
-      std::vector<double> ot(nq * hd);
-      for (int t = 0; t < T; ++t) {
-        for (int i = 0; i < nq * hd; ++i) qf[i] = (float)q[(size_t)t * nq * hd + i];
-        attention_fp64(nq, nkv, hd, t + 1, qf.data(), Kf.data(), Vf.data(), ot.data());
-        for (int i = 0; i < nq * hd; ++i) o[(size_t)t * nq * hd + i] = bf16_round((float)ot[i]);
-      }
-    }
-    {
-      auto Wo = tensor(seed, b + 6, (int64_t)d * nq * hd, 0);
-      matmul(o, T, nq * hd, Wo, d, y);
-      for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
-    }
-    save(h);
-    auto wn2 = tensor(seed, b + 11, d, 1);
-    rmsnorm_bf16(h, T, d, wn2, c.eps, x);
-    {
-      auto Wg = tensor(seed, b + 7, (int64_t)c.ffn * d, 0);
-      matmul(x, T, d, Wg, c.ffn, g);
-    }
-    {
-      auto Wu = tensor(seed, b + 8, (int64_t)c.ffn * d, 0);
-      matmul(x, T, d, Wu, c.ffn, u);
-    }
-    for (size_t i = 0; i < g.size(); ++i) {
-      double sg = g[i] / (1.0 + std::exp(-g[i]));  // SiLU
-      g[i] = bf16_round((float)(sg * u[i]));
-    }
-    {
-      auto Wd = tensor(seed, b + 9, (int64_t)d * c.ffn, 0);
-      matmul(g, T, c.ffn, Wd, d, y);
-      for (size_t i = 0; i < h.size(); ++i) h[i] += y[i];
-    }
-    save(h);
-  }
+  for (int l = 0; l < c.n_layers; ++l) layer_forward(c, seed, l, h, T, save);
+  std::vector<double> x, y;
   auto wf = tensor(seed, 2, d, 1);
   const int R = T - first_row;
   std::vector<double> hl((size_t)R * d);
@@ -252,6 +260,12 @@ void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, in
   auto Wl = tensor(seed, 1, (int64_t)c.vocab * d, 0);
   matmul(x, R, d, Wl, c.vocab, y);
   std::memcpy(logits, y.data(), sizeof(double) * (size_t)R * c.vocab);
+}
+
+void decoder_layer(const ModelCfg& c, uint64_t seed, int layer, const double* h_in, int T, double* h_out) {
+  std::vector<double> h(h_in, h_in + (size_t)T * c.d);
+  layer_forward(c, seed, layer, h, T, [](const std::vector<double>&) {});
+  std::memcpy(h_out, h.data(), sizeof(double) * (size_t)T * c.d);
 }
 
 // C8 greedy: argmax, lowest index on ties.

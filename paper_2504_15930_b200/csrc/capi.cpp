@@ -124,6 +124,11 @@ sgs_status sgs_debug_forward(sgs_handle* h, const int32_t* tokens, int32_t T, fl
   return h->eng.debug_forward(tokens, T, dump);
 }
 
+sgs_status sgs_debug_layer(sgs_handle* h, int32_t layer, const float* h_in, int32_t T, float* h_out) {
+  if (!h || !h_in || !h_out || layer < 0) return SGS_E_INVAL;
+  return h->eng.debug_forward(nullptr, T, h_out, layer, h_in);
+}
+
 sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms) {
   if (!h || !ms) return SGS_E_INVAL;
   *ms = h->eng.last_ms;

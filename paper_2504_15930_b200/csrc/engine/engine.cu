@@ -771,20 +771,27 @@ sgs_status Engine::run_decode(int b) {
 sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, const int32_t* d_tokens,
                                  const int32_t* d_pos, const int32_t* d_slot, const int32_t* d_offs,
                                  const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
-                                 const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump) {
+                                 const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump,
+                                 int only_layer, const float* h_in) {
   const int d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn,
             V = m_.vocab;
   const int qkvN = (nq + 2 * nkv) * hd;
   const int np = (int)idx.size();
-  CK(embed(embed_, d_tokens, nullptr, nullptr, h_, T, d, st_), "embed");
-  ++launches;
   int n_dump = 0;
   auto save = [&]() -> cudaError_t {
     if (!dump) return cudaSuccess;
     return cudaMemcpyAsync(dump + (size_t)(n_dump++) * T * d, h_, (size_t)T * d * 4, cudaMemcpyDeviceToHost, st_);
   };
-  CK(save(), "dump");
-  for (int l = 0; l < m_.n_layers; ++l) {
+  if (h_in) {  // layer-local parity: start from a given residual stream
+    CK(cudaMemcpyAsync(h_, h_in, (size_t)T * d * 4, cudaMemcpyHostToDevice, st_), "h_in");
+  } else {
+    CK(embed(embed_, d_tokens, nullptr, nullptr, h_, T, d, st_), "embed");
+    ++launches;
+    CK(save(), "dump");
+  }
+  const int l_begin = only_layer >= 0 ? only_layer : 0;
+  const int l_end = only_layer >= 0 ? only_layer + 1 : m_.n_layers;
+  for (int l = l_begin; l < l_end; ++l) {
     const Layer& Ly = layers_[l];
     CK(rmsnorm(h_, Ly.n1, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm1");
     CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, T, false), "gemm qkv");
@@ -803,6 +810,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     CK(save(), "dump");
     launches += 5;
   }
+  if (only_layer >= 0) return SGS_OK;
   CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
   float* lg = logits_ + (size_t)((e_.max_batch + 15) / 16 * 16 + row_base) * V;
   CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
@@ -813,7 +821,13 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
 
 // Standalone prefill forward of one prompt in slot 0 (idle handle only) with
 // the residual stream dumped after the embedding and every residual add.
-sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump) {
+sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, int layer, const float* h_in) {
+  if (layer >= m_.n_layers || (layer >= 0 && !h_in) || (layer < 0 && !tokens)) {
+    err = "debug_forward: bad layer / input";
+    return SGS_E_INVAL;
+  }
+  std::vector<int32_t> zeros;
+  if (!tokens) zeros.assign(T > 0 ? T : 0, 0), tokens = zeros.data();
   if (null_ || !sched.idle()) {
     err = "debug_forward needs a device handle with nothing in flight";
     return SGS_E_STATE;
@@ -843,7 +857,7 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump) 
   CK(apply_bt_deltas(bt_, L_.max_pages, MD, np, st_), "bt");
   std::vector<int32_t> idx(1, 0);
   sgs_status s = prefill_chunk(idx, 0, MD + o_tok, MD + o_pos, MD + o_slot, MD + o_offs, MD + o_qb, (T + 63) / 64,
-                               MD + o_last, MD + o_last + 1, MD + o_last + 2, T, dump);
+                               MD + o_last, MD + o_last + 1, MD + o_last + 2, T, dump, layer, h_in);
   if (s != SGS_OK) return s;
   CK(cudaStreamSynchronize(st_), "debug sync");
   return SGS_OK;

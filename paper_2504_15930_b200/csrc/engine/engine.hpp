@@ -53,7 +53,8 @@ class Engine {
   sgs_status comm_init(const uint8_t id[128], int rank, int world);
   sgs_status update_weights(int root);
   sgs_status last_logits(float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap, int32_t* rows);
-  sgs_status debug_forward(const int32_t* tokens, int32_t T, float* dump);
+  sgs_status debug_forward(const int32_t* tokens, int32_t T, float* dump, int layer = -1,
+                           const float* h_in = nullptr);
 
   static sgs_status layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64_t n_pages, ArenaLayout* L);
 
@@ -78,7 +79,8 @@ class Engine {
   sgs_status prefill_chunk(const std::vector<int32_t>& idx, int row_base, const int32_t* d_tokens,
                            const int32_t* d_pos, const int32_t* d_slot, const int32_t* d_offs,
                            const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
-                           const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump = nullptr);
+                           const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump = nullptr,
+                           int only_layer = -1, const float* h_in = nullptr);
   cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
   cudaError_t gate_up(const void* W, int T);
   void build_tensor_table();

@@ -26,13 +26,21 @@ constexpr int GEMM_BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;
 constexpr int GEMM_SMEM_BUDGET = 200 * 1024;
 
+// CG = 1: one CTA per 128-row weight tile (decode-sized token tiles).
+// CG = 2: a CTA pair (cluster of 2) computes a 256-row tile with
+// tcgen05.mma.cta_group::2: each CTA stages its 128 weight rows and half of
+// the token tile, the leader issues the MMAs, and the accumulator rows land in
+// each CTA's own TMEM.  Per SM this halves the token-tile shared-memory
+// traffic, which bounds the 1-CTA kernel at large token tiles.
+template <int CG>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
                         int chunks_per_split, int mode, int tmem_cols, int n_acc, int acc_stride) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int b_bytes = BN * GEMM_BK * 2;
+  const int bl = BN / CG;                 // token rows staged by this CTA
+  const int b_bytes = bl * GEMM_BK * 2;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)stages * GEMM_A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)stages * b_bytes);
@@ -42,6 +50,8 @@ __global__ void __launch_bounds__(256, 1)
   float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [64][17] SwiGLU exchange (mode 3)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
   const int m0 = blockIdx.x * GEMM_BM;
   const int n0 = blockIdx.y * BN;
   const int kc0 = blockIdx.z * chunks_per_split;
@@ -56,54 +66,84 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(tmem_full, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 2) {
+    if (CG == 2)
+      tmem_alloc_2sm(tmem_slot, tmem_cols);
+    else
+      tmem_alloc(tmem_slot, tmem_cols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // the peer's barriers exist before any cross-CTA arrival
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   pdl_trigger();
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (both CTAs; the leader's barrier counts both CTAs' bytes)
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
+    const uint32_t tx = (uint32_t)CG * (GEMM_A_BYTES + b_bytes);
+    auto load_a = [&](int s, int i) {
+      if (CG == 2)
+        tma_load_2d_2sm(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
+      else
+        tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
+    };
+    auto load_b = [&](int s, int i) {
+      if (CG == 2)
+        tma_load_2d_2sm(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0 + (int)rank * bl, &full[s]);
+      else
+        tma_load_2d(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[s]);
+    };
     // The weight tiles do not depend on the previous kernel: fill the ring
     // with them before waiting for it (overlaps the weight stream with the
     // predecessor's tail), then load the activation tiles.
     const int pre = nk < stages ? nk : stages;
     for (int i = 0; i < pre; ++i) {
-      mbar_expect_tx(&full[i], GEMM_A_BYTES + b_bytes);
-      tma_load_2d(sA + (size_t)i * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[i]);
+      if (leader) mbar_expect_tx(&full[i], tx);
+      load_a(i, i);
     }
     pdl_wait();
-    for (int i = 0; i < pre; ++i) tma_load_2d(sB + (size_t)i * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[i]);
+    for (int i = 0; i < pre; ++i) load_b(i, i);
     for (int i = pre; i < nk; ++i) {
       const int s = i % stages;
       mbar_wait(&empty[s], ((i / stages) - 1) & 1);
-      mbar_expect_tx(&full[s], GEMM_A_BYTES + b_bytes);
-      tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
-      tma_load_2d(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[s]);
+      if (leader) mbar_expect_tx(&full[s], tx);
+      load_a(s, i);
+      load_b(s, i);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
-    const uint32_t idesc = umma_idesc_bf16(GEMM_BM, BN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (single thread of the leader CTA)
+    const uint32_t idesc = umma_idesc_bf16(GEMM_BM * CG, BN);
     for (int i = 0; i < nk; ++i) {
       const int s = i % stages;
       mbar_wait(&full[s], (i / stages) & 1);
       tc_fence_after();
       const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * GEMM_A_BYTES));
       const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_bytes));
-#pragma unroll
       // k-chunk i accumulates into TMEM accumulator i % n_acc: the tensor-core
       // fp32 accumulation truncates, so short chains + an IEEE fp32 sum of the
       // accumulators in the epilogue keep the error at fp32-GEMM level.
       const uint32_t d = tmem + (uint32_t)((i % n_acc) * acc_stride);
 #pragma unroll
-      for (int k = 0; k < GEMM_BK / 16; ++k)  // K = 16 per MMA: advance 32 B inside the swizzle atom
-        umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
-      umma_commit(&empty[s]);
+      for (int k = 0; k < GEMM_BK / 16; ++k) {  // K = 16 per MMA: advance 32 B inside the swizzle atom
+        if (CG == 2)
+          umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+        else
+          umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+      }
+      if (CG == 2)
+        umma_commit_2sm(&empty[s]);
+      else
+        umma_commit(&empty[s]);
     }
-    umma_commit(tmem_full);
+    if (CG == 2)
+      umma_commit_2sm(tmem_full);
+    else
+      umma_commit(tmem_full);
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global (lane = output feature)
     const int e = warp - 4;
@@ -168,10 +208,16 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // the leader's MMAs read the peer's shared memory until tmem_full
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, tmem_cols);
+    if (CG == 2)
+      tmem_dealloc_2sm(tmem, tmem_cols);
+    else
+      tmem_dealloc(tmem, tmem_cols);
   }
 }
 
@@ -252,6 +298,8 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (T <= 0) return cudaSuccess;
   if (N % GEMM_BM != 0 || K % GEMM_BK != 0) return cudaErrorInvalidValue;
   const int BN = T >= 256 ? 256 : ((T + 15) / 16) * 16;
+  // CTA pairs for compute-bound token tiles (BN >= 128) when the 256-row pair tiles N
+  const int CG = (BN >= 128 && N % (2 * GEMM_BM) == 0) ? 2 : 1;
   const int kc = K / GEMM_BK;
   if (splits <= 0) splits = mode == 1 ? gemm_auto_splits(N, K, T) : 1;
   if (splits > 1 && mode != 1) return cudaErrorInvalidValue;
@@ -259,8 +307,8 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   splits = (kc + per - 1) / per;  // every split has >= 1 chunk
   CUtensorMap tw, tx;
   if (!cached_tmap(&tw, W, N, K, GEMM_BM)) return cudaErrorInvalidValue;
-  if (!cached_tmap(&tx, X, T, K, BN)) return cudaErrorInvalidValue;
-  const int stage_bytes = GEMM_A_BYTES + BN * GEMM_BK * 2;
+  if (!cached_tmap(&tx, X, T, K, BN / CG)) return cudaErrorInvalidValue;
+  const int stage_bytes = GEMM_A_BYTES + (BN / CG) * GEMM_BK * 2;
   // decode-sized tiles (BN <= 64) use half the shared memory and TMEM so two
   // CTAs fit on an SM: the next GEMM (PDL) streams its weights while the
   // current one drains
@@ -279,12 +327,28 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   while (tmem_cols < n_acc * acc_stride) tmem_cols <<= 1;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_bf16_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_bf16_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   dim3 grid(N / GEMM_BM, (T + BN - 1) / BN, splits);
-  return launch_pdl(gemm_bf16_tc_kernel, grid, dim3(256), smem, stream, tw, tx, C, T, ldc, BN, stages, kc, per, mode,
-                    tmem_cols, n_acc, acc_stride);
+  if (CG == 1)
+    return launch_pdl(gemm_bf16_tc_kernel<1>, grid, dim3(256), smem, stream, tw, tx, C, T, ldc, BN, stages, kc, per,
+                      mode, tmem_cols, n_acc, acc_stride);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc_kernel<2>, tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols,
+                            n_acc, acc_stride);
 }
 
 }  // namespace sgs

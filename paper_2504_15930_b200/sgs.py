@@ -27,7 +27,7 @@ EXPORTS = [
     "sgs_kernel_launches", "sgs_fit_profile", "sgs_dispatch_plan", "sgs_attn_workspace_bytes",
     "sgs_op_decode_attention", "sgs_op_gemm", "sgs_op_rmsnorm", "sgs_op_rope_append", "sgs_rope_table",
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
-    "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log",
+    "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer",
 ]
 
 
@@ -122,6 +122,7 @@ def _declare(L):
     L.sgs_set_roofline.argtypes = [vp, ctypes.c_double, ctypes.c_double]
     L.sgs_kernel_roofline_ms.argtypes = [vp, i32, P(ctypes.c_double)]
     L.sgs_iter_log.argtypes = [vp, P(i64), i64, P(i64)]
+    L.sgs_debug_layer.argtypes = [vp, i32, P(ctypes.c_float), i32, P(ctypes.c_float)]
     L.sgs_op_silu_mul.argtypes = [vp, vp, i32, i32, vp]
     L.sgs_debug_forward.argtypes = [vp, P(i32), i32, P(ctypes.c_float)]
     L.sgs_op_prefill_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
@@ -316,6 +317,14 @@ class Instance:
         out = np.zeros((2 * self.shape.n_layers + 1, len(toks), self.shape.d_model), np.float32)
         _check(lib().sgs_debug_forward(self.h, _i32p(toks), len(toks),
                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))), self.h)
+        return out
+
+    def debug_layer(self, layer: int, h_in) -> np.ndarray:
+        """Run one decoder layer of the CUDA path on h_in [T, d] (fp32); returns h after the layer."""
+        h = np.ascontiguousarray(h_in, np.float32)
+        out = np.zeros_like(h)
+        _check(lib().sgs_debug_layer(self.h, layer, h.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), h.shape[0],
+                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))), self.h)
         return out
 
     def last_iter_ms(self) -> float:

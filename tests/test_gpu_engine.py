@@ -135,3 +135,28 @@ def test_7b_shape_spot_parity(sgs):
     assert np.array_equal(inst.trace(0), o["iter_blob"])
     worst = _check_teacher_forced(shape, 4321, tr, comps, rows, tr.ids[:2].tolist(), tol=TOL_7B_28L)
     print("7B worst max-abs logits error", worst)
+
+
+@pytest.mark.parametrize("model", ["qwen2.5-7b", "qwen2.5-14b", "qwen2.5-32b"])
+def test_layer_local_parity_full_shapes(sgs, model):
+    # Layer-local parity: the CUDA path's decoder layer l applied to
+    # a residual stream supplied by the test equals the oracle's layer l on the
+    # same input to within half a bf16 ulp of the largest element (the depth
+    # chaos of the end-to-end comparison does not enter); sampled layers of the
+    # full 7B/14B/32B shapes, T = 40 positions (spans the 16-token pages and a
+    # partial 64-query prefill block).
+    shape = workload.MODELS[model]
+    inst = sgs.Instance(shape, 4, 128, device=0, n_pages=64, weight_seed=77)
+    rng = np.random.default_rng(0)
+    T = 40
+    for layer in sorted({0, shape.n_layers // 2, shape.n_layers - 1}):
+        h_in = (rng.standard_normal((T, shape.d_model)) * (1.0 + layer / 8)).astype(np.float32)
+        got = inst.debug_layer(layer, h_in).astype(np.float64)
+        ref = oracle.decoder_layer(shape, 77, layer, h_in.astype(np.float64))
+        err = np.abs(got - ref).max()
+        scale = np.abs(ref).max()
+        print(model, "layer", layer, "max err", err, "max |h|", scale)
+        assert err <= scale * 2 ** -8, (model, layer, err, scale)
+    inst.close()
+    del inst
+    torch.cuda.empty_cache()

@@ -232,3 +232,13 @@ def test_rope_invariants():
     e = np.zeros(hd); e[0] = 1.0
     r = oracle.rope(e, 3, theta)
     assert abs(r[0] - np.cos(3)) < 1e-15 and abs(r[hd // 2] - np.sin(3)) < 1e-15
+
+
+def test_decoder_layer_composes_to_forward():
+    # regression pin of the layer-local entry point: layer l applied to the
+    # stream after layer l-1 reproduces the full forward's dump bit for bit
+    shape = workload.MODELS["tiny"]
+    toks = np.random.default_rng(5).integers(0, shape.vocab, size=20)
+    dump = oracle.decoder_dump(shape, 9, toks)
+    for l in range(shape.n_layers):
+        assert np.array_equal(oracle.decoder_layer(shape, 9, l, dump[2 * l]), dump[2 * l + 2])
