@@ -263,6 +263,15 @@ sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v,
  * gu is zeroed after it is read. */
 sgs_status sgs_op_silu_mul(const float* gu, void* m, int32_t T, int32_t f, void* stream);
 
+/* K9 top-p (R18): p = softmax(logits/temperature) in fp32; nucleus =
+ * shortest prefix in (p desc, id asc) order with mass >= top_p; u = 24-bit
+ * uniform of Philox4x32-10(key = seed, ctr = (sample_id, step)) times the
+ * nucleus mass; ids[r] = first token of that order whose cumulative mass > u.
+ * sample_ids: device uint64 [rows]; steps: device int32 [rows]. */
+sgs_status sgs_op_sample_top_p(const float* logits, int32_t rows, int32_t V, float temperature, float top_p,
+                               uint64_t seed, const uint64_t* sample_ids, const int32_t* steps, int32_t* ids,
+                               void* stream);
+
 /* K9 greedy: ids[r] = argmax_v logits[r, v] (lowest index on ties). */
 sgs_status sgs_op_argmax(const float* logits, int32_t rows, int32_t V, int32_t* ids, void* stream);
 

@@ -303,6 +303,15 @@ sgs_status sgs_op_silu_mul(const float* gu, void* m, int32_t T, int32_t f, void*
   return cuda_status(sgs::silu_mul(gu, m, T, f, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+sgs_status sgs_op_sample_top_p(const float* logits, int32_t rows, int32_t V, float temperature, float top_p,
+                               uint64_t seed, const uint64_t* sample_ids, const int32_t* steps, int32_t* ids,
+                               void* stream) {
+  if (!logits || !ids || !sample_ids || !steps || rows < 0 || V <= 0 || !(top_p > 0.f)) return SGS_E_INVAL;
+  return cuda_status(sgs::sample_top_p(logits, rows, V, temperature, top_p, seed,
+                                       reinterpret_cast<const uint32_t*>(sample_ids), ids, nullptr, steps, nullptr,
+                                       nullptr, 0, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 sgs_status sgs_op_argmax(const float* logits, int32_t rows, int32_t V, int32_t* ids, void* stream) {
   if (!logits || !ids || rows < 0 || V <= 0) return SGS_E_INVAL;
   return cuda_status(sgs::argmax_rows(logits, rows, V, ids, nullptr, nullptr, nullptr, nullptr, 0,

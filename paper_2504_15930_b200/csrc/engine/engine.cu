@@ -67,8 +67,9 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   // per-iteration metadata: bt deltas, prefill tokens/pos/slot, decode rows, attention work lists
   // attention work list bound of attn_plan: 2*148 + b*nkv (+ slack)
   const int64_t max_items = 2 * 148 + Bpad * nkv + 64;
-  // fixed decode region (graph-replayable): counts[4] | slot,pos,ctx,tok [Bpad] | combs | items
-  L->meta_dec_bytes = align_up(4 * (4 + 4 * Bpad) + max_items * (int64_t)(sizeof(AttnItem) + sizeof(AttnComb)), 256);
+  // fixed decode region (graph-replayable): counts[4] | slot,pos,ctx,tok [Bpad] | sample id (lo,hi) [Bpad]
+  // | combs | items
+  L->meta_dec_bytes = align_up(4 * (4 + 6 * Bpad) + max_items * (int64_t)(sizeof(AttnItem) + sizeof(AttnComb)), 256);
   // prefill tokens of one iteration: up to B admitted prompts of <= min(max_ctx, prefill chunk) tokens
   const int64_t adm_tok = B * std::min<int64_t>(e.max_ctx, pf);
   L->meta_bytes = L->meta_dec_bytes +
@@ -471,6 +472,17 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
   return e;
 }
 
+// a13: greedy (parity mode, lowest index on ties) or top-p with Philox keyed by
+// (sample_seed, sample id, token index); writes the next input token and the history
+cudaError_t Engine::sample(const float* logits, int rows, const uint32_t* sid, const int32_t* slot,
+                           const int32_t* tok_idx) {
+  ++launches;
+  if (e_.sampling == SGS_SAMPLE_TOP_P)
+    return sample_top_p(logits, rows, m_.vocab, e_.temperature, e_.top_p, e_.sample_seed, sid, nullptr, slot, tok_idx,
+                        last_tok_, hist_, max_gen_, st_);
+  return argmax_rows(logits, rows, m_.vocab, nullptr, slot, tok_idx, last_tok_, hist_, max_gen_, st_);
+}
+
 // m = bf16(SiLU(x Wg^T) * (x Wu^T)): one GEMM with the SwiGLU epilogue when
 // the gate/up GEMM needs no split-K (always at the model shapes: 2 f / 128 >=
 // 148 tiles), else the fp32 GEMM + the silu_mul kernel.
@@ -540,7 +552,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   }
   int row_base = 0;
   for (auto& c : chunks) {
-    std::vector<int32_t> tok, pos, slot, offs(1, 0), qb, last, pfs, pft;
+    std::vector<int32_t> tok, pos, slot, offs(1, 0), qb, last, pfs, pft, pfid;
     for (size_t k = 0; k < c.idx.size(); ++k) {
       const Sample& s = S[c.idx[k]];
       tok.insert(tok.end(), prompt_store_.begin() + s.tok_off, prompt_store_.begin() + s.tok_off + s.P);
@@ -550,6 +562,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
       last.push_back(offs.back() - 1);
       pfs.push_back(s.slot);
       pft.push_back(0);
+      pfid.push_back((int32_t)(uint32_t)s.id), pfid.push_back((int32_t)(uint32_t)(s.id >> 32));
     }
     c.o_tok = put(tok.data(), tok.size());
     c.o_pos = put(pos.data(), pos.size());
@@ -560,6 +573,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     c.o_last = put(last.data(), last.size());
     c.o_pfslot = put(pfs.data(), pfs.size());
     c.o_pftok = put(pft.data(), pft.size());
+    put(pfid.data(), pfid.size());  // sample ids (lo, hi), right after the token indices
     c.row_base = row_base;
     row_base += (int)c.idx.size();
   }
@@ -568,13 +582,16 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   const int Bk = (n_run + 15) / 16 * 16;  // CUDA-graph bucket; rows [n_run, Bk) are inert (slot -1)
   int32_t* D = reinterpret_cast<int32_t*>(meta_host_);
   int32_t *dslot = D + 4, *dpos = dslot + Bpad, *dctx = dpos + Bpad, *dtok = dctx + Bpad;
+  uint32_t* dsid = reinterpret_cast<uint32_t*>(dtok + Bpad);  // sample id (lo, hi) per row, top-p key
   for (int r = 0; r < Bk; ++r) {
     if (r < n_run) {
       const Sample& s = S[plan.running[r]];
       const int j = s.produced - 1;  // tokens generated before this iteration (plan already counted this one)
       dslot[r] = s.slot, dpos[r] = s.P + j - 1, dctx[r] = s.P + j, dtok[r] = j;
+      dsid[2 * r] = (uint32_t)s.id, dsid[2 * r + 1] = (uint32_t)(s.id >> 32);
     } else {
       dslot[r] = -1, dpos[r] = 0, dctx[r] = 1, dtok[r] = 0;
+      dsid[2 * r] = 0, dsid[2 * r + 1] = 0;
     }
   }
   AttnPlan ap;
@@ -585,7 +602,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     return SGS_E_NOMEM;
   }
   D[0] = (int32_t)ap.items.size(), D[1] = (int32_t)ap.combs.size(), D[2] = n_run, D[3] = 0;
-  AttnComb* hcombs = reinterpret_cast<AttnComb*>(D + 4 + 4 * Bpad);
+  AttnComb* hcombs = reinterpret_cast<AttnComb*>(D + 4 + 6 * Bpad);
   AttnItem* hitems = reinterpret_cast<AttnItem*>(hcombs + L_.max_items);
   std::memcpy(hcombs, ap.combs.data(), ap.combs.size() * sizeof(AttnComb));
   std::memcpy(hitems, ap.items.data(), ap.items.size() * sizeof(AttnItem));
@@ -706,7 +723,8 @@ sgs_status Engine::decode_body(int Bk) {
   const int32_t* d_pos = d_slot + Bpad;
   const int32_t* d_ctx = d_pos + Bpad;
   const int32_t* d_tok = d_ctx + Bpad;
-  const AttnComb* d_combs = reinterpret_cast<const AttnComb*>(d_tok + Bpad);
+  const uint32_t* d_sid = reinterpret_cast<const uint32_t*>(d_tok + Bpad);
+  const AttnComb* d_combs = reinterpret_cast<const AttnComb*>(d_tok + 3 * Bpad);
   const AttnItem* d_items = reinterpret_cast<const AttnItem*>(d_combs + L_.max_items);
   float* part_o = reinterpret_cast<float*>(attn_ws_);
   float* part_ml = part_o + (size_t)L_.max_items * (nq / nkv) * hd;
@@ -736,8 +754,8 @@ sgs_status Engine::decode_body(int Bk) {
   }
   CK(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm f");
   CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
-  CK(argmax_rows(logits_, Bk, V, nullptr, d_slot, d_tok, last_tok_, hist_, max_gen_, st_), "argmax");
-  launches += 2;
+  CK(sample(logits_, Bk, d_sid, d_slot, d_tok), "sampler");
+  launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }
 
@@ -814,8 +832,8 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
   CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
   float* lg = logits_ + (size_t)((e_.max_batch + 15) / 16 * 16 + row_base) * V;
   CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
-  CK(argmax_rows(lg, np, V, nullptr, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, st_), "argmax");
-  launches += 2;
+  CK(sample(lg, np, reinterpret_cast<const uint32_t*>(d_pf_tok + np), d_pf_slot, d_pf_tok), "sampler");
+  launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }
 
@@ -851,6 +869,7 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, 
   for (int b = 0; b < (T + 63) / 64; ++b) meta.push_back(0), meta.push_back(b);
   const size_t o_last = meta.size();
   meta.push_back(T - 1), meta.push_back(0), meta.push_back(0);  // last row, pf slot, pf tok
+  meta.push_back(0), meta.push_back(0);                         // sample id (lo, hi)
   std::memcpy(meta_host_, meta.data(), meta.size() * 4);
   const int32_t* MD = reinterpret_cast<const int32_t*>(meta_dev_);
   CK(cudaMemcpyAsync(meta_dev_, meta_host_, meta.size() * 4, cudaMemcpyHostToDevice, st_), "meta");

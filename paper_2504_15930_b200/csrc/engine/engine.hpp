@@ -83,6 +83,7 @@ class Engine {
                            int only_layer = -1, const float* h_in = nullptr);
   cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
   cudaError_t gate_up(const void* W, int T);
+  cudaError_t sample(const float* logits, int rows, const uint32_t* sid, const int32_t* slot, const int32_t* tok_idx);
   void build_tensor_table();
   // kernel-class timing record: bytes = bfix + brow * rows (bfix < 0: the
   // iteration's decode-attention bytes/flops), flops = frow * rows

@@ -249,6 +249,167 @@ cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, cons
                     out_hist, max_gen);
 }
 
+// ------------------------------------------------------------------ top-p sampler
+// DESIGN.md R18: p = softmax(logits / tau) (fp32); nucleus = shortest prefix of
+// the tokens ordered by (p desc, id asc) whose mass reaches top_p; u = 24-bit
+// uniform from Philox4x32-10(key = seed, ctr = (sample id, step)) scaled by the
+// nucleus mass; the sample is the token at which the cumulative mass in that
+// order first exceeds u.  No sort: the ordered cumulative mass is located by a
+// radix select over the bits of p (positive floats order like their bits), 8
+// bits per pass, with a block-wide 256-bin mass histogram.
+__device__ __forceinline__ void philox_dev(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                           uint32_t k1, uint32_t* out) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0, c1 = lo1, c2 = n2, c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0, out[1] = c1, out[2] = c2, out[3] = c3;
+}
+
+// Largest bit pattern P such that mass(p >= P) >= target (the p value of the
+// token at which the ordered cumulative mass reaches target); *above = mass(p > P).
+__device__ float radix_mass_select(const float* __restrict__ x, int V, float m, float inv_tau, float target,
+                                   uint32_t* P_out, float* above_out, float* hist) {
+  uint32_t prefix = 0, mask = 0;
+  float above = 0.f;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0.f;
+    __syncthreads();
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      const float p = __expf((x[i] - m) * inv_tau);
+      const uint32_t bits = __float_as_uint(p);
+      if ((bits & mask) == prefix) atomicAdd(&hist[(bits >> shift) & 255], p);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float c = above;
+      int k = 255;
+      for (; k > 0; --k) {
+        if (c + hist[k] >= target) break;
+        c += hist[k];
+      }
+      above = c;
+      prefix |= (uint32_t)k << shift;
+      mask |= 255u << shift;
+      hist[256] = above, reinterpret_cast<uint32_t*>(hist)[257] = prefix;
+    }
+    __syncthreads();
+    above = hist[256];
+    prefix = reinterpret_cast<uint32_t*>(hist)[257];
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  *P_out = prefix;
+  *above_out = above;
+  return __uint_as_float(prefix);
+}
+
+__global__ void __launch_bounds__(1024) top_p_kernel(const float* __restrict__ logits, int V, float inv_tau,
+                                                     float top_p, uint64_t seed, const uint32_t* __restrict__ sid,
+                                                     const int32_t* __restrict__ slot,
+                                                     const int32_t* __restrict__ tok_idx, int32_t* ids,
+                                                     int32_t* last_tok, int32_t* out_hist, int max_gen) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;
+  if (slot && slot[r] < 0) return;
+  const float* x = logits + (size_t)r * V;
+  __shared__ float hist[258];
+  __shared__ float red[32];
+  __shared__ int cnt[32];
+  // max and normaliser
+  float mx = -INFINITY;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) mx = fmaxf(mx, x[i]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    v = warp_max(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float m = red[0];
+  __syncthreads();
+  float z = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) z += __expf((x[i] - m) * inv_tau);
+  z = warp_sum(z);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = z;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float Z = red[0];
+  __syncthreads();
+  // nucleus: tokens with p > theta plus the first k_eq (by id) with p == theta
+  uint32_t tb;
+  float above;
+  const float theta = radix_mass_select(x, V, m, inv_tau, fminf(top_p, 1.f) * Z, &tb, &above, hist);
+  const int k_eq = max(1, (int)ceilf((fminf(top_p, 1.f) * Z - above) / theta));
+  const float mass = above + (float)k_eq * theta;
+  // u in [0, mass)
+  const uint64_t sidv = sid ? ((uint64_t)sid[2 * r] | ((uint64_t)sid[2 * r + 1] << 32)) : (uint64_t)r;
+  const uint64_t step = tok_idx ? (uint64_t)tok_idx[r] : 0;
+  uint32_t rnd[4];
+  philox_dev((uint32_t)sidv, (uint32_t)(sidv >> 32), (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)seed,
+             (uint32_t)(seed >> 32), rnd);
+  const float u = (float)(rnd[0] >> 8) * (1.0f / 16777216.0f) * mass;
+  // the token where the ordered cumulative mass first exceeds u
+  uint32_t ub;
+  float above_u;
+  // nextafter: the cumulative mass must strictly exceed u
+  const float theta_u = radix_mass_select(x, V, m, inv_tau, __uint_as_float(__float_as_uint(u) + 1), &ub, &above_u,
+                                          hist);
+  int j = (int)floorf((u - above_u) / theta_u);
+  if (ub == tb) j = min(j, k_eq - 1);
+  j = max(j, 0);
+  // j-th token (ascending id) with p == theta_u
+  __shared__ int chosen;
+  if (threadIdx.x == 0) chosen = -1;
+  __syncthreads();
+  int base = 0;
+  for (int i0 = 0; i0 < V && chosen < 0; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const bool eq = i < V && __float_as_uint(__expf((x[i] - m) * inv_tau)) == ub;
+    const unsigned bal = __ballot_sync(0xffffffffu, eq);
+    const int wpre = __popc(bal & ((1u << (threadIdx.x & 31)) - 1));
+    if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = __popc(bal);
+    __syncthreads();
+    int before = base;
+    for (int w = 0; w < (threadIdx.x >> 5); ++w) before += cnt[w];
+    int tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += cnt[w];
+    if (eq && before + wpre == j) chosen = i;
+    __syncthreads();
+    base += tot;
+  }
+  if (threadIdx.x == 0) {
+    const int tok = chosen >= 0 ? chosen : 0;
+    if (ids) ids[r] = tok;
+    if (slot) {
+      last_tok[slot[r]] = tok;
+      out_hist[(size_t)slot[r] * max_gen + tok_idx[r]] = tok;
+    }
+  }
+}
+
+cudaError_t sample_top_p(const float* logits, int rows, int V, float temperature, float top_p, uint64_t seed,
+                         const uint32_t* sample_ids, int32_t* ids, const int32_t* slot, const int32_t* tok_idx,
+                         int32_t* last_tok, int32_t* out_hist, int max_gen, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (temperature <= 0.f) return argmax_rows(logits, rows, V, ids, slot, tok_idx, last_tok, out_hist, max_gen, stream);
+  return launch_pdl(top_p_kernel, dim3(rows), dim3(1024), 0, stream, logits, V, 1.f / temperature, top_p, seed,
+                    sample_ids, slot, tok_idx, ids, last_tok, out_hist, max_gen);
+}
+
 // ------------------------------------------------------------------ weights
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;

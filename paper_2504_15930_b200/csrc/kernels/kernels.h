@@ -62,6 +62,10 @@ cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, cons
                         const int32_t* tok_idx, int32_t* last_tok, int32_t* out_hist, int max_gen,
                         cudaStream_t stream);
 // Row-block mapping (blk, stride, off) for the interleaved gate/up weights; blk 0 = contiguous.
+// top-p (nucleus) sampling, R18; sample_ids: uint32 pairs (lo, hi) per row.
+cudaError_t sample_top_p(const float* logits, int rows, int V, float temperature, float top_p, uint64_t seed,
+                         const uint32_t* sample_ids, int32_t* ids, const int32_t* slot, const int32_t* tok_idx,
+                         int32_t* last_tok, int32_t* out_hist, int max_gen, cudaStream_t stream);
 cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
                       int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
 cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream,

@@ -27,7 +27,7 @@ EXPORTS = [
     "sgs_kernel_launches", "sgs_fit_profile", "sgs_dispatch_plan", "sgs_attn_workspace_bytes",
     "sgs_op_decode_attention", "sgs_op_gemm", "sgs_op_rmsnorm", "sgs_op_rope_append", "sgs_rope_table",
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
-    "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer",
+    "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer", "sgs_op_sample_top_p",
 ]
 
 
@@ -123,6 +123,7 @@ def _declare(L):
     L.sgs_kernel_roofline_ms.argtypes = [vp, i32, P(ctypes.c_double)]
     L.sgs_iter_log.argtypes = [vp, P(i64), i64, P(i64)]
     L.sgs_debug_layer.argtypes = [vp, i32, P(ctypes.c_float), i32, P(ctypes.c_float)]
+    L.sgs_op_sample_top_p.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, u64, vp, vp, vp, vp]
     L.sgs_op_silu_mul.argtypes = [vp, vp, i32, i32, vp]
     L.sgs_debug_forward.argtypes = [vp, P(i32), i32, P(ctypes.c_float)]
     L.sgs_op_prefill_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
@@ -159,7 +160,8 @@ class Instance:
                  n_pages: int | None = None, mem_fraction: float = 0.92, n_instances: int = 1,
                  instance_rank: int = 0, dispatch: str = "skew", alpha_pct: int = 20, score: int = 0,
                  tail_ceil: int = 0, profile=(2000, 1000, 208, 5000), weight_seed: int = 1234,
-                 sample_seed: int = 0, flags: int = 0, max_prefill_tokens: int = 16384, stream=None):
+                 sample_seed: int = 0, flags: int = 0, max_prefill_tokens: int = 16384, stream=None,
+                 top_p: float | None = None, temperature: float = 1.0):
         L = lib()
         self.shape = shape
         self.m = model_cfg(shape)
@@ -169,7 +171,7 @@ class Instance:
         e.n_instances, e.instance_rank = n_instances, instance_rank
         e.dispatch, e.alpha_pct, e.score, e.tail_ceil = DISPATCH[dispatch], alpha_pct, score, tail_ceil
         e.profile = TbProfile(*profile)
-        e.sampling, e.temperature, e.top_p = 0, 1.0, 1.0
+        e.sampling, e.temperature, e.top_p = (1 if top_p is not None else 0), temperature, (top_p or 1.0)
         e.sample_seed, e.weight_seed, e.flags = sample_seed, weight_seed, flags
         self.arena = None
         self.stream = None
@@ -438,6 +440,12 @@ def op_rope_append(qkv, bias, pos, slot, block_table, cos_sin, q_out, kv, nq, nk
 def op_silu_mul(gu, m):
     T, f = m.shape
     _check(lib().sgs_op_silu_mul(_ptr(gu), _ptr(m), T, f, _cur_stream(gu)))
+
+
+def op_sample_top_p(logits, temperature, top_p, seed, sample_ids, steps, ids):
+    rows, V = logits.shape
+    _check(lib().sgs_op_sample_top_p(_ptr(logits), rows, V, temperature, top_p, seed, _ptr(sample_ids), _ptr(steps),
+                                     _ptr(ids), _cur_stream(logits)))
 
 
 def op_argmax(logits, ids):

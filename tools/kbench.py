@@ -68,10 +68,14 @@ def gemm_grid(out):
         for T in ARGS.T or (1, 16, 64, 128, 256):
             X = torch.randn(T, K, device="cuda").bfloat16()
             C = torch.zeros(T, N, device="cuda")
-            ms = bench(lambda i: sgs.op_gemm(Ws[i % nrot], X, C, mode=1, splits=0))
+            mode = 0 if T >= 256 else 1
+            ms = bench(lambda i: sgs.op_gemm(Ws[i % nrot], X, C, mode=mode, splits=1 if mode == 0 else 0))
+            # cuBLAS on the same operands (bf16 out), as the library yardstick
+            ms_cb = bench(lambda i: torch.matmul(X, Ws[i % nrot].t()))
             r = dict(kernel="gemm", name=name, N=N, K=K, T=T, us=round(ms * 1e3, 1),
                      GBs=round(N * K * 2 / ms / 1e6, 1), frac_hbm=round(N * K * 2 / ms / 1e6 / PEAK_GBS, 3),
-                     TFLOPs=round(2 * N * K * T / ms / 1e9, 1))
+                     TFLOPs=round(2 * N * K * T / ms / 1e9, 1), cublas_us=round(ms_cb * 1e3, 1),
+                     cublas_TFLOPs=round(2 * N * K * T / ms_cb / 1e9, 1))
             print(json.dumps(r), flush=True)
             out.append(r)
 
