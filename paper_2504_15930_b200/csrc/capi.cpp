@@ -224,7 +224,7 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
   for (int i = 0; i < b; ++i)
     if (hctx[i] < 1 || (hctx[i] + page - 1) / page > max_pages_per_seq) return SGS_E_INVAL;
   sgs::AttnPlan plan;
-  sgs::attn_plan(hctx.data(), b, nkv, page, split_pages, &plan);
+  sgs::attn_plan(hctx.data(), nullptr, b, nkv, page, split_pages, &plan);
   const int g = nq / nkv;
   const int64_t need = sgs::attn_workspace_bytes((int)plan.items.size(), plan.n_parts, g, hd);
   if (need > workspace_bytes) return SGS_E_NOMEM;
@@ -245,7 +245,7 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
   int* arrive = reinterpret_cast<int*>(part_ml + (size_t)std::max(plan.n_parts, 1) * g * 2);
   if (!plan.combs.empty() && cudaMemsetAsync(arrive, 0, plan.combs.size() * sizeof(int), st) != cudaSuccess)
     return SGS_E_CUDA;
-  cudaError_t e = sgs::attn_decode(q, kv, block_table, ctx, nullptr, nullptr, d_items, (int)plan.items.size(), d_combs,
+  cudaError_t e = sgs::attn_decode(q, kv, block_table, nullptr, d_items, (int)plan.items.size(), d_combs,
                                    (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, out_fp32,
                                    part_o, part_ml, arrive, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host plan vectors die here

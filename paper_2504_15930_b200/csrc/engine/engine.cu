@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "nccl.h"
@@ -148,6 +149,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
     return SGS_E_INVAL;
   }
   null_ = e.device < 0;
+  if (const char* sk = std::getenv("SGS_DEBUG_SKIP")) skip_ = std::atoi(sk);
   max_gen_ = e.max_ctx + 1;
   if (null_) {
     n_pages_ = e.n_pages;
@@ -595,7 +597,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     }
   }
   AttnPlan ap;
-  attn_plan(dctx, n_run, nkv, e_.page_size, 0, &ap);
+  attn_plan(dctx, dslot, n_run, nkv, e_.page_size, 0, &ap);
   if ((int)ap.items.size() > L_.max_items || ap.n_parts > L_.max_items) {
     err = "attention work list exceeds workspace";
     poisoned = true;
@@ -731,30 +733,35 @@ sgs_status Engine::decode_body(int Bk) {
   int* arrive = reinterpret_cast<int*>(part_ml + (size_t)L_.max_items * (nq / nkv) * 2);  // zeroed at init
   const int cap_items = std::min(L_.max_items, 2 * 148 + Bk * nkv + 64);
   const int cap_combs = Bk * nkv;
-  CK(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), "embed");
+  // SGS_DEBUG_SKIP (timing ablation only; results are garbage): bit k skips
+  // kernel class k of the decode program
+  auto on = [&](int bit) { return !(skip_ & (1 << bit)); };
+  if (on(9)) CK(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), "embed");
   ++launches;
   for (int l = 0; l < m_.n_layers; ++l) {
     const Layer& Ly = layers_[l];
-    CK(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm1");
-    CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false), "gemm qkv");
-    CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, Bk, nq, nkv,
-                   hd, e_.page_size, st_),
-       "rope_append");
+    if (on(0)) CK(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm1");
+    if (on(1)) CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false), "gemm qkv");
+    if (on(2))
+      CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, Bk, nq,
+                     nkv, hd, e_.page_size, st_),
+         "rope_append");
     KRec kr;
     ktic(&kr, 0);
-    CK(attn_decode(q_, Ly.kv, bt_, d_ctx, d_slot, counts, d_items, cap_items, d_combs, cap_combs, nq, nkv, hd,
-                   e_.page_size, L_.max_pages, ao_, 0, part_o, part_ml, arrive, st_),
-       "attn_decode");
+    if (on(3))
+      CK(attn_decode(q_, Ly.kv, bt_, counts, d_items, cap_items, d_combs, cap_combs, nq, nkv, hd, e_.page_size,
+                     L_.max_pages, ao_, 0, part_o, part_ml, arrive, st_),
+         "attn_decode");
     ktoc(&kr, -1.0, 0.0, 0.0, 0);
-    CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
-    CK(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm2");
-    CK(gate_up(Ly.wgu, Bk), "gemm gate_up + SwiGLU");
-    CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
+    if (on(4)) CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
+    if (on(0)) CK(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm2");
+    if (on(5)) CK(gate_up(Ly.wgu, Bk), "gemm gate_up + SwiGLU");
+    if (on(6)) CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
     launches += 6;
   }
-  CK(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm f");
-  CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
-  CK(sample(logits_, Bk, d_sid, d_slot, d_tok), "sampler");
+  if (on(0)) CK(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm f");
+  if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
+  if (on(8)) CK(sample(logits_, Bk, d_sid, d_slot, d_tok), "sampler");
   launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }
@@ -797,7 +804,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
   const int np = (int)idx.size();
   int n_dump = 0;
   auto save = [&]() -> cudaError_t {
-    if (!dump) return cudaSuccess;
+    if (!dump || only_layer >= 0) return cudaSuccess;  // layer-local mode returns only the final h
     return cudaMemcpyAsync(dump + (size_t)(n_dump++) * T * d, h_, (size_t)T * d * 4, cudaMemcpyDeviceToHost, st_);
   };
   if (h_in) {  // layer-local parity: start from a given residual stream
@@ -828,7 +835,10 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     CK(save(), "dump");
     launches += 5;
   }
-  if (only_layer >= 0) return SGS_OK;
+  if (only_layer >= 0) {
+    if (dump) CK(cudaMemcpyAsync(dump, h_, (size_t)T * d * 4, cudaMemcpyDeviceToHost, st_), "h_out");
+    return SGS_OK;
+  }
   CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
   float* lg = logits_ + (size_t)((e_.max_batch + 15) / 16 * 16 + row_base) * V;
   CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");

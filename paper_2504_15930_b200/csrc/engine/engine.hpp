@@ -109,6 +109,7 @@ class Engine {
   };
   std::vector<DecodeGraph> graphs_[2];  // [timed]: variant with event-record nodes
   bool timing_now_ = false;             // this iteration is a timing sample
+  int skip_ = 0;                        // SGS_DEBUG_SKIP ablation mask (decode program)
   int64_t timing_iter_ = 0;
   static constexpr int kTimingStride = 32;  // 1 in 32 iterations carries the per-kernel events
   std::vector<KRec>* rec_target_ = nullptr;  // non-null while capturing

@@ -37,8 +37,7 @@ __device__ __forceinline__ void combine_merge(const AttnComb& c, int nq, int nkv
 template <int HD>
 __global__ void __launch_bounds__(128, 2)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv,
-                       const int32_t* __restrict__ bt, const int32_t* __restrict__ ctx,
-                       const int32_t* __restrict__ row_slot, const AttnItem* __restrict__ items, int n_items,
+                       const int32_t* __restrict__ bt, const AttnItem* __restrict__ items, int n_items,
                        const int32_t* __restrict__ counts,
                        int nq, int nkv, int max_pages,
                        float scale_log2, void* __restrict__ out, int out_fp32, float* __restrict__ part_o,
@@ -51,13 +50,20 @@ __global__ void __launch_bounds__(128, 2)
   __shared__ uint64_t bars[ATTN_WARPS][ATTN_STAGES];
 
   pdl_trigger();
-  pdl_wait();
-  if ((int)blockIdx.x >= (counts ? counts[0] : n_items)) return;
+  // Before griddepcontrol.wait: the work item, the block table and every KV
+  // page that does not hold the newest token were written before this CUDA
+  // graph (stream segment) started, so their loads overlap the predecessor
+  // kernels; only q and the newest page (rope_append's output) wait.
+  if ((int)blockIdx.x >= (counts ? counts[0] : n_items)) {
+    pdl_wait();
+    return;
+  }
   const AttnItem it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = nq / nkv;
-  const int L = ctx[it.row];
-  const int32_t* btr = bt + (size_t)(row_slot ? row_slot[it.row] : it.row) * max_pages;
+  const int L = it.ctx;
+  const int last_page = (L - 1) / PAGE_T;  // written by the predecessor this iteration
+  const int32_t* btr = bt + (size_t)it.slot * max_pages;
   uint8_t* my = smem + (size_t)warp * ATTN_STAGES * STAGE;
 
   if (lane == 0) {
@@ -75,8 +81,14 @@ __global__ void __launch_bounds__(128, 2)
     mbar_expect_tx(b, STAGE);
     bulk_g2s(my + (size_t)(i % ATTN_STAGES) * STAGE, src, STAGE, b);
   };
+  const int first = n_my < ATTN_STAGES ? n_my : ATTN_STAGES;
+  int pre = 0;  // ring slots whose page is complete (pages ascend with i)
+  while (pre < first && it.p0 + warp + ATTN_WARPS * pre < last_page) ++pre;
   if (lane == 0)
-    for (int i = 0; i < n_my && i < ATTN_STAGES; ++i) issue(i);
+    for (int i = 0; i < pre; ++i) issue(i);
+  pdl_wait();
+  if (lane == 0)
+    for (int i = pre; i < first; ++i) issue(i);
 
   // q fragments (A operand, rows = heads of the group)
   const int r0 = lane >> 2, r1 = r0 + 8, cq = 2 * (lane & 3);
@@ -307,7 +319,7 @@ __device__ __forceinline__ void combine_merge(const AttnComb& c, int nq, int nkv
 }
 
 // ------------------------------------------------------------------ host side
-void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, AttnPlan* plan) {
+void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page, int split_pages, AttnPlan* plan) {
   plan->items.clear();
   plan->combs.clear();
   plan->n_parts = 0;
@@ -326,13 +338,14 @@ void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, At
     if (nch > ATTN_MAX_PARTS) nch = ATTN_MAX_PARTS;
     for (int h = 0; h < nkv; ++h) {
       if (nch == 1) {
-        plan->items.push_back(AttnItem{i, h, 0, np, -1, -1});
+        plan->items.push_back(AttnItem{i, h, 0, np, -1, -1, slot ? slot[i] : i, ctx[i]});
         continue;
       }
       const int part0 = plan->n_parts;
       for (int c = 0; c < nch; ++c) {
         const int p0 = (int)((int64_t)np * c / nch), p1 = (int)((int64_t)np * (c + 1) / nch);
-        plan->items.push_back(AttnItem{i, h, p0, p1, plan->n_parts++, (int32_t)plan->combs.size()});
+        plan->items.push_back(
+            AttnItem{i, h, p0, p1, plan->n_parts++, (int32_t)plan->combs.size(), slot ? slot[i] : i, ctx[i]});
       }
       plan->combs.push_back(AttnComb{i, h, part0, nch});
     }
@@ -349,8 +362,8 @@ int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd) {
 }
 
 template <int HD>
-static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx,
-                                 const int32_t* row_slot, const AttnItem* items, int n_items, const int32_t* counts,
+static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* bt, const AttnItem* items,
+                                 int n_items, const int32_t* counts,
                                  int nq, int nkv, int max_pages, void* out, int out_fp32, float* part_o,
                                  float* part_ml, const AttnComb* combs, int* arrive, cudaStream_t stream) {
   constexpr int STAGE = 2 * PAGE_T * HD * 2;
@@ -364,13 +377,13 @@ static cudaError_t launch_decode(const void* q, const void* kv, const int32_t* b
   }
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
   return launch_pdl(attn_decode_kernel<HD>, dim3(n_items), dim3(128), smem, stream,
-                    reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt, ctx,
-                    row_slot, items, n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml,
+                    reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kv), bt,
+                    items, n_items, counts, nq, nkv, max_pages, scale_log2, out, out_fp32, part_o, part_ml,
                     combs, arrive);
 }
 
-cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* ctx, const int32_t* row_slot,
-                        const int32_t* counts, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs,
+cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const int32_t* counts,
+                        const AttnItem* items, int n_items, const AttnComb* combs, int n_combs,
                         int nq, int nkv, int hd, int page, int max_pages, void* out, int out_fp32, float* part_o,
                         float* part_ml, int* arrive, cudaStream_t stream) {
   (void)n_combs;
@@ -379,13 +392,13 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const 
   if (n_items <= 0) return cudaSuccess;
   switch (hd) {
     case 32:
-      return launch_decode<32>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
+      return launch_decode<32>(q, kv, bt, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
                                part_o, part_ml, combs, arrive, stream);
     case 64:
-      return launch_decode<64>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
+      return launch_decode<64>(q, kv, bt, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
                                part_o, part_ml, combs, arrive, stream);
     case 128:
-      return launch_decode<128>(q, kv, bt, ctx, row_slot, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
+      return launch_decode<128>(q, kv, bt, items, n_items, counts, nq, nkv, max_pages, out, out_fp32,
                                 part_o, part_ml, combs, arrive, stream);
     default:
       return cudaErrorInvalidValue;

@@ -16,56 +16,75 @@
 namespace sgs {
 
 // ------------------------------------------------------------------ RMSNorm
+// One block per row, d/8 threads, 8 elements per thread held in registers
+// (single pass over x).  The weight row is loaded before griddepcontrol.wait
+// (weights never change inside a launch sequence).
+template <int VPT>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                                __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ rows, int d, float eps) {
   pdl_trigger();
+  const int i0 = threadIdx.x * 4 * VPT;
+  uint2 wb[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) wb[k] = *reinterpret_cast<const uint2*>(w + i0 + 4 * k);
   pdl_wait();
   const int t = blockIdx.x;
   const int src = rows ? rows[t] : t;
   const float* xr = x + (size_t)src * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + i);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  // fp64 sum of squares and scaling (latency-bound kernel: the arithmetic is
+  // free), so the bf16 rounding of x sees the fp32 residual exactly scaled
+  float4 v[VPT];
+  double ss = 0.0;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    v[k] = *reinterpret_cast<const float4*>(xr + i0 + 4 * k);
+    ss += (double)v[k].x * v[k].x + (double)v[k].y * v[k].y + (double)v[k].z * v[k].z + (double)v[k].w * v[k].w;
   }
-  __shared__ float red[32];
-  ss = warp_sum(ss);
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
+    double a = threadIdx.x < ((blockDim.x + 31) >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) red[0] = a;
   }
   __syncthreads();
-  const float r = rsqrtf(red[0] / (float)d + eps);
+  const double r = 1.0 / sqrt(red[0] / (double)d + (double)eps);
   __nv_bfloat16* yr = y + (size_t)t * d;
-  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + i);
-    const uint2 wb = *reinterpret_cast<const uint2*>(w + i);
-    const float w0 = __uint_as_float(wb.x << 16), w1 = __uint_as_float(wb.x & 0xffff0000u);
-    const float w2 = __uint_as_float(wb.y << 16), w3 = __uint_as_float(wb.y & 0xffff0000u);
+  auto f = [&](float x, uint32_t wbits) { return (float)((double)x * r * (double)__uint_as_float(wbits)); };
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
     uint2 o;
-    o.x = pack_bf16x2(v.x * r * w0, v.y * r * w1);
-    o.y = pack_bf16x2(v.z * r * w2, v.w * r * w3);
-    *reinterpret_cast<uint2*>(yr + i) = o;
+    o.x = pack_bf16x2(f(v[k].x, wb[k].x << 16), f(v[k].y, wb[k].x & 0xffff0000u));
+    o.y = pack_bf16x2(f(v[k].z, wb[k].y << 16), f(v[k].w, wb[k].y & 0xffff0000u));
+    *reinterpret_cast<uint2*>(yr + i0 + 4 * k) = o;
   }
 }
 
 cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows, int T, int d, float eps,
                     cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  if (d % 4) return cudaErrorInvalidValue;
-  int threads = d >= 1024 ? 256 : 128;
-  return launch_pdl(rmsnorm_kernel, dim3(T), dim3(threads), 0, stream, x, reinterpret_cast<const __nv_bfloat16*>(w),
-                    reinterpret_cast<__nv_bfloat16*>(y), rows, d, eps);
+  auto W = reinterpret_cast<const __nv_bfloat16*>(w);
+  auto Y = reinterpret_cast<__nv_bfloat16*>(y);
+  // the sum of squares is a warp/block reduction whose order depends on the
+  // thread count; every row uses the same configuration for a given d
+  if (d % 8 == 0 && d / 8 <= 1024 && d / 8 >= 32)
+    return launch_pdl(rmsnorm_kernel<2>, dim3(T), dim3(d / 8), 0, stream, x, W, Y, rows, d, eps);
+  if (d % 4 == 0 && d / 4 <= 1024 && d / 4 >= 32)
+    return launch_pdl(rmsnorm_kernel<1>, dim3(T), dim3(d / 4), 0, stream, x, W, Y, rows, d, eps);
+  return cudaErrorInvalidValue;
 }
 
 // ------------------------------------------------------------------ RoPE + KV append
-// One block per row.  Pair index j in [0, (nq+2nkv) * hd/2): head = j / half,
-// i = j % half.  q/k heads rotate (x_i, x_{i+half}); v heads copy.  The fp32
-// qkv row is zeroed after it is read, so the next split-K QKV GEMM (fp32 red.add)
-// finds a zeroed accumulator without a memset.
+// Grid (row, 128-pair group): thread j of the group handles pair index
+// j in [0, (nq+2nkv) * hd/2): head = j / half, i = j % half.  q/k heads rotate
+// (x_i, x_{i+half}); v heads copy.  Everything but the qkv row (position,
+// slot, block-table entry, bias, cos/sin) is read before griddepcontrol.wait.
+// The fp32 qkv row is zeroed after it is read, so the next split-K QKV GEMM
+// (fp32 red.add) finds a zeroed accumulator without a memset.
 __global__ void rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                    const int32_t* __restrict__ bt, int max_pages, const float* __restrict__ cs,
@@ -73,51 +92,54 @@ __global__ void rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16*
                                    __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out, int nq,
                                    int nkv, int hd, int page) {
   pdl_trigger();
-  pdl_wait();
   const int t = blockIdx.x;
   const int half = hd >> 1;
   const int nh = nq + 2 * nkv;
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  const bool active = j < nh * half;
+  const int hh = j / half, i = j % half;
   const int ps = pos[t];
-  float* row = qkv + (size_t)t * nh * hd;
-  const float* c = cs + (size_t)ps * half * 2;
   const int rc = hd / 8;
-  int pg = -1, r = ps % page;
+  const int r = ps % page;
   const int sl = slot ? slot[t] : -1;
-  if (kv && sl >= 0) pg = bt[(size_t)sl * max_pages + ps / page];
-  for (int j = threadIdx.x; j < nh * half; j += blockDim.x) {
-    const int hh = j / half, i = j % half;
-    float x1 = row[hh * hd + i], x2 = row[hh * hd + i + half];
-    row[hh * hd + i] = 0.f;
-    row[hh * hd + i + half] = 0.f;
+  int pg = -1;
+  if (kv && sl >= 0 && hh >= nq && active) pg = bt[(size_t)sl * max_pages + ps / page];
+  float b1 = 0.f, b2 = 0.f, co = 1.f, si = 0.f;
+  if (active) {
     if (bias) {
-      x1 += __bfloat162float(bias[hh * hd + i]);
-      x2 += __bfloat162float(bias[hh * hd + i + half]);
+      b1 = __bfloat162float(bias[hh * hd + i]);
+      b2 = __bfloat162float(bias[hh * hd + i + half]);
     }
-    float y1 = x1, y2 = x2;
     if (hh < nq + nkv) {
-      const float co = c[2 * i], si = c[2 * i + 1];
-      y1 = x1 * co - x2 * si;
-      y2 = x2 * co + x1 * si;
+      const float2 c = *reinterpret_cast<const float2*>(cs + ((size_t)ps * half + i) * 2);
+      co = c.x, si = c.y;
     }
-    const __nv_bfloat16 b1 = __float2bfloat16_rn(y1), b2 = __float2bfloat16_rn(y2);
-    if (hh < nq) {
-      q_out[((size_t)t * nq + hh) * hd + i] = b1;
-      q_out[((size_t)t * nq + hh) * hd + i + half] = b2;
-    } else {
-      const int isv = hh >= nq + nkv;
-      const int kvh = isv ? hh - nq - nkv : hh - nq;
-      if (pg >= 0) {
-        __nv_bfloat16* base = kv + (((size_t)pg * nkv + kvh) * 2 + isv) * (size_t)page * hd + (size_t)r * hd;
-        const int e1 = i, e2 = i + half;
-        base[(((e1 >> 3) ^ kv_swz(r, rc)) << 3) + (e1 & 7)] = b1;
-        base[(((e2 >> 3) ^ kv_swz(r, rc)) << 3) + (e2 & 7)] = b2;
-      }
-      __nv_bfloat16* cont = isv ? v_out : k_out;
-      if (cont) {
-        cont[((size_t)t * nkv + kvh) * hd + i] = b1;
-        cont[((size_t)t * nkv + kvh) * hd + i + half] = b2;
-      }
-    }
+  }
+  pdl_wait();
+  if (!active) return;
+  float* row = qkv + (size_t)t * nh * hd;
+  const float x1 = row[hh * hd + i] + b1, x2 = row[hh * hd + i + half] + b2;
+  row[hh * hd + i] = 0.f;
+  row[hh * hd + i + half] = 0.f;
+  const float y1 = x1 * co - x2 * si, y2 = x2 * co + x1 * si;  // v heads: co = 1, si = 0
+  const __nv_bfloat16 o1 = __float2bfloat16_rn(y1), o2 = __float2bfloat16_rn(y2);
+  if (hh < nq) {
+    q_out[((size_t)t * nq + hh) * hd + i] = o1;
+    q_out[((size_t)t * nq + hh) * hd + i + half] = o2;
+    return;
+  }
+  const int isv = hh >= nq + nkv;
+  const int kvh = isv ? hh - nq - nkv : hh - nq;
+  if (pg >= 0) {
+    __nv_bfloat16* base = kv + (((size_t)pg * nkv + kvh) * 2 + isv) * (size_t)page * hd + (size_t)r * hd;
+    const int e1 = i, e2 = i + half;
+    base[(((e1 >> 3) ^ kv_swz(r, rc)) << 3) + (e1 & 7)] = o1;
+    base[(((e2 >> 3) ^ kv_swz(r, rc)) << 3) + (e2 & 7)] = o2;
+  }
+  __nv_bfloat16* cont = isv ? v_out : k_out;
+  if (cont) {
+    cont[((size_t)t * nkv + kvh) * hd + i] = o1;
+    cont[((size_t)t * nkv + kvh) * hd + i + half] = o2;
   }
 }
 
@@ -125,7 +147,8 @@ cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, 
                         const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
                         void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  return launch_pdl(rope_append_kernel, dim3(T), dim3(256), 0, stream, const_cast<float*>(qkv),
+  const int pairs = (nq + 2 * nkv) * (hd / 2);
+  return launch_pdl(rope_append_kernel, dim3(T, (pairs + 127) / 128), dim3(128), 0, stream, const_cast<float*>(qkv),
                     reinterpret_cast<const __nv_bfloat16*>(bias), pos, slot, block_table, max_pages, cos_sin,
                     reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(kv),
                     reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), nq, nkv, hd,
@@ -133,26 +156,35 @@ cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, 
 }
 
 // ------------------------------------------------------------------ embedding gather
+// The table row is gathered before griddepcontrol.wait (the token ids come
+// from the host metadata or the previous iteration's sampler, both complete
+// before a decode/prefill launch sequence starts); h is written after it.
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tokens,
                              const int32_t* __restrict__ slots, const int32_t* __restrict__ last_tok,
                              float* __restrict__ h, int d) {
   pdl_trigger();
-  pdl_wait();
   const int t = blockIdx.x;
   const int sl = slots ? slots[t] : 0;
   const int tok = slots ? (sl >= 0 ? last_tok[sl] : 0) : tokens[t];  // slot -1: padding row
   const __nv_bfloat16* e = E + (size_t)tok * d;
-  float* o = h + (size_t)t * d;
-  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(e + i);
-    *reinterpret_cast<float2*>(o + i) = make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
-  }
+  const int i = threadIdx.x * 8;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (i < d) v = *reinterpret_cast<const uint4*>(e + i);
+  pdl_wait();
+  if (i >= d) return;
+  float* o = h + (size_t)t * d + i;
+  *reinterpret_cast<float4*>(o) = make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                                              __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+  *reinterpret_cast<float4*>(o + 4) = make_float4(__uint_as_float(v.z << 16), __uint_as_float(v.z & 0xffff0000u),
+                                                  __uint_as_float(v.w << 16), __uint_as_float(v.w & 0xffff0000u));
 }
 
 cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, const int32_t* last_tok, float* h,
                   int T, int d, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  return launch_pdl(embed_kernel, dim3(T), dim3(128), 0, stream, reinterpret_cast<const __nv_bfloat16*>(E), tokens,
+  if (d % 8 || d / 8 > 1024) return cudaErrorInvalidValue;
+  const int threads = (d / 8 + 31) / 32 * 32;
+  return launch_pdl(embed_kernel, dim3(T), dim3(threads), 0, stream, reinterpret_cast<const __nv_bfloat16*>(E), tokens,
                     slots, last_tok, h, d);
 }
 
@@ -171,7 +203,7 @@ __global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restric
     const float2 uv = *reinterpret_cast<const float2*>(u);
     *reinterpret_cast<float2*>(g) = make_float2(0.f, 0.f);  // zeroed for a split-K successor
     *reinterpret_cast<float2*>(u) = make_float2(0.f, 0.f);
-    const float s0 = gv.x / (1.f + __expf(-gv.x)), s1 = gv.y / (1.f + __expf(-gv.y));
+    const float s0 = gv.x / (1.f + expf(-gv.x)), s1 = gv.y / (1.f + expf(-gv.y));
     *reinterpret_cast<uint32_t*>(m + (size_t)t * f + i) = pack_bf16x2(s0 * uv.x, s1 * uv.y);
   }
 }

@@ -25,45 +25,71 @@ constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;
 constexpr int GEMM_SMEM_BUDGET = 200 * 1024;
+constexpr int GEMM_GROUP = 16;  // weight tiles (pairs) per rasterisation group
 
-// CG = 1: one CTA per 128-row weight tile (decode-sized token tiles).
-// CG = 2: a CTA pair (cluster of 2) computes a 256-row tile with
-// tcgen05.mma.cta_group::2: each CTA stages its 128 weight rows and half of
-// the token tile, the leader issues the MMAs, and the accumulator rows land in
-// each CTA's own TMEM.  Per SM this halves the token-tile shared-memory
-// traffic, which bounds the 1-CTA kernel at large token tiles.
+// CG = 1: one CTA per 128-row weight tile.  CG = 2: a CTA pair (cluster of
+// 2) computes a 256-row tile with tcgen05.mma.cta_group::2: each CTA stages
+// its 128 weight rows and half of the token tile, the leader issues the MMAs,
+// and the accumulator rows land in each CTA's own TMEM.  Per SM this halves
+// the token-tile shared-memory and L2 traffic of the 1-CTA kernel.
+//
+// Persistent: a CTA (pair) walks the work units u = blockIdx/CG, +grid/CG, ...
+// (unit = weight tile x token tile x K split, grouped rasterisation).  The
+// shared-memory ring runs continuously across units, and with nbuf = 2 the
+// TMEM accumulator is double-buffered so the epilogue of unit i overlaps the
+// MMAs of unit i+1 (tmem_full / tmem_empty barrier pair per buffer).
 template <int CG>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
-                        int chunks_per_split, int mode, int tmem_cols, int n_acc, int acc_stride) {
+                        int chunks_per_split, int mode, int tmem_cols, int n_acc, int acc_stride, int num_mp,
+                        int num_n, int units, int nbuf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int bl = BN / CG;                 // token rows staged by this CTA
+  const int bl = BN / CG;  // token rows staged by this CTA
   const int b_bytes = bl * GEMM_BK * 2;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)stages * GEMM_A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)stages * b_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* tmem_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + stages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [64][17] SwiGLU exchange (mode 3)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
-  const int m0 = blockIdx.x * GEMM_BM;
-  const int n0 = blockIdx.y * BN;
-  const int kc0 = blockIdx.z * chunks_per_split;
-  const int kc1 = min(kc0 + chunks_per_split, k_chunks_total);
-  const int nk = kc1 - kc0;
+  const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
+  const uint32_t buf_stride = nbuf == 2 ? (uint32_t)tmem_cols / 2 : 0u;
+
+  // unit -> (m0, n0, first k chunk, k chunks).  Grouped rasterisation:
+  // consecutive units walk GEMM_GROUP weight tiles (pairs) of one token tile,
+  // then the same weight tiles for the next token tile, so concurrently
+  // running units share weight tiles through L2.
+  auto coords = [&](int u, int& m0, int& n0, int& kc0, int& nk) {
+    const int per_split = num_mp * num_n;
+    const int sp = u / per_split, r = u - sp * per_split;
+    const int per_group = GEMM_GROUP * num_n;
+    const int first = (r / per_group) * GEMM_GROUP;
+    const int gsize = min(num_mp - first, GEMM_GROUP);
+    const int mt = first + (r % per_group) % gsize;
+    const int nt = (r % per_group) / gsize;
+    m0 = (mt * CG + (int)rank) * GEMM_BM;
+    n0 = nt * BN;
+    kc0 = sp * chunks_per_split;
+    nk = min(kc0 + chunks_per_split, k_chunks_total) - kc0;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4 * CG);  // one arrival per epilogue warp of the pair
+    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -86,124 +112,161 @@ __global__ void __launch_bounds__(256, 1)
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
     const uint32_t tx = (uint32_t)CG * (GEMM_A_BYTES + b_bytes);
-    auto load_a = [&](int s, int i) {
-      if (CG == 2)
-        tma_load_2d_2sm(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
-      else
-        tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
-    };
-    auto load_b = [&](int s, int i) {
-      if (CG == 2)
-        tma_load_2d_2sm(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0 + (int)rank * bl, &full[s]);
-      else
-        tma_load_2d(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[s]);
-    };
-    // The weight tiles do not depend on the previous kernel: fill the ring
-    // with them before waiting for it (overlaps the weight stream with the
-    // predecessor's tail), then load the activation tiles.
-    const int pre = nk < stages ? nk : stages;
-    for (int i = 0; i < pre; ++i) {
-      if (leader) mbar_expect_tx(&full[i], tx);
-      load_a(i, i);
-    }
-    pdl_wait();
-    for (int i = 0; i < pre; ++i) load_b(i, i);
-    for (int i = pre; i < nk; ++i) {
-      const int s = i % stages;
-      mbar_wait(&empty[s], ((i / stages) - 1) & 1);
-      if (leader) mbar_expect_tx(&full[s], tx);
-      load_a(s, i);
-      load_b(s, i);
+    int it = 0;  // position in the ring, continuous across units
+    for (int u = pair; u < units; u += npairs) {
+      int m0, n0, kc0, nk;
+      coords(u, m0, n0, kc0, nk);
+      auto load_a = [&](int s, int i) {
+        if (CG == 2)
+          tma_load_2d_2sm(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
+        else
+          tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
+      };
+      auto load_b = [&](int s, int i) {
+        if (CG == 2)
+          tma_load_2d_2sm(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0 + (int)rank * bl, &full[s]);
+        else
+          tma_load_2d(sB + (size_t)s * b_bytes, &tmX, (kc0 + i) * GEMM_BK, n0, &full[s]);
+      };
+      int i0 = 0;
+      if (u == pair) {
+        // The weight tiles do not depend on the previous kernel: fill the
+        // ring with them before waiting for it (overlaps the weight stream
+        // with the predecessor's tail), then load the activation tiles.
+        const int pre = nk < stages ? nk : stages;
+        for (int i = 0; i < pre; ++i) {
+          if (leader) mbar_expect_tx(&full[i], tx);
+          load_a(i, i);
+        }
+        pdl_wait();
+        for (int i = 0; i < pre; ++i) load_b(i, i);
+        i0 = pre;
+        it = pre;
+      }
+      for (int i = i0; i < nk; ++i, ++it) {
+        const int s = it % stages;
+        if (it >= stages) mbar_wait(&empty[s], ((it / stages) - 1) & 1);
+        if (leader) mbar_expect_tx(&full[s], tx);
+        load_a(s, i);
+        load_b(s, i);
+      }
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (single thread of the leader CTA)
     const uint32_t idesc = umma_idesc_bf16(GEMM_BM * CG, BN);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % stages;
-      mbar_wait(&full[s], (i / stages) & 1);
-      tc_fence_after();
-      const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * GEMM_A_BYTES));
-      const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_bytes));
-      // k-chunk i accumulates into TMEM accumulator i % n_acc: the tensor-core
-      // fp32 accumulation truncates, so short chains + an IEEE fp32 sum of the
-      // accumulators in the epilogue keep the error at fp32-GEMM level.
-      const uint32_t d = tmem + (uint32_t)((i % n_acc) * acc_stride);
+    int it = 0, tc = 0;
+    for (int u = pair; u < units; u += npairs, ++tc) {
+      int m0, n0, kc0, nk;
+      coords(u, m0, n0, kc0, nk);
+      const int buf = nbuf == 2 ? (tc & 1) : 0, use = nbuf == 2 ? (tc >> 1) : tc;
+      if (use > 0) {  // the epilogue of this buffer's previous unit has drained it
+        mbar_wait(&tmem_empty[buf], (use - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t base = tmem + (uint32_t)buf * buf_stride;
+      for (int i = 0; i < nk; ++i, ++it) {
+        const int s = it % stages;
+        mbar_wait(&full[s], (it / stages) & 1);
+        tc_fence_after();
+        const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * GEMM_A_BYTES));
+        const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_bytes));
+        // k-chunk i accumulates into TMEM accumulator i % n_acc: the tensor-core
+        // fp32 accumulation truncates, so short chains + an IEEE fp32 sum of the
+        // accumulators in the epilogue keep the error at fp32-GEMM level.
+        const uint32_t d = base + (uint32_t)((i % n_acc) * acc_stride);
 #pragma unroll
-      for (int k = 0; k < GEMM_BK / 16; ++k) {  // K = 16 per MMA: advance 32 B inside the swizzle atom
+        for (int k = 0; k < GEMM_BK / 16; ++k) {  // K = 16 per MMA: advance 32 B inside the swizzle atom
+          if (CG == 2)
+            umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+          else
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+        }
         if (CG == 2)
-          umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+          umma_commit_2sm(&empty[s]);
         else
-          umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
       }
       if (CG == 2)
-        umma_commit_2sm(&empty[s]);
+        umma_commit_2sm(&tmem_full[buf]);
       else
-        umma_commit(&empty[s]);
+        umma_commit(&tmem_full[buf]);
     }
-    if (CG == 2)
-      umma_commit_2sm(tmem_full);
-    else
-      umma_commit(tmem_full);
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global (lane = output feature)
     const int e = warp - 4;
     pdl_wait();  // C may still be read by the predecessor (write-after-read)
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int n = m0 + 32 * e + lane;
-    const int used = nk < n_acc ? nk : n_acc;
-    for (int c = 0; c < BN; c += 16) {
-      float acc[16];
-      {
-        uint32_t r[16];
-        tmem_ld16(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)c, r);
-        tmem_wait_ld();
+    int tc = 0;
+    for (int u = pair; u < units; u += npairs, ++tc) {
+      int m0, n0, kc0, nk;
+      coords(u, m0, n0, kc0, nk);
+      const int buf = nbuf == 2 ? (tc & 1) : 0, use = nbuf == 2 ? (tc >> 1) : tc;
+      mbar_wait(&tmem_full[buf], use & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + (uint32_t)buf * buf_stride + ((uint32_t)(32 * e) << 16);
+      const int n = m0 + 32 * e + lane;
+      const int used = nk < n_acc ? nk : n_acc;
+      for (int c = 0; c < BN; c += 16) {
+        float acc[16];
+        {
+          uint32_t r[16];
+          tmem_ld16(base + (uint32_t)c, r);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(r[j]);
-      }
-      for (int a = 1; a < used; ++a) {
-        uint32_t r[16];
-        tmem_ld16(tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(a * acc_stride + c), r);
-        tmem_wait_ld();
+          for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(r[j]);
+        }
+        for (int a = 1; a < used; ++a) {
+          uint32_t r[16];
+          tmem_ld16(base + (uint32_t)(a * acc_stride + c), r);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[j]);
-      }
-      if (mode == 3) {
-        // fused SwiGLU: this tile's rows 0..63 are gate rows and 64..127 the up
-        // rows of the same 64 features; warps 2-3 hand their up values to warps
-        // 0-1 through shared memory, which write m = bf16(SiLU(g) * u)
-        if (e >= 2)
+          for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[j]);
+        }
+        if (mode == 3) {
+          // fused SwiGLU: this tile's rows 0..63 are gate rows and 64..127 the up
+          // rows of the same 64 features; warps 2-3 hand their up values to warps
+          // 0-1 through shared memory, which write m = bf16(SiLU(g) * u)
+          if (e >= 2)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) xch[((e - 2) * 32 + lane) * 17 + j] = acc[j];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (e < 2) {
-          const int feat = (m0 >> 1) + 32 * e + lane;
-          __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(C);
+            for (int j = 0; j < 16; ++j) xch[((e - 2) * 32 + lane) * 17 + j] = acc[j];
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (e < 2) {
+            const int feat = (m0 >> 1) + 32 * e + lane;
+            __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(C);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int t = n0 + c + j;
-            if (t < T) {
-              const float g = acc[j], u = xch[(32 * e + lane) * 17 + j];
-              M[(size_t)t * ldc + feat] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+            for (int j = 0; j < 16; ++j) {
+              const int t = n0 + c + j;
+              if (t < T) {
+                const float g = acc[j], uu = xch[(32 * e + lane) * 17 + j];
+                M[(size_t)t * ldc + feat] = __float2bfloat16_rn(g / (1.f + expf(-g)) * uu);
+              }
             }
           }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          continue;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        continue;
-      }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = n0 + c + j;
-        if (t < T) {
-          float* p = C + (size_t)t * ldc + n;
-          const float v = acc[j];
-          if (mode == 0)
-            *p = v;
-          else if (mode == 1)
-            atomicAdd(p, v);
-          else
-            *p += v;
+        for (int j = 0; j < 16; ++j) {
+          const int t = n0 + c + j;
+          if (t < T) {
+            float* p = C + (size_t)t * ldc + n;
+            const float v = acc[j];
+            if (mode == 0)
+              *p = v;
+            else if (mode == 1)
+              atomicAdd(p, v);
+            else
+              *p += v;
+          }
         }
+      }
+      // hand the accumulator buffer back to the MMA issuer (leader CTA)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2)
+          mbar_arrive_cluster(&tmem_empty[buf], 0);
+        else
+          mbar_arrive(&tmem_empty[buf]);
       }
     }
   }
@@ -282,6 +345,19 @@ static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t
   return true;
 }
 
+static int sm_count() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
+  }
+  return n[dev];
+}
+
 int gemm_auto_splits(int N, int K, int T) {
   const int bn = T >= 256 ? 256 : ((T + 15) / 16) * 16;
   const int tiles = (N / GEMM_BM) * ((T + bn - 1) / bn);
@@ -309,32 +385,44 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (!cached_tmap(&tw, W, N, K, GEMM_BM)) return cudaErrorInvalidValue;
   if (!cached_tmap(&tx, X, T, K, BN / CG)) return cudaErrorInvalidValue;
   const int stage_bytes = GEMM_A_BYTES + (BN / CG) * GEMM_BK * 2;
-  // decode-sized tiles (BN <= 64) use half the shared memory and TMEM so two
-  // CTAs fit on an SM: the next GEMM (PDL) streams its weights while the
-  // current one drains
-  const bool small = BN <= 64;
+  // decode-sized tiles (BN <= 128) use half the shared memory and TMEM so two
+  // CTAs fit on an SM: the next tile (or the next GEMM, via PDL) streams its
+  // weights while the current one drains
+  const bool small = BN <= 128;
   int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
   if (stages > 12) stages = 12;
   if (stages > kc) stages = kc < 2 ? 2 : kc;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16 + 64 * 17 * 4;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + 64 * 17 * 4;
+  // persistent grid: one CTA (pair) per resident slot, at most one per unit
+  const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
+  const int units = num_mp * num_n * splits;
+  const int slots = sm_count() * (small ? 2 : 1) / CG;
+  const int pairs = units < slots ? units : slots;
+  // double-buffer TMEM when a CTA runs several compute-bound units; decode-
+  // sized units (BN <= 64) keep all accumulators for precision (their
+  // epilogue is short and the co-resident CTA keeps HBM busy meanwhile)
+  const int nbuf = (units > pairs && BN >= 128) ? 2 : 1;
   // accumulator interleave: as many TMEM accumulators as fit (<= 8), each 32-column aligned
+  const int budget = small ? 256 : 512;
   const int acc_stride = (BN + 31) / 32 * 32;
-  int n_acc = (small ? 256 : 512) / acc_stride;
+  int n_acc = budget / (nbuf * acc_stride);
   if (n_acc > 8) n_acc = 8;
   if (n_acc > per) n_acc = per;
   if (n_acc < 1) n_acc = 1;
   int tmem_cols = 32;
-  while (tmem_cols < n_acc * acc_stride) tmem_cols <<= 1;
+  while (tmem_cols < nbuf * n_acc * acc_stride) tmem_cols <<= 1;
+  if (nbuf == 2 && tmem_cols / 2 < n_acc * acc_stride) tmem_cols <<= 1;
+  if (tmem_cols > 512) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_bf16_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(gemm_bf16_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  dim3 grid(N / GEMM_BM, (T + BN - 1) / BN, splits);
+  const dim3 grid(pairs * CG);
   if (CG == 1)
     return launch_pdl(gemm_bf16_tc_kernel<1>, grid, dim3(256), smem, stream, tw, tx, C, T, ldc, BN, stages, kc, per,
-                      mode, tmem_cols, n_acc, acc_stride);
+                      mode, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(256);
@@ -348,7 +436,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, gemm_bf16_tc_kernel<2>, tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols,
-                            n_acc, acc_stride);
+                            n_acc, acc_stride, num_mp, num_n, units, nbuf);
 }
 
 }  // namespace sgs

@@ -18,6 +18,7 @@ int gemm_auto_splits(int N, int K, int T);
 struct AttnItem {
   int32_t row, kvh, p0, p1, part;  // part < 0: the item covers the whole row -> final output
   int32_t comb;                     // split items: index of their AttnComb
+  int32_t slot, ctx;                // block-table row and context length of the sample
 };
 struct AttnComb {
   int32_t row, kvh, part0, nparts;
@@ -30,16 +31,21 @@ struct AttnPlan {
 // Split-K plan over pages: rows with more than `chunk` pages are split (at
 // most 64 parts per row and kv head).  The item count is bounded by
 // 2*148 + 2*b*nkv (+ the split_pages override).
-void attn_plan(const int32_t* ctx, int b, int nkv, int page, int split_pages, AttnPlan* plan);
+// slot[row] is the block-table row of each sample (NULL: the row index).
+void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page, int split_pages, AttnPlan* plan);
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
 // items/combs are device arrays (already copied); part buffers in workspace.
-// block_table rows are indexed by row_slot[row] (NULL: by row); ctx is per row.
+// Each item carries its sample's block-table row (slot) and context length.
 // Split items merge in-kernel: the last part of a (row, kv head) to finish
 // combines (arrive = zero-initialised int[n_combs] counters, self re-arming).
 // counts (device, optional): {n_items, n_combs} read by the kernels, in which
 // case n_items / n_combs are only the launch capacities (CUDA-graph replay).
-cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_table, const int32_t* ctx,
-                        const int32_t* row_slot, const int32_t* counts, const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
+// PDL: items, counts, the block table and every KV page older than the one
+// holding token ctx-1 are read before griddepcontrol.wait (they are written
+// before the launching CUDA graph / stream segment starts, never by the
+// predecessor kernels); q and the newest page are read after it.
+cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_table, const int32_t* counts,
+                        const AttnItem* items, int n_items, const AttnComb* combs, int n_combs, int nq, int nkv,
                         int hd, int page, int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
                         int* arrive, cudaStream_t stream);
 

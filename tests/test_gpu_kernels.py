@@ -29,6 +29,10 @@ def _bf(shape, seed, scale=1.0):
     (3584, 18944, 256, 2, 1),     # 7B down at b = 256 (+= residual)
     (1024, 512, 1000, 0, 1),      # prefill-shaped: several N tiles + ragged tail
     (9472, 3584, 200, 0, 1),      # 74 N tiles (half-wave of 148 SMs)
+    # persistent multi-unit paths (double-buffered TMEM accumulators):
+    (4096, 3584, 2048, 0, 1),     # CTA pairs, 128 units over 74 pairs
+    (1152, 512, 8192, 2, 1),      # single CTAs (N not a multiple of 256), 288 units
+    (40960, 1024, 64, 0, 1),      # decode-sized tiles, 2 CTAs per SM, 320 units
 ])
 def test_gemm_vs_fp64(sgs, N, K, T, mode, splits):
     W = _bf((N, K), 1, 0.02).cuda()
@@ -228,7 +232,8 @@ def _interleave_gate_up(Wg, Wu):
     return torch.stack([Wg.view(f // 64, 64, K), Wu.view(f // 64, 64, K)], 1).reshape(2 * f, K)
 
 
-@pytest.mark.parametrize("f,K,T", [(512, 128, 5), (18944, 3584, 1), (18944, 3584, 96), (13824, 5120, 300)])
+@pytest.mark.parametrize("f,K,T", [(512, 128, 5), (18944, 3584, 1), (18944, 3584, 96), (13824, 5120, 300),
+                                   (18944, 3584, 1000)])
 def test_gemm_fused_swiglu_vs_fp64(sgs, f, K, T):
     Wg, Wu = _bf((f, K), 3, 0.02), _bf((f, K), 4, 0.02)
     X = _bf((T, K), 5, 1.0)
