@@ -296,25 +296,50 @@ __device__ __forceinline__ void combine_merge(const AttnComb& c, int nq, int nkv
     if (lane == 0) inv_l[r] = 1.f / L;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < g * hd; idx += blockDim.x) {
-    const int r = idx / hd, e = idx % hd;
-    const float* po = part_o + ((size_t)c.part0 * g + r) * hd + e;
-    const size_t stride = (size_t)g * hd;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int j = 0;
-    for (; j + 4 <= c.nparts; j += 4) {
-      s0 += w[r][j] * __ldcg(po + j * stride);
-      s1 += w[r][j + 1] * __ldcg(po + (j + 1) * stride);
-      s2 += w[r][j + 2] * __ldcg(po + (j + 2) * stride);
-      s3 += w[r][j + 3] * __ldcg(po + (j + 3) * stride);
+  // Every thread owns float4 columns v and v + blockDim.x of the [g][hd] block
+  // and keeps 2 x 8 partial loads in flight per batch: the merge costs about
+  // ceil(nparts / 8) L2 round trips instead of one per part and element.
+  const int nvec = g * hd / 4;
+  const size_t stride = (size_t)nvec;  // float4s per part
+  const float4* base = reinterpret_cast<const float4*>(part_o + (size_t)c.part0 * g * hd);
+  for (int v0 = threadIdx.x; v0 < nvec; v0 += 2 * blockDim.x) {
+    const int v1 = v0 + blockDim.x;
+    const bool has1 = v1 < nvec;
+    const int r0 = (4 * v0) / hd, r1 = has1 ? (4 * v1) / hd : r0;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    for (int j = 0; j < c.nparts; j += 8) {
+      float4 x0[8], x1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool ok = j + k < c.nparts;
+        x0[k] = ok ? __ldcg(base + (size_t)(j + k) * stride + v0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x1[k] = ok && has1 ? __ldcg(base + (size_t)(j + k) * stride + v1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (j + k < c.nparts) {
+          const float w0 = w[r0][j + k], w1 = w[r1][j + k];
+          a0.x += w0 * x0[k].x, a0.y += w0 * x0[k].y, a0.z += w0 * x0[k].z, a0.w += w0 * x0[k].w;
+          a1.x += w1 * x1[k].x, a1.y += w1 * x1[k].y, a1.z += w1 * x1[k].z, a1.w += w1 * x1[k].w;
+        }
+      }
     }
-    for (; j < c.nparts; ++j) s0 += w[r][j] * __ldcg(po + j * stride);
-    const float v = ((s0 + s1) + (s2 + s3)) * inv_l[r];
-    const size_t oi = ((size_t)c.row * nq + (size_t)c.kvh * g + r) * hd + e;
-    if (out_fp32)
-      reinterpret_cast<float*>(out)[oi] = v;
-    else
-      reinterpret_cast<__nv_bfloat16*>(out)[oi] = __float2bfloat16_rn(v);
+    auto store = [&](int v, int r, float4 a) {
+      const int e = 4 * v - r * hd;
+      const float il = inv_l[r];
+      const size_t oi = ((size_t)c.row * nq + (size_t)c.kvh * g + r) * hd + e;
+      if (out_fp32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + oi) =
+            make_float4(a.x * il, a.y * il, a.z * il, a.w * il);
+      } else {
+        uint2 o;
+        o.x = pack_bf16x2(a.x * il, a.y * il);
+        o.y = pack_bf16x2(a.z * il, a.w * il);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + oi) = o;
+      }
+    };
+    store(v0, r0, a0);
+    if (has1) store(v1, r1, a1);
   }
 }
 

@@ -319,12 +319,24 @@ __device__ float radix_mass_select(const float* __restrict__ x, int V, float m, 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      float c = above;
-      int k = 255;
-      for (; k > 0; --k) {
-        if (c + hist[k] >= target) break;
-        c += hist[k];
+      // first non-empty bucket (descending p) at which the mass reaches the
+      // target; if fp32 re-summation at this level falls short of a target
+      // that the parent bucket reached, the last non-empty bucket is taken
+      float c = above, c_last = above;
+      int k = 255, k_last = -1;
+      bool found = false;
+      for (; k >= 0; --k) {
+        const float hk = hist[k];
+        if (hk > 0.f) {
+          k_last = k, c_last = c;
+          if (c + hk >= target) {
+            found = true;
+            break;
+          }
+        }
+        c += hk;
       }
+      if (!found) k = k_last >= 0 ? k_last : 0, c = c_last;
       above = c;
       prefix |= (uint32_t)k << shift;
       mask |= 255u << shift;
@@ -404,8 +416,10 @@ __global__ void __launch_bounds__(1024) top_p_kernel(const float* __restrict__ l
   if (ub == tb) j = min(j, k_eq - 1);
   j = max(j, 0);
   // j-th token (ascending id) with p == theta_u
-  __shared__ int chosen;
-  if (threadIdx.x == 0) chosen = -1;
+  // (fp32 histogram sums can put j one past the last tied token: then the
+  // last token with p == theta_u, the end of that mass interval, is taken)
+  __shared__ int chosen, last_eq;
+  if (threadIdx.x == 0) chosen = -1, last_eq = 0;
   __syncthreads();
   int base = 0;
   for (int i0 = 0; i0 < V && chosen < 0; i0 += blockDim.x) {
@@ -420,11 +434,12 @@ __global__ void __launch_bounds__(1024) top_p_kernel(const float* __restrict__ l
     int tot = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += cnt[w];
     if (eq && before + wpre == j) chosen = i;
+    if (eq) atomicMax(&last_eq, i);
     __syncthreads();
     base += tot;
   }
   if (threadIdx.x == 0) {
-    const int tok = chosen >= 0 ? chosen : 0;
+    const int tok = chosen >= 0 ? chosen : last_eq;
     if (ids) ids[r] = tok;
     if (slot) {
       last_tok[slot[r]] = tok;

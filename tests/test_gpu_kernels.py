@@ -269,7 +269,10 @@ def test_silu_mul_interleaved_vs_fp64(sgs):
 def test_sample_top_p_vs_oracle(sgs, V, temp, top_p):
     # same fp32 logits on both sides; the GPU takes its decisions in fp32, the
     # oracle in fp64, so draws may differ only where u sits within rounding of a
-    # cumulative-mass boundary (R18): >= 99% identical over the draws
+    # cumulative-mass boundary (R18): >= 98% identical over the draws,
+    # and every differing GPU draw is a token whose fp64 cumulative-mass
+    # interval lies within 1e-4 of u (the fp32 softmax / prefix-sum error over
+    # up to 152064 terms) -- i.e. a draw the exact arithmetic nearly makes
     rows = 64
     g = torch.Generator().manual_seed(V + int(100 * top_p))
     x = torch.randn(rows, V, generator=g) * 3
@@ -285,4 +288,22 @@ def test_sample_top_p_vs_oracle(sgs, V, temp, top_p):
         for r in range(rows):
             ref = oracle.sample_top_p(x[r].numpy(), temp, top_p, seed, int(sid[r]), int(steps[r]))
             agree += got[r] == ref
-    assert agree >= 0.99 * 3 * rows, agree
+            if got[r] != ref:
+                _check_near_boundary(x[r].numpy(), temp, top_p, seed, int(sid[r]), int(steps[r]), got[r])
+    assert agree >= 0.98 * 3 * rows, agree
+
+
+def _check_near_boundary(x, temp, top_p, seed, sid, step, tok, tol=1e-4):
+    z = x.astype(np.float64) / temp
+    p = np.exp(z - z.max())
+    p /= p.sum()
+    order = np.lexsort((np.arange(len(p)), -p))  # p desc, id asc
+    cum = np.cumsum(p[order])
+    n = int(np.searchsorted(cum, top_p)) + 1 if top_p < 1 else len(p)
+    n = min(n, len(p))
+    mass = cum[n - 1]
+    r = oracle.philox([sid & 0xFFFFFFFF, sid >> 32, step & 0xFFFFFFFF, step >> 32], [seed & 0xFFFFFFFF, seed >> 32])
+    u = (r[0] >> 8) / 16777216.0 * mass
+    q = int(np.flatnonzero(order == tok)[0])
+    lo = cum[q - 1] if q > 0 else 0.0
+    assert q < n + 1 and lo - tol <= u <= cum[q] + tol, (tok, q, n, lo, cum[q], u)
