@@ -21,14 +21,16 @@ namespace sgs {
 // (weights never change inside a launch sequence).
 template <int VPT>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                               __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ rows, int d, float eps) {
+                               __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ rows, int T, int d,
+                               float eps) {
   pdl_trigger();
   const int i0 = threadIdx.x * 4 * VPT;
   uint2 wb[VPT];
 #pragma unroll
   for (int k = 0; k < VPT; ++k) wb[k] = *reinterpret_cast<const uint2*>(w + i0 + 4 * k);
   pdl_wait();
-  const int t = blockIdx.x;
+  __shared__ double red[32];
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
   const int src = rows ? rows[t] : t;
   const float* xr = x + (size_t)src * d;
   // fp64 sum of squares and scaling (latency-bound kernel: the arithmetic is
@@ -40,7 +42,6 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
     v[k] = *reinterpret_cast<const float4*>(xr + i0 + 4 * k);
     ss += (double)v[k].x * v[k].x + (double)v[k].y * v[k].y + (double)v[k].z * v[k].z + (double)v[k].w * v[k].w;
   }
-  __shared__ double red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -62,6 +63,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
     o.y = pack_bf16x2(f(v[k].z, wb[k].y << 16), f(v[k].w, wb[k].y & 0xffff0000u));
     *reinterpret_cast<uint2*>(yr + i0 + 4 * k) = o;
   }
+  __syncthreads();  // red[] is reused by the next row
+  }
 }
 
 cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows, int T, int d, float eps,
@@ -71,88 +74,125 @@ cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows,
   auto Y = reinterpret_cast<__nv_bfloat16*>(y);
   // the sum of squares is a warp/block reduction whose order depends on the
   // thread count; every row uses the same configuration for a given d
+  const int grid = T < 1184 ? T : 1184;  // grid-stride over rows beyond 8 CTAs per SM
   if (d % 8 == 0 && d / 8 <= 1024 && d / 8 >= 32)
-    return launch_pdl(rmsnorm_kernel<2>, dim3(T), dim3(d / 8), 0, stream, x, W, Y, rows, d, eps);
+    return launch_pdl(rmsnorm_kernel<2>, dim3(grid), dim3(d / 8), 0, stream, x, W, Y, rows, T, d, eps);
   if (d % 4 == 0 && d / 4 <= 1024 && d / 4 >= 32)
-    return launch_pdl(rmsnorm_kernel<1>, dim3(T), dim3(d / 4), 0, stream, x, W, Y, rows, d, eps);
+    return launch_pdl(rmsnorm_kernel<1>, dim3(grid), dim3(d / 4), 0, stream, x, W, Y, rows, T, d, eps);
   return cudaErrorInvalidValue;
 }
 
 // ------------------------------------------------------------------ RoPE + KV append
-// Grid (row, 128-pair group): thread j of the group handles pair index
-// j in [0, (nq+2nkv) * hd/2): head = j / half, i = j % half.  q/k heads rotate
-// (x_i, x_{i+half}); v heads copy.  Everything but the qkv row (position,
-// slot, block-table entry, bias, cos/sin) is read before griddepcontrol.wait.
-// The fp32 qkv row is zeroed after it is read, so the next split-K QKV GEMM
-// (fp32 red.add) finds a zeroed accumulator without a memset.
-__global__ void rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
-                                   const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
-                                   const int32_t* __restrict__ bt, int max_pages, const float* __restrict__ cs,
-                                   __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv,
-                                   __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out, int nq,
-                                   int nkv, int hd, int page) {
+// Work unit = a "duo" of adjacent rotation pairs (i, i+1), i even, of one head:
+// duo j of a row -> head = 2j / half, i = 2j % half; q/k heads rotate
+// (x_i, x_{i+half}), v heads copy; all loads/stores are 2-wide.  Grid
+// (row block, duo group): small batches spread a row over up to 9 CTAs so
+// the store issue of a row is not serialised on one SM; large batches use
+// few fat CTAs that stride over rows (the CTA launch rate bounds thousands of
+// tiny CTAs).  Position, slot, block-table entry, bias and cos/sin are read
+// before griddepcontrol.wait; after it every qkv load of the unit is issued
+// before any store.  The fp32 qkv row is zeroed after it is read, so the next
+// split-K QKV GEMM (fp32 red.add) finds a zeroed accumulator without a memset.
+constexpr int ROPE_THREADS = 128, ROPE_U = 8;
+__global__ void __launch_bounds__(ROPE_THREADS)
+    rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
+                       const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+                       const int32_t* __restrict__ bt, int max_pages, const float* __restrict__ cs,
+                       __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv,
+                       __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out, int T, int nq, int nkv,
+                       int hd, int page, int per) {
   pdl_trigger();
-  const int t = blockIdx.x;
   const int half = hd >> 1;
   const int nh = nq + 2 * nkv;
-  const int j = blockIdx.y * blockDim.x + threadIdx.x;
-  const bool active = j < nh * half;
-  const int hh = j / half, i = j % half;
-  const int ps = pos[t];
+  const int nduo = nh * half / 2;
   const int rc = hd / 8;
-  const int r = ps % page;
-  const int sl = slot ? slot[t] : -1;
-  int pg = -1;
-  if (kv && sl >= 0 && hh >= nq && active) pg = bt[(size_t)sl * max_pages + ps / page];
-  float b1 = 0.f, b2 = 0.f, co = 1.f, si = 0.f;
-  if (active) {
-    if (bias) {
-      b1 = __bfloat162float(bias[hh * hd + i]);
-      b2 = __bfloat162float(bias[hh * hd + i + half]);
+  const int j0 = blockIdx.y * per, j1 = min(j0 + per, nduo);
+  bool waited = false;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    const int ps = pos[t];
+    const int r = ps % page;
+    const int sl = slot ? slot[t] : -1;
+    const int pg = (kv && sl >= 0) ? bt[(size_t)sl * max_pages + ps / page] : -1;
+    float2 b1[ROPE_U], b2[ROPE_U], x1[ROPE_U], x2[ROPE_U];
+    float4 c[ROPE_U];
+#pragma unroll
+    for (int u = 0; u < ROPE_U; ++u) {
+      const int j = j0 + threadIdx.x + ROPE_THREADS * u;
+      b1[u] = b2[u] = make_float2(0.f, 0.f);
+      c[u] = make_float4(1.f, 0.f, 1.f, 0.f);  // (cos, sin) of pairs i and i+1; identity for v heads
+      if (j < j1) {
+        const int hh = (2 * j) / half, i = 2 * j - hh * half;
+        if (bias) {
+          b1[u] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(bias + hh * hd + i));
+          b2[u] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(bias + hh * hd + i + half));
+        }
+        if (hh < nq + nkv) c[u] = *reinterpret_cast<const float4*>(cs + ((size_t)ps * half + i) * 2);
+      }
     }
-    if (hh < nq + nkv) {
-      const float2 c = *reinterpret_cast<const float2*>(cs + ((size_t)ps * half + i) * 2);
-      co = c.x, si = c.y;
+    if (!waited) pdl_wait(), waited = true;
+    float* row = qkv + (size_t)t * nh * hd;
+#pragma unroll
+    for (int u = 0; u < ROPE_U; ++u) {
+      const int j = j0 + threadIdx.x + ROPE_THREADS * u;
+      if (j < j1) {
+        const int hh = (2 * j) / half, i = 2 * j - hh * half;
+        x1[u] = *reinterpret_cast<const float2*>(row + hh * hd + i);
+        x2[u] = *reinterpret_cast<const float2*>(row + hh * hd + i + half);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ROPE_U; ++u) {
+      const int j = j0 + threadIdx.x + ROPE_THREADS * u;
+      if (j >= j1) continue;
+      const int hh = (2 * j) / half, i = 2 * j - hh * half;
+      *reinterpret_cast<float2*>(row + hh * hd + i) = make_float2(0.f, 0.f);
+      *reinterpret_cast<float2*>(row + hh * hd + i + half) = make_float2(0.f, 0.f);
+      const float a0 = x1[u].x + b1[u].x, a1 = x1[u].y + b1[u].y;  // x_i, x_{i+1}
+      const float e0 = x2[u].x + b2[u].x, e1 = x2[u].y + b2[u].y;  // x_{i+half}, x_{i+1+half}
+      const float y10 = a0 * c[u].x - e0 * c[u].y, y20 = e0 * c[u].x + a0 * c[u].y;
+      const float y11 = a1 * c[u].z - e1 * c[u].w, y21 = e1 * c[u].z + a1 * c[u].w;
+      const __nv_bfloat162 o1 = __floats2bfloat162_rn(y10, y11), o2 = __floats2bfloat162_rn(y20, y21);
+      if (hh < nq) {
+        *reinterpret_cast<__nv_bfloat162*>(q_out + ((size_t)t * nq + hh) * hd + i) = o1;
+        *reinterpret_cast<__nv_bfloat162*>(q_out + ((size_t)t * nq + hh) * hd + i + half) = o2;
+        continue;
+      }
+      const int isv = hh >= nq + nkv;
+      const int kvh = isv ? hh - nq - nkv : hh - nq;
+      if (pg >= 0) {
+        __nv_bfloat16* base = kv + (((size_t)pg * nkv + kvh) * 2 + isv) * (size_t)page * hd + (size_t)r * hd;
+        const int e1i = i, e2i = i + half;  // even: both elements stay in one 8-element chunk
+        *reinterpret_cast<__nv_bfloat162*>(base + ((((e1i >> 3) ^ kv_swz(r, rc)) << 3) + (e1i & 7))) = o1;
+        *reinterpret_cast<__nv_bfloat162*>(base + ((((e2i >> 3) ^ kv_swz(r, rc)) << 3) + (e2i & 7))) = o2;
+      }
+      __nv_bfloat16* cont = isv ? v_out : k_out;
+      if (cont) {
+        *reinterpret_cast<__nv_bfloat162*>(cont + ((size_t)t * nkv + kvh) * hd + i) = o1;
+        *reinterpret_cast<__nv_bfloat162*>(cont + ((size_t)t * nkv + kvh) * hd + i + half) = o2;
+      }
     }
   }
-  pdl_wait();
-  if (!active) return;
-  float* row = qkv + (size_t)t * nh * hd;
-  const float x1 = row[hh * hd + i] + b1, x2 = row[hh * hd + i + half] + b2;
-  row[hh * hd + i] = 0.f;
-  row[hh * hd + i + half] = 0.f;
-  const float y1 = x1 * co - x2 * si, y2 = x2 * co + x1 * si;  // v heads: co = 1, si = 0
-  const __nv_bfloat16 o1 = __float2bfloat16_rn(y1), o2 = __float2bfloat16_rn(y2);
-  if (hh < nq) {
-    q_out[((size_t)t * nq + hh) * hd + i] = o1;
-    q_out[((size_t)t * nq + hh) * hd + i + half] = o2;
-    return;
-  }
-  const int isv = hh >= nq + nkv;
-  const int kvh = isv ? hh - nq - nkv : hh - nq;
-  if (pg >= 0) {
-    __nv_bfloat16* base = kv + (((size_t)pg * nkv + kvh) * 2 + isv) * (size_t)page * hd + (size_t)r * hd;
-    const int e1 = i, e2 = i + half;
-    base[(((e1 >> 3) ^ kv_swz(r, rc)) << 3) + (e1 & 7)] = o1;
-    base[(((e2 >> 3) ^ kv_swz(r, rc)) << 3) + (e2 & 7)] = o2;
-  }
-  __nv_bfloat16* cont = isv ? v_out : k_out;
-  if (cont) {
-    cont[((size_t)t * nkv + kvh) * hd + i] = o1;
-    cont[((size_t)t * nkv + kvh) * hd + i + half] = o2;
-  }
+  if (!waited) pdl_wait();
 }
 
 cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
                         const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
                         void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  const int pairs = (nq + 2 * nkv) * (hd / 2);
-  return launch_pdl(rope_append_kernel, dim3(T, (pairs + 127) / 128), dim3(128), 0, stream, const_cast<float*>(qkv),
+  if (hd % 4) return cudaErrorInvalidValue;
+  const int nduo = (nq + 2 * nkv) * (hd / 2) / 2;
+  const int gmin = (nduo + ROPE_THREADS * ROPE_U - 1) / (ROPE_THREADS * ROPE_U);
+  const int gmax = (nduo + ROPE_THREADS - 1) / ROPE_THREADS;
+  int G = (4 * 148 + T - 1) / T;  // about 4 CTAs per SM
+  G = G < gmin ? gmin : (G > gmax ? gmax : G);
+  const int per = (nduo + G - 1) / G;
+  int rows = (1184 + G - 1) / G;  // beyond 8 CTAs per SM the CTAs stride over rows
+  rows = T < rows ? T : rows;
+  return launch_pdl(rope_append_kernel, dim3(rows, G), dim3(ROPE_THREADS), 0, stream, const_cast<float*>(qkv),
                     reinterpret_cast<const __nv_bfloat16*>(bias), pos, slot, block_table, max_pages, cos_sin,
                     reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(kv),
-                    reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), nq, nkv, hd,
-                    page);
+                    reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), T, nq, nkv, hd,
+                    page, per);
 }
 
 // ------------------------------------------------------------------ embedding gather
@@ -161,22 +201,25 @@ cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, 
 // before a decode/prefill launch sequence starts); h is written after it.
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tokens,
                              const int32_t* __restrict__ slots, const int32_t* __restrict__ last_tok,
-                             float* __restrict__ h, int d) {
+                             float* __restrict__ h, int T, int d) {
   pdl_trigger();
-  const int t = blockIdx.x;
-  const int sl = slots ? slots[t] : 0;
-  const int tok = slots ? (sl >= 0 ? last_tok[sl] : 0) : tokens[t];  // slot -1: padding row
-  const __nv_bfloat16* e = E + (size_t)tok * d;
-  const int i = threadIdx.x * 8;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  if (i < d) v = *reinterpret_cast<const uint4*>(e + i);
-  pdl_wait();
-  if (i >= d) return;
-  float* o = h + (size_t)t * d + i;
-  *reinterpret_cast<float4*>(o) = make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
-                                              __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
-  *reinterpret_cast<float4*>(o + 4) = make_float4(__uint_as_float(v.z << 16), __uint_as_float(v.z & 0xffff0000u),
-                                                  __uint_as_float(v.w << 16), __uint_as_float(v.w & 0xffff0000u));
+  bool waited = false;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    const int sl = slots ? slots[t] : 0;
+    const int tok = slots ? (sl >= 0 ? last_tok[sl] : 0) : tokens[t];  // slot -1: padding row
+    const __nv_bfloat16* e = E + (size_t)tok * d;
+    const int i = threadIdx.x * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (i < d) v = *reinterpret_cast<const uint4*>(e + i);
+    if (!waited) pdl_wait(), waited = true;
+    if (i >= d) continue;
+    float* o = h + (size_t)t * d + i;
+    *reinterpret_cast<float4*>(o) = make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                                                __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+    *reinterpret_cast<float4*>(o + 4) = make_float4(__uint_as_float(v.z << 16), __uint_as_float(v.z & 0xffff0000u),
+                                                    __uint_as_float(v.w << 16), __uint_as_float(v.w & 0xffff0000u));
+  }
+  if (!waited) pdl_wait();
 }
 
 cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, const int32_t* last_tok, float* h,
@@ -184,8 +227,9 @@ cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, co
   if (T <= 0) return cudaSuccess;
   if (d % 8 || d / 8 > 1024) return cudaErrorInvalidValue;
   const int threads = (d / 8 + 31) / 32 * 32;
-  return launch_pdl(embed_kernel, dim3(T), dim3(threads), 0, stream, reinterpret_cast<const __nv_bfloat16*>(E), tokens,
-                    slots, last_tok, h, d);
+  const int grid = T < 1184 ? T : 1184;
+  return launch_pdl(embed_kernel, dim3(grid), dim3(threads), 0, stream, reinterpret_cast<const __nv_bfloat16*>(E),
+                    tokens, slots, last_tok, h, T, d);
 }
 
 // ------------------------------------------------------------------ SwiGLU

@@ -55,7 +55,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tmem_full = empty + stages;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-  float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [64][17] SwiGLU exchange (mode 3)
+  // [4 warps][32][17]: per-warp transpose (features x tokens -> tokens x
+  // feature quads) for the vectorised epilogue; rows 0..63 double as the
+  // SwiGLU exchange (mode 3)
+  float* xch = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -203,7 +206,6 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tmem_full[buf], use & 1);
       tc_fence_after();
       const uint32_t base = tmem + (uint32_t)buf * buf_stride + ((uint32_t)(32 * e) << 16);
-      const int n = m0 + 32 * e + lane;
       const int used = nk < n_acc ? nk : n_acc;
       for (int c = 0; c < BN; c += 16) {
         float acc[16];
@@ -244,20 +246,34 @@ __global__ void __launch_bounds__(256, 1)
           asm volatile("bar.sync 1, 128;" ::: "memory");
           continue;
         }
+        // transpose through shared memory so each thread owns 4 consecutive
+        // features of one token: 16-byte stores / red.global.add.v4.f32
+        // (a quarter of the scalar atomics of split-K)
+        float* xt = xch + (size_t)e * 32 * 17;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 16; ++j) xt[lane * 17 + j] = acc[j];
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int item = lane + 32 * it, j = item >> 3, qd = item & 7;
           const int t = n0 + c + j;
           if (t < T) {
-            float* p = C + (size_t)t * ldc + n;
-            const float v = acc[j];
-            if (mode == 0)
-              *p = v;
-            else if (mode == 1)
-              atomicAdd(p, v);
-            else
-              *p += v;
+            float4 v;
+            v.x = xt[(4 * qd + 0) * 17 + j], v.y = xt[(4 * qd + 1) * 17 + j];
+            v.z = xt[(4 * qd + 2) * 17 + j], v.w = xt[(4 * qd + 3) * 17 + j];
+            float* p = C + (size_t)t * ldc + m0 + 32 * e + 4 * qd;
+            if (mode == 0) {
+              *reinterpret_cast<float4*>(p) = v;
+            } else if (mode == 1) {
+              red_add_v4(p, v);
+            } else {
+              float4 o = *reinterpret_cast<float4*>(p);
+              o.x += v.x, o.y += v.y, o.z += v.z, o.w += v.w;
+              *reinterpret_cast<float4*>(p) = o;
+            }
           }
         }
+        __syncwarp();
       }
       // hand the accumulator buffer back to the MMA issuer (leader CTA)
       tc_fence_before();
@@ -392,7 +408,8 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
   if (stages > 12) stages = 12;
   if (stages > kc) stages = kc < 2 ? 2 : kc;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + 64 * 17 * 4;
+  if (ldc % 4 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return cudaErrorInvalidValue;  // float4 epilogue
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + 4 * 32 * 17 * 4;
   // persistent grid: one CTA (pair) per resident slot, at most one per unit
   const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
   const int units = num_mp * num_n * splits;

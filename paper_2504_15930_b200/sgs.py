@@ -9,7 +9,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsgs.so")
+# SGS_LIB_PATH: an alternative in-tree build of the same library (A/B timing in tools/ab.sh)
+LIB_PATH = os.environ.get("SGS_LIB_PATH") or os.path.join(_HERE, "libsgs.so")
 
 SGS_OK = 0
 STATUS = {0: "SGS_OK", -1: "SGS_E_INVAL", -2: "SGS_E_NOMEM", -3: "SGS_E_STATE", -4: "SGS_E_CAPACITY",
