@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
                         int chunks_per_split, int mode, int tmem_cols, int n_acc, int acc_stride, int num_mp,
-                        int num_n, int units, int nbuf) {
+                        int num_n, int units, int nbuf, int xbufs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int bl = BN / CG;  // token rows staged by this CTA
@@ -55,8 +55,9 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tmem_full = empty + stages;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-  // [4 warps][32][17]: per-warp transpose (features x tokens -> tokens x
-  // feature quads) for the vectorised epilogue; rows 0..63 double as the
+  // 2 x [4 warps][32][17]: per-warp transpose (features x tokens -> tokens x
+  // feature quads) for the vectorised epilogue; both halves serve as the
+  // double-buffered SwiGLU exchange (mode 3); rows 0..63 double as the
   // SwiGLU exchange (mode 3)
   float* xch = reinterpret_cast<float*>(tmem_slot + 4);
 
@@ -224,26 +225,26 @@ __global__ void __launch_bounds__(256, 1)
           for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[j]);
         }
         if (mode == 3) {
-          // fused SwiGLU: this tile's rows 0..63 are gate rows and 64..127 the up
-          // rows of the same 64 features; warps 2-3 hand their up values to warps
-          // 0-1 through shared memory, which write m = bf16(SiLU(g) * u)
-          if (e >= 2)
+          // fused SwiGLU: tile rows 0..63 are gate rows and 64..127 the up rows
+          // of the same 64 features (warps 0-1: g, warps 2-3: u).  All four
+          // warps publish their 16 tokens to shared memory (double-buffered
+          // by chunk parity when xbufs == 2: one barrier per chunk); warp w
+          // then writes m = bf16(SiLU(g) * u) for features 32 (w & 1) + lane
+          // and tokens 8 (w >> 1) + 0..7 (lane = feature: 64-byte stores).
+          __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(C);
+          float* xb = xch + (size_t)((c >> 4) & (xbufs - 1)) * (4 * 32 * 17);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) xch[((e - 2) * 32 + lane) * 17 + j] = acc[j];
+          for (int j = 0; j < 16; ++j) xb[(e * 32 + lane) * 17 + j] = acc[j];
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (e < 2) {
-            const int feat = (m0 >> 1) + 32 * e + lane;
-            __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(C);
+          const int fg = e & 1, th = e >> 1;
+          const int feat = (m0 >> 1) + 32 * fg + lane;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int t = n0 + c + j;
-              if (t < T) {
-                const float g = acc[j], uu = xch[(32 * e + lane) * 17 + j];
-                M[(size_t)t * ldc + feat] = __float2bfloat16_rn(g / (1.f + expf(-g)) * uu);
-              }
-            }
+          for (int k = 0; k < 8; ++k) {
+            const int j = 8 * th + k, t = n0 + c + j;
+            const float g = xb[(fg * 32 + lane) * 17 + j], uu = xb[((2 + fg) * 32 + lane) * 17 + j];
+            if (t < T) M[(size_t)t * ldc + feat] = __float2bfloat16_rn(g / (1.f + expf(-g)) * uu);
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (xbufs == 1) asm volatile("bar.sync 1, 128;" ::: "memory");  // single buffer: drain before reuse
           continue;
         }
         // transpose through shared memory so each thread owns 4 consecutive
@@ -409,7 +410,10 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (stages > 12) stages = 12;
   if (stages > kc) stages = kc < 2 ? 2 : kc;
   if (ldc % 4 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return cudaErrorInvalidValue;  // float4 epilogue
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + 4 * 32 * 17 * 4;
+  // epilogue exchange: double-buffered for compute-bound tiles (mode 3 then
+  // needs one barrier per 16-token chunk); decode tiles keep the smem for stages
+  const int xbufs = small ? 1 : 2;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + (size_t)xbufs * 4 * 32 * 17 * 4;
   // persistent grid: one CTA (pair) per resident slot, at most one per unit
   const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
   const int units = num_mp * num_n * splits;
@@ -439,7 +443,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   const dim3 grid(pairs * CG);
   if (CG == 1)
     return launch_pdl(gemm_bf16_tc_kernel<1>, grid, dim3(256), smem, stream, tw, tx, C, T, ldc, BN, stages, kc, per,
-                      mode, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf);
+                      mode, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(256);
@@ -453,7 +457,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, gemm_bf16_tc_kernel<2>, tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols,
-                            n_acc, acc_stride, num_mp, num_n, units, nbuf);
+                            n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs);
 }
 
 }  // namespace sgs

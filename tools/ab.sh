@@ -8,8 +8,9 @@ out=${1:-gpurun_out/ab}
 shift
 args=${@:---ctx 2048 --b 1 16 64 256 --decode-iters 8}
 mkdir -p $out
-for r in 1 2 3; do
-  for v in A B; do
+for r in 1 2 3 4; do
+  order="A B"; [ $((r % 2)) = 0 ] && order="B A"  # ABBA: cancels thermal / clock drift
+  for v in $order; do
     lib=$A; [ $v = B ] && lib=$B
     SGS_LIB_PATH=$lib python tools/tb_sweep.py $args --out $out/${v}$r.json > $out/${v}$r.log 2>&1
   done

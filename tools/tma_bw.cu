@@ -1,0 +1,141 @@
+// TMA load-bandwidth microbenchmark (design study for the GEMM pipeline):
+// every CTA streams `iters` 2-D tiles (box 64 bf16 x ROWS, 128-byte swizzle)
+// through an S-stage shared-memory ring; a consumer warp only waits on the
+// full barrier and releases the slot.  Modes: 0 = each CTA reads its own
+// rows of a buffer larger than L2 (HBM stream), 1 = all CTAs read the same
+// 2 MB region (L2-resident).  Prints GB/s per configuration.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tma_bw tools/tma_bw.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtensorMap tm, int stages, int iters,
+                                                 int box_rows, int mode, int rows_total, unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int box_bytes = box_rows * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * box_bytes);
+  uint64_t* empty = full + stages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int row_tiles = rows_total / box_rows;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < iters; ++i) {
+      const int s = i % stages;
+      if (i >= stages) {
+        const uint32_t par = ((i / stages) - 1) & 1;
+        asm volatile(
+            "{\n.reg .pred p;\nW1:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W1;\n}\n" ::"r"(
+                su32(&empty[s])),
+            "r"(par)
+            : "memory");
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(box_bytes)
+                   : "memory");
+      // mode 0: CTA-private row band, walk K then rows; mode 1: 2 MB shared window
+      int x, y;
+      if (mode == 0) {
+        const int kt = 64;  // 64 K-tiles of 64 columns per row band (K = 4096)
+        const int band = (blockIdx.x * 64 + i / kt) % row_tiles;
+        x = (i % kt) * 64, y = band * box_rows;
+      } else {
+        const int win = (2 << 20) / (box_rows * 128);  // tiles in 2 MB
+        const int t = (blockIdx.x * 7 + i) % win;
+        x = (t % 64) * 64, y = (t / 64) * box_rows;
+      }
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+              su32(smem + (size_t)s * box_bytes)),
+          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(su32(&full[s])), "r"(x), "r"(y)
+          : "memory");
+    }
+  } else if (threadIdx.x == 32) {
+    unsigned long long acc = 0;
+    for (int i = 0; i < iters; ++i) {
+      const int s = i % stages;
+      const uint32_t par = (i / stages) & 1;
+      asm volatile(
+          "{\n.reg .pred p;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W2;\n}\n" ::"r"(
+              su32(&full[s])),
+          "r"(par)
+          : "memory");
+      acc += smem[(size_t)s * box_bytes + (i & 127)];
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+    }
+    if (acc == 0xFFFFFFFFFFFFull) *sink = acc;
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+  void* fnp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q);
+  EncodeFn enc = reinterpret_cast<EncodeFn>(fnp);
+  const int K = 4096;
+  const int rows = 65536;  // 512 MB of bf16 >> L2
+  void* buf = nullptr;
+  cudaMalloc(&buf, (size_t)rows * K * 2);
+  cudaMemset(buf, 1, (size_t)rows * K * 2);
+  unsigned long long* sink;
+  cudaMalloc(&sink, 8);
+  cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int mode = 0; mode < 2; ++mode)
+    for (int box_rows : {128, 256})
+      for (int per_sm : {1, 2})
+        for (int stages : {2, 4, 6, 8, 12}) {
+          const int box_bytes = box_rows * 128;
+          const size_t smem = 1024 + (size_t)stages * box_bytes + 2 * stages * 8;
+          if (smem * per_sm > 227 * 1024) continue;
+          CUtensorMap tm;
+          cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+          cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+          cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+          cuuint32_t es[2] = {1, 1};
+          if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            printf("encode failed\n");
+            return 1;
+          }
+          const int grid = sms * per_sm;
+          const int iters = (int)((256LL << 20) * (mode == 0 ? 1 : 2) / ((long long)grid * box_bytes));
+          for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(a);
+            tma_stream<<<grid, 64, smem>>>(tm, stages, iters, box_rows, mode, rows, sink);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+          }
+          float ms = 0;
+          cudaEventElapsedTime(&ms, a, b);
+          const double bytes = (double)grid * iters * box_bytes;
+          printf("{\"mode\": \"%s\", \"box_rows\": %d, \"ctas_per_sm\": %d, \"stages\": %d, \"GBs\": %.1f, "
+                 "\"GBs_per_sm\": %.1f, \"inflight_KB_per_sm\": %d}\n",
+                 mode == 0 ? "hbm" : "l2", box_rows, per_sm, stages, bytes / ms / 1e6, bytes / ms / 1e6 / sms,
+                 stages * box_bytes * per_sm / 1024);
+          fflush(stdout);
+        }
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("status %s\n", cudaGetErrorString(e));
+  return 0;
+}
