@@ -13,6 +13,7 @@
 // rows of C (coalesced: lane = output feature).  Split-K over gridDim.z with
 // fp32 red.add when mode == 1.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -38,19 +39,26 @@ constexpr int GEMM_GROUP = 16;  // weight tiles (pairs) per rasterisation group
 // shared-memory ring runs continuously across units, and with nbuf = 2 the
 // TMEM accumulator is double-buffered so the epilogue of unit i overlaps the
 // MMAs of unit i+1 (tmem_full / tmem_empty barrier pair per buffer).
-template <int CG>
+// One instantiation per (CG, epilogue MODE, k-chunks per stage KCS): each
+// kernel carries only its own producer and epilogue code, which keeps it
+// under the ~40 KB instruction-cache knee (a 46 KB all-modes kernel measured
+// 14% slower on decode-sized GEMMs).
+template <int CG, int MODE, int KCS>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
-                        int chunks_per_split, int mode, int tmem_cols, int n_acc, int acc_stride, int num_mp,
-                        int num_n, int units, int nbuf, int xbufs) {
+                        int chunks_per_split, int tmem_cols, int n_acc, int acc_stride, int num_mp, int num_n,
+                        int units, int nbuf, int xbufs) {
+  constexpr int mode = MODE, kcs = KCS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int bl = BN / CG;  // token rows staged by this CTA
-  const int b_bytes = bl * GEMM_BK * 2;
+  const int b_bytes = bl * GEMM_BK * 2;  // one k-chunk of the token tile
+  // a stage holds kcs consecutive k-chunks of each operand (one 3-D TMA box)
+  const int a_stage = kcs * GEMM_A_BYTES, b_stage = kcs * b_bytes;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)stages * GEMM_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)stages * b_bytes);
+  uint8_t* sB = smem + (size_t)stages * a_stage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)stages * b_stage);
   uint64_t* empty = full + stages;
   uint64_t* tmem_full = empty + stages;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
@@ -87,7 +95,7 @@ __global__ void __launch_bounds__(256, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kcs > 1 ? 2 : 1);  // split producers: the weight and the activation thread each arrive
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -111,8 +119,12 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
 
   pdl_trigger();
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer (both CTAs; the leader's barrier counts both CTAs' bytes)
+  if (kcs == 1 && warp == 0 && lane == 0) {
+    // ---------------- TMA producer, decode-sized tiles: one thread, 2-D boxes
+    // (both CTAs; the leader's barrier counts both CTAs' bytes).  The weight
+    // tiles do not depend on the previous kernel: the ring is filled with
+    // them before griddepcontrol.wait (overlapping the predecessor's tail),
+    // then the activation tiles follow.
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
     const uint32_t tx = (uint32_t)CG * (GEMM_A_BYTES + b_bytes);
@@ -134,9 +146,6 @@ __global__ void __launch_bounds__(256, 1)
       };
       int i0 = 0;
       if (u == pair) {
-        // The weight tiles do not depend on the previous kernel: fill the
-        // ring with them before waiting for it (overlaps the weight stream
-        // with the predecessor's tail), then load the activation tiles.
         const int pre = nk < stages ? nk : stages;
         for (int i = 0; i < pre; ++i) {
           if (leader) mbar_expect_tx(&full[i], tx);
@@ -155,6 +164,34 @@ __global__ void __launch_bounds__(256, 1)
         load_b(s, i);
       }
     }
+  } else if (kcs > 1 && (warp == 0 || warp == 3) && lane == 0) {
+    // ---------------- TMA producers, compute-bound tiles (both CTAs): warp 0
+    // streams the weight tiles, warp 3 the activation tiles, one 3-D box of
+    // kcs k-chunks per stage each (fewer, larger requests).  The leader's
+    // full barrier counts both producers and both CTAs' bytes.  The weights
+    // do not depend on the previous kernel, so warp 0 never waits for it.
+    const bool is_w = warp == 0;
+    const CUtensorMap* tm = is_w ? &tmW : &tmX;
+    prefetch_tmap(tm);
+    if (!is_w) pdl_wait();
+    const uint32_t tx = (uint32_t)CG * (is_w ? a_stage : b_stage);
+    uint8_t* base = is_w ? sA : sB;
+    const int sbytes = is_w ? a_stage : b_stage;
+    int it = 0;  // position in the ring, continuous across units
+    for (int u = pair; u < units; u += npairs) {
+      int m0, n0, kc0, nk;
+      coords(u, m0, n0, kc0, nk);
+      const int row = is_w ? m0 : n0 + (int)rank * bl;
+      for (int i = 0; i < nk; i += kcs, ++it) {
+        const int s = it % stages;
+        if (it >= stages) mbar_wait(&empty[s], ((it / stages) - 1) & 1);
+        if (leader) mbar_expect_tx(&full[s], tx);
+        if (CG == 2)
+          tma_load_3d_2sm(base + (size_t)s * sbytes, tm, row, (kc0 + i), &full[s]);
+        else
+          tma_load_3d(base + (size_t)s * sbytes, tm, row, (kc0 + i), &full[s]);
+      }
+    }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (single thread of the leader CTA)
     const uint32_t idesc = umma_idesc_bf16(GEMM_BM * CG, BN);
@@ -168,22 +205,26 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
       }
       const uint32_t base = tmem + (uint32_t)buf * buf_stride;
-      for (int i = 0; i < nk; ++i, ++it) {
+      for (int i = 0; i < nk; i += kcs, ++it) {
         const int s = it % stages;
         mbar_wait(&full[s], (it / stages) & 1);
         tc_fence_after();
-        const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * GEMM_A_BYTES));
-        const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_bytes));
-        // k-chunk i accumulates into TMEM accumulator i % n_acc: the tensor-core
-        // fp32 accumulation truncates, so short chains + an IEEE fp32 sum of the
-        // accumulators in the epilogue keep the error at fp32-GEMM level.
-        const uint32_t d = base + (uint32_t)((i % n_acc) * acc_stride);
+        for (int kk = 0; kk < kcs; ++kk) {
+          const int ci = i + kk;  // k-chunk index within the unit
+          const uint64_t ad = umma_desc_sw128(smem_u32(sA + (size_t)s * a_stage + (size_t)kk * GEMM_A_BYTES));
+          const uint64_t bd = umma_desc_sw128(smem_u32(sB + (size_t)s * b_stage + (size_t)kk * b_bytes));
+          // k-chunk ci accumulates into TMEM accumulator ci % n_acc: the
+          // tensor-core fp32 accumulation truncates, so short chains + an IEEE
+          // fp32 sum of the accumulators in the epilogue keep the error at
+          // fp32-GEMM level.
+          const uint32_t d = base + (uint32_t)((ci % n_acc) * acc_stride);
 #pragma unroll
-        for (int k = 0; k < GEMM_BK / 16; ++k) {  // K = 16 per MMA: advance 32 B inside the swizzle atom
-          if (CG == 2)
-            umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
-          else
-            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i >= n_acc || k > 0) ? 1u : 0u);
+          for (int k = 0; k < GEMM_BK / 16; ++k) {  // K = 16 per MMA: advance 32 B inside the swizzle atom
+            if (CG == 2)
+              umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (ci >= n_acc || k > 0) ? 1u : 0u);
+            else
+              umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (ci >= n_acc || k > 0) ? 1u : 0u);
+          }
         }
         if (CG == 2)
           umma_commit_2sm(&empty[s]);
@@ -319,15 +360,26 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 2-D bf16 row-major [rows, cols] tensor, box [box_rows, 64] with 128-byte swizzle.
-static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+// Row-major bf16 [rows, cols] matrix viewed as (64, rows, cols/64) with
+// strides (2 cols, row pitch, 128 B): box (64, box_rows, kc) = kc consecutive
+// k-chunks of box_rows rows, 128-byte swizzle.
+static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)GEMM_BK, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+  if (kc == 1) {  // 2-D [rows, cols], box [box_rows, 64]
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)GEMM_BK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)GEMM_BK, (cuuint64_t)rows, (cuuint64_t)(cols / GEMM_BK)};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)GEMM_BK * 2};
+  cuuint32_t box[3] = {(cuuint32_t)GEMM_BK, (cuuint32_t)box_rows, (cuuint32_t)kc};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -336,27 +388,29 @@ static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
 struct TmapKey {
   const void* p;
   int64_t rows, cols;
-  int box;
-  bool operator==(const TmapKey& o) const { return p == o.p && rows == o.rows && cols == o.cols && box == o.box; }
+  int box, kc;
+  bool operator==(const TmapKey& o) const {
+    return p == o.p && rows == o.rows && cols == o.cols && box == o.box && kc == o.kc;
+  }
 };
 struct TmapKeyHash {
   size_t operator()(const TmapKey& k) const {
     return std::hash<const void*>()(k.p) ^ (size_t)(k.rows * 1315423911u) ^ (size_t)(k.cols * 2654435761u) ^
-           (size_t)k.box;
+           (size_t)k.box ^ ((size_t)k.kc << 20);
   }
 };
 
-static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc) {
   static std::mutex mu;
   static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
-  TmapKey k{ptr, rows, cols, box_rows};
+  TmapKey k{ptr, rows, cols, box_rows, kc};
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(k);
   if (it != cache.end()) {
     *out = it->second;
     return true;
   }
-  if (!make_tmap(out, ptr, rows, cols, box_rows)) return false;
+  if (!make_tmap(out, ptr, rows, cols, box_rows, kc)) return false;
   if (cache.size() > 4096) cache.clear();
   cache.emplace(k, *out);
   return true;
@@ -386,6 +440,31 @@ int gemm_auto_splits(int N, int K, int T) {
   return s > maxs ? maxs : s;
 }
 
+// Launch one instantiation: PDL always, plus a 2-CTA cluster for CG == 2.
+template <typename Kern, typename... Args>
+static cudaError_t launch_gemm(Kern kern, int cg, dim3 grid, size_t smem, cudaStream_t stream, Args... args) {
+  static thread_local std::unordered_map<const void*, bool> attr;  // per instantiation
+  bool& done = attr[reinterpret_cast<const void*>(kern)];
+  if (!done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = true;
+  }
+  if (cg == 1) return launch_pdl(kern, grid, dim3(256), smem, stream, args...);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
                       cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
@@ -396,19 +475,25 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   const int kc = K / GEMM_BK;
   if (splits <= 0) splits = mode == 1 ? gemm_auto_splits(N, K, T) : 1;
   if (splits > 1 && mode != 1) return cudaErrorInvalidValue;
-  const int per = (kc + splits - 1) / splits;
-  splits = (kc + per - 1) / per;  // every split has >= 1 chunk
-  CUtensorMap tw, tx;
-  if (!cached_tmap(&tw, W, N, K, GEMM_BM)) return cudaErrorInvalidValue;
-  if (!cached_tmap(&tx, X, T, K, BN / CG)) return cudaErrorInvalidValue;
-  const int stage_bytes = GEMM_A_BYTES + (BN / CG) * GEMM_BK * 2;
   // decode-sized tiles (BN <= 128) use half the shared memory and TMEM so two
   // CTAs fit on an SM: the next tile (or the next GEMM, via PDL) streams its
   // weights while the current one drains
   const bool small = BN <= 128;
+  // k-chunks per stage (one 3-D TMA box per operand): 2 for the compute-bound
+  // tiles (fewer, larger TMA requests), 1 for decode tiles (deeper ring)
+  static const int kcs_env = std::getenv("SGS_GEMM_KCS") ? std::atoi(std::getenv("SGS_GEMM_KCS")) : 2;
+  const int kcs = (!small && kc % kcs_env == 0) ? kcs_env : 1;
+  int per = (kc + splits - 1) / splits;
+  per = (per + kcs - 1) / kcs * kcs;  // every split covers whole stages
+  splits = (kc + per - 1) / per;      // every split has >= 1 chunk
+  CUtensorMap tw, tx;
+  if (!cached_tmap(&tw, W, N, K, GEMM_BM, kcs)) return cudaErrorInvalidValue;
+  if (!cached_tmap(&tx, X, T, K, BN / CG, kcs)) return cudaErrorInvalidValue;
+  const int stage_bytes = kcs * (GEMM_A_BYTES + (BN / CG) * GEMM_BK * 2);
   int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
   if (stages > 12) stages = 12;
-  if (stages > kc) stages = kc < 2 ? 2 : kc;
+  const int kst = kc / kcs;  // stages-worth of chunks in the whole K
+  if (stages > kst) stages = kst < 2 ? 2 : kst;
   if (ldc % 4 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return cudaErrorInvalidValue;  // float4 epilogue
   // epilogue exchange: double-buffered for compute-bound tiles (mode 3 then
   // needs one barrier per 16-token chunk); decode tiles keep the smem for stages
@@ -434,30 +519,20 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   while (tmem_cols < nbuf * n_acc * acc_stride) tmem_cols <<= 1;
   if (nbuf == 2 && tmem_cols / 2 < n_acc * acc_stride) tmem_cols <<= 1;
   if (tmem_cols > 512) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(gemm_bf16_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
   const dim3 grid(pairs * CG);
-  if (CG == 1)
-    return launch_pdl(gemm_bf16_tc_kernel<1>, grid, dim3(256), smem, stream, tw, tx, C, T, ldc, BN, stages, kc, per,
-                      mode, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc_kernel<2>, tw, tx, C, T, ldc, BN, stages, kc, per, mode, tmem_cols,
-                            n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs);
+  switch ((CG - 1) * 8 + mode * 2 + (kcs - 1)) {
+#define SGS_GEMM_CASE(cg, md, kk)                                                                                     \
+  case (cg - 1) * 8 + md * 2 + (kk - 1):                                                                            \
+    return launch_gemm(gemm_bf16_tc_kernel<cg, md, kk>, cg, grid, smem, stream, tw, tx, C, T, ldc, BN, stages, kc, \
+                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs);
+    SGS_GEMM_CASE(1, 0, 1) SGS_GEMM_CASE(1, 0, 2) SGS_GEMM_CASE(1, 1, 1) SGS_GEMM_CASE(1, 1, 2)
+    SGS_GEMM_CASE(1, 2, 1) SGS_GEMM_CASE(1, 2, 2) SGS_GEMM_CASE(1, 3, 1) SGS_GEMM_CASE(1, 3, 2)
+    SGS_GEMM_CASE(2, 0, 1) SGS_GEMM_CASE(2, 0, 2) SGS_GEMM_CASE(2, 1, 1) SGS_GEMM_CASE(2, 1, 2)
+    SGS_GEMM_CASE(2, 2, 1) SGS_GEMM_CASE(2, 2, 2) SGS_GEMM_CASE(2, 3, 1) SGS_GEMM_CASE(2, 3, 2)
+#undef SGS_GEMM_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace sgs

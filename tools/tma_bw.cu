@@ -15,11 +15,12 @@
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtensorMap tm, int stages, int iters,
-                                                 int box_rows, int mode, int rows_total, unsigned long long* sink) {
+__global__ void __launch_bounds__(96) tma_stream(const __grid_constant__ CUtensorMap tm, int stages, int iters,
+                                                 int box_rows, int mode, int rows_total, unsigned long long* sink,
+                                                 int kc, int producers) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int box_bytes = box_rows * 128;
+  const int box_bytes = box_rows * 128 * kc;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * box_bytes);
   uint64_t* empty = full + stages;
   if (threadIdx.x == 0) {
@@ -31,8 +32,9 @@ __global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtenso
   }
   __syncthreads();
   const int row_tiles = rows_total / box_rows;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < iters; ++i) {
+  const int pid = threadIdx.x == 0 ? 0 : (threadIdx.x == 64 ? 1 : -1);
+  if (pid >= 0 && pid < producers) {
+    for (int i = pid; i < iters; i += producers) {
       const int s = i % stages;
       if (i >= stages) {
         const uint32_t par = ((i / stages) - 1) & 1;
@@ -44,21 +46,21 @@ __global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtenso
       }
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(box_bytes)
                    : "memory");
-      // mode 0: CTA-private row band, walk K then rows; mode 1: 2 MB shared window
+      // mode 0: CTA-private row bands (distinct data, HBM); mode 1: 2 MB shared window (L2)
+      const int kt = 64 / kc;  // boxes per row band (K = 4096 = 64 chunks)
       int x, y;
       if (mode == 0) {
-        const int kt = 64;  // 64 K-tiles of 64 columns per row band (K = 4096)
-        const int band = (blockIdx.x * 64 + i / kt) % row_tiles;
-        x = (i % kt) * 64, y = band * box_rows;
+        const int band = (blockIdx.x * 3 + i / kt) % row_tiles;
+        x = (i % kt) * kc, y = band * box_rows;
       } else {
-        const int win = (2 << 20) / (box_rows * 128);  // tiles in 2 MB
+        const int win = (2 << 20) / box_bytes;
         const int t = (blockIdx.x * 7 + i) % win;
-        x = (t % 64) * 64, y = (t / 64) * box_rows;
+        x = (t % kt) * kc, y = (t / kt) * box_rows;
       }
       asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-              su32(smem + (size_t)s * box_bytes)),
-          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(su32(&full[s])), "r"(x), "r"(y)
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+          "[%2];" ::"r"(su32(smem + (size_t)s * box_bytes)),
+          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(su32(&full[s])), "r"(0), "r"(y), "r"(x)
           : "memory");
     }
   } else if (threadIdx.x == 32) {
@@ -100,41 +102,48 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
+  struct Cfg { int mode, box_rows, kc, per_sm, stages, producers; };
+  std::vector<Cfg> cfgs;
   for (int mode = 0; mode < 2; ++mode)
     for (int box_rows : {128, 256})
-      for (int per_sm : {1, 2})
-        for (int stages : {2, 4, 6, 8, 12}) {
-          const int box_bytes = box_rows * 128;
-          const size_t smem = 1024 + (size_t)stages * box_bytes + 2 * stages * 8;
-          if (smem * per_sm > 227 * 1024) continue;
-          CUtensorMap tm;
-          cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-          cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-          cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-          cuuint32_t es[2] = {1, 1};
-          if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-            printf("encode failed\n");
-            return 1;
-          }
-          const int grid = sms * per_sm;
-          const int iters = (int)((256LL << 20) * (mode == 0 ? 1 : 2) / ((long long)grid * box_bytes));
-          for (int rep = 0; rep < 2; ++rep) {
-            cudaEventRecord(a);
-            tma_stream<<<grid, 64, smem>>>(tm, stages, iters, box_rows, mode, rows, sink);
-            cudaEventRecord(b);
-            cudaEventSynchronize(b);
-          }
-          float ms = 0;
-          cudaEventElapsedTime(&ms, a, b);
-          const double bytes = (double)grid * iters * box_bytes;
-          printf("{\"mode\": \"%s\", \"box_rows\": %d, \"ctas_per_sm\": %d, \"stages\": %d, \"GBs\": %.1f, "
-                 "\"GBs_per_sm\": %.1f, \"inflight_KB_per_sm\": %d}\n",
-                 mode == 0 ? "hbm" : "l2", box_rows, per_sm, stages, bytes / ms / 1e6, bytes / ms / 1e6 / sms,
-                 stages * box_bytes * per_sm / 1024);
-          fflush(stdout);
-        }
+      for (int kc : {1, 2, 4})
+        for (int per_sm : {1, 2})
+          for (int producers : {1, 2})
+            for (int stages : {3, 6}) cfgs.push_back({mode, box_rows, kc, per_sm, stages, producers});
+  for (const Cfg& c : cfgs) {
+    const int box_bytes = c.box_rows * 128 * c.kc;
+    const size_t smem = 1024 + (size_t)c.stages * box_bytes + 2 * c.stages * 8;
+    if (smem * c.per_sm > 226 * 1024 || c.box_rows * c.kc > 256 * 2 + 0 && c.kc * c.box_rows > 512) continue;
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)c.box_rows, (cuuint32_t)c.kc};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS) {
+      printf("encode failed kc=%d rows=%d\n", c.kc, c.box_rows);
+      continue;
+    }
+    const int grid = sms * c.per_sm;
+    const int iters = (int)((256LL << 20) * (c.mode == 0 ? 1 : 2) / ((long long)grid * box_bytes));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(a);
+      tma_stream<<<grid, 96, smem>>>(tm, c.stages, iters, c.box_rows, c.mode, rows, sink, c.kc, c.producers);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      if (rep > 0 && ms < best) best = ms;
+    }
+    const double bytes = (double)grid * iters * box_bytes;
+    printf("{\"mode\": \"%s\", \"box_KB\": %d, \"box_rows\": %d, \"kc\": %d, \"ctas_per_sm\": %d, \"producers\": %d, "
+           "\"stages\": %d, \"GBs\": %.1f, \"GBs_per_sm\": %.1f}\n",
+           c.mode == 0 ? "hbm" : "l2", box_bytes / 1024, c.box_rows, c.kc, c.per_sm, c.producers, c.stages,
+           bytes / best / 1e6, bytes / best / 1e6 / sms);
+    fflush(stdout);
+  }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;
