@@ -350,17 +350,29 @@ void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page
   plan->n_parts = 0;
   int64_t total = 0;
   for (int i = 0; i < b; ++i) total += (int64_t)((ctx[i] + page - 1) / page) * nkv;
-  int chunk = split_pages;
-  if (chunk <= 0) {
-    // about one wave of 2 CTAs per SM (148 SMs), at least two pages per warp
-    const int64_t target = 2 * 148;
-    chunk = (int)std::max<int64_t>(2 * ATTN_WARPS, (total + target - 1) / target);
-  }
+  // One wave of 2 CTAs per SM (296 slots): a (row, kv head) with np pages
+  // gets floor(296 np / total) parts, so the items never spill into a second,
+  // nearly empty wave; parts keep >= 2 pages per warp and there are at most
+  // ATTN_SPLIT_CAP of them (the last-arriving CTA merges them serially).
+  constexpr int64_t kSlots = 2 * 148;
+  constexpr int ATTN_SPLIT_CAP = 32;
+  auto parts = [&](int np) {
+    int nch = (int)(kSlots * np / total);
+    const int by_pages = np / (2 * ATTN_WARPS);
+    if (nch > by_pages) nch = by_pages;
+    if (nch > ATTN_SPLIT_CAP) nch = ATTN_SPLIT_CAP;
+    return nch < 1 ? 1 : nch;
+  };
   for (int i = 0; i < b; ++i) {
     const int np = (ctx[i] + page - 1) / page;
     if (np == 0) continue;
-    int nch = (np + chunk - 1) / chunk;
-    if (nch > ATTN_MAX_PARTS) nch = ATTN_MAX_PARTS;
+    int nch;
+    if (split_pages > 0) {
+      nch = (np + split_pages - 1) / split_pages;
+      if (nch > ATTN_MAX_PARTS) nch = ATTN_MAX_PARTS;
+    } else {
+      nch = parts(np);
+    }
     for (int h = 0; h < nkv; ++h) {
       if (nch == 1) {
         plan->items.push_back(AttnItem{i, h, 0, np, -1, -1, slot ? slot[i] : i, ctx[i]});

@@ -93,7 +93,7 @@ cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows,
 // before griddepcontrol.wait; after it every qkv load of the unit is issued
 // before any store.  The fp32 qkv row is zeroed after it is read, so the next
 // split-K QKV GEMM (fp32 red.add) finds a zeroed accumulator without a memset.
-constexpr int ROPE_THREADS = 128, ROPE_U = 8;
+constexpr int ROPE_THREADS = 128, ROPE_U = 4;  // small unroll: the kernel stays far below the I-cache knee
 __global__ void __launch_bounds__(ROPE_THREADS)
     rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
                        const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,

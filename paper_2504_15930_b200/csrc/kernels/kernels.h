@@ -28,9 +28,10 @@ struct AttnPlan {
   std::vector<AttnComb> combs;
   int n_parts = 0;
 };
-// Split-K plan over pages: rows with more than `chunk` pages are split (at
-// most 64 parts per row and kv head).  The item count is bounded by
-// 2*148 + 2*b*nkv (+ the split_pages override).
+// Split-K plan over pages: about one wave of 2 CTAs per SM -- a (row, kv
+// head) with np of the total pages gets floor(296 np / total) parts (>= 8
+// pages each, <= 32 parts).  The item count is bounded by 296 + b*nkv (+ the
+// split_pages override, <= 64 parts per row and kv head).
 // slot[row] is the block-table row of each sample (NULL: the row index).
 void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page, int split_pages, AttnPlan* plan);
 int64_t attn_workspace_bytes(int max_items, int max_parts, int g, int hd);
