@@ -1,9 +1,10 @@
 // a4 / K10: causal prefill attention over each admitted prompt (the prompt
 // tokens "establish the KV cache", §2.1).  Flash-style: one CTA =
-// (prompt, query head, 64-query block), 4 warps x 16 query rows; key/value
-// tiles of 64 tokens staged in shared memory (XOR-swizzled rows), S = Q K^T
-// on mma.sync bf16 with fp32 accumulation, online softmax in fp32 (exp2),
-// O += P V with P in fp16.  The prompt K/V come from the contiguous copy the
+// (prompt, kv head, 16 queries) with one warp per query head of the GQA group
+// sharing the key/value tiles; tiles of 64 tokens are double-buffered in
+// shared memory with cp.async (XOR-swizzled rows), S = Q K^T on mma.sync bf16
+// with fp32 accumulation, online softmax in fp32 (exp2), O += P V with P split
+// into two fp16 parts.  The prompt K/V come from the contiguous copy the
 // RoPE/append kernel writes for prefill rows.
 #include <cmath>
 
@@ -12,22 +13,57 @@
 
 namespace sgs {
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One CTA = (prompt, kv head, 16 consecutive queries); warp w handles q head
+// kh * G + w of the group, so the K/V tiles staged in shared memory serve all
+// G query heads that read them (GQA).  Key/value tiles of 64 tokens are
+// double-buffered with cp.async (zero-filled past the prompt end).
 template <int HD>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                         const __nv_bfloat16* __restrict__ v, const int32_t* __restrict__ offs,
                         const int32_t* __restrict__ qblocks, int nq, int nkv, float scale_log2,
                         __nv_bfloat16* __restrict__ out) {
-  constexpr int BQ = 64, BK = 64, RC = HD / 8, NT = HD / 8;
-  __shared__ __align__(128) uint8_t sK[BK * HD * 2];
-  __shared__ __align__(128) uint8_t sV[BK * HD * 2];
-  const int p = qblocks[2 * blockIdx.x], qb = qblocks[2 * blockIdx.x + 1];
-  const int h = blockIdx.y, kh = h / (nq / nkv);
-  const int off = offs[p], P = offs[p + 1] - off;
+  constexpr int BK = 64, RC = HD / 8, NT = HD / 8;
+  constexpr int TILE = BK * HD * 2;  // bytes of K (or V) per tile
+  extern __shared__ __align__(128) uint8_t sm[];  // [2 buffers][K | V]
+  pdl_trigger();
+  pdl_wait();
+  const int e = blockIdx.x >> 2, sub = blockIdx.x & 3;
+  const int p = qblocks[2 * e], qb = qblocks[2 * e + 1];
+  const int kh = blockIdx.y, G = nq / nkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = qb * BQ + warp * 16;
-  const int r0 = lane >> 2, r1 = r0 + 8, cq = 2 * (lane & 3);
+  const int h = kh * G + warp;
+  const int off = offs[p], P = offs[p + 1] - off;
+  const int q0 = qb * 64 + sub * 16;
+  if (q0 >= P) return;
+  const int kend = min(P, q0 + 16);
+  const int ntiles = (kend + BK - 1) / BK;
+  const uint32_t sbase = smem_u32(sm);
 
+  auto load_tile = [&](int kt, int buf) {
+    const uint32_t kb = sbase + (uint32_t)(buf * 2 * TILE), vb = kb + TILE;
+    for (int c = threadIdx.x; c < BK * RC; c += blockDim.x) {
+      const int r = c / RC, ch = c % RC, key = kt * BK + r;
+      const bool ok = key < P;
+      const size_t src = ((size_t)(off + (ok ? key : 0)) * nkv + kh) * HD + ch * 8;
+      const uint32_t dst = (uint32_t)(r * HD * 2 + ((ch ^ kv_swz(r, RC)) << 4));
+      cp_async16(kb + dst, k + src, ok ? 16 : 0);
+      cp_async16(vb + dst, v + src, ok ? 16 : 0);
+    }
+    cp_async_commit();
+  };
+  load_tile(0, 0);
+
+  const int r0 = lane >> 2, r1 = r0 + 8, cq = 2 * (lane & 3);
   uint32_t qa[HD / 16][4];
   {
     const uint32_t* Q = reinterpret_cast<const uint32_t*>(q);
@@ -48,27 +84,19 @@ __global__ void __launch_bounds__(128)
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const int ktok = ((lane >> 4) << 3) + (lane & 7), kchk = (lane >> 3) & 1;
   const int vtok = (((lane >> 3) & 1) << 3) + (lane & 7), vchk = lane >> 4;
-  const int kend = min(P, (qb + 1) * BQ);
-  const uint32_t kbase = smem_u32(sK), vbase = smem_u32(sV);
 
-  for (int kt = 0; kt * BK < kend; ++kt) {
-    __syncthreads();
-    for (int c = threadIdx.x; c < BK * RC; c += blockDim.x) {
-      const int r = c / RC, ch = c % RC, key = kt * BK + r;
-      uint4 kvv = make_uint4(0, 0, 0, 0), vvv = make_uint4(0, 0, 0, 0);
-      if (key < P) {
-        const size_t src = ((size_t)(off + key) * nkv + kh) * HD + ch * 8;
-        kvv = *reinterpret_cast<const uint4*>(k + src);
-        vvv = *reinterpret_cast<const uint4*>(v + src);
-      }
-      const int dst = r * HD * 2 + ((ch ^ kv_swz(r, RC)) << 4);
-      *reinterpret_cast<uint4*>(sK + dst) = kvv;
-      *reinterpret_cast<uint4*>(sV + dst) = vvv;
+  for (int kt = 0; kt < ntiles; ++kt) {
+    if (kt + 1 < ntiles) {
+      load_tile(kt + 1, (kt + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (q0 + 15 < kt * BK) continue;  // whole tile is in this warp's future
+    const uint32_t kbase = sbase + (uint32_t)((kt & 1) * 2 * TILE), vbase = kbase + TILE;
 #pragma unroll
     for (int j = 0; j < BK / 16; ++j) {
+      if (kt * BK + 16 * j > q0 + 15) break;  // sub-tile entirely in the future of these queries
       float sc[2][4];
 #pragma unroll
       for (int t = 0; t < 2; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
@@ -81,14 +109,16 @@ __global__ void __launch_bounds__(128)
         mma_bf16_16816(sc[0], qa[kk], b0, b1);
         mma_bf16_16816(sc[1], qa[kk], b2, b3);
       }
+      if (kt * BK + 16 * j + 15 > q0 || kt * BK + 16 * j + 15 >= P) {  // diagonal / ragged sub-tile
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int key = kt * BK + 16 * j + 8 * t + cq + (e & 1);
-          const int qry = q0 + (e < 2 ? r0 : r1);
-          if (key > qry || key >= P) sc[t][e] = -INFINITY;
-        }
+          for (int el = 0; el < 4; ++el) {
+            const int key = kt * BK + 16 * j + 8 * t + cq + (el & 1);
+            const int qry = q0 + (el < 2 ? r0 : r1);
+            if (key > qry || key >= P) sc[t][el] = -INFINITY;
+          }
+      }
       float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])) * scale_log2;
       float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3])) * scale_log2;
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
@@ -137,6 +167,7 @@ __global__ void __launch_bounds__(128)
         mma_f16_16816(o[2 * nn + 1], pl, h2, h3);
       }
     }
+    __syncthreads();  // this buffer is refilled by the load issued in iteration kt + 1
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -156,29 +187,37 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+template <int HD>
+static cudaError_t launch_prefill(const void* q, const void* k, const void* v, const int32_t* offs,
+                                  const int32_t* qblocks, int n_qblocks, int nq, int nkv, float sl2, void* out,
+                                  cudaStream_t stream) {
+  constexpr int smem = 2 * 2 * 64 * HD * 2;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_prefill_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  return launch_pdl(attn_prefill_kernel<HD>, dim3(4 * n_qblocks, nkv), dim3(32 * (nq / nkv)), (size_t)smem, stream,
+                    reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
+                    reinterpret_cast<const __nv_bfloat16*>(v), offs, qblocks, nq, nkv, sl2,
+                    reinterpret_cast<__nv_bfloat16*>(out));
+}
+
 cudaError_t attn_prefill(const void* q, const void* k, const void* v, const int32_t* offs, const int32_t* qblocks,
                          int n_qblocks, int nq, int nkv, int hd, void* out, cudaStream_t stream) {
   if (n_qblocks <= 0) return cudaSuccess;
+  if (nq % nkv != 0 || nq / nkv > 8) return cudaErrorInvalidValue;  // one warp per query head of a group
   const float sl2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
-  dim3 grid(n_qblocks, nq);
-  auto Q = reinterpret_cast<const __nv_bfloat16*>(q);
-  auto K = reinterpret_cast<const __nv_bfloat16*>(k);
-  auto V = reinterpret_cast<const __nv_bfloat16*>(v);
-  auto O = reinterpret_cast<__nv_bfloat16*>(out);
   switch (hd) {
     case 32:
-      attn_prefill_kernel<32><<<grid, 128, 0, stream>>>(Q, K, V, offs, qblocks, nq, nkv, sl2, O);
-      break;
+      return launch_prefill<32>(q, k, v, offs, qblocks, n_qblocks, nq, nkv, sl2, out, stream);
     case 64:
-      attn_prefill_kernel<64><<<grid, 128, 0, stream>>>(Q, K, V, offs, qblocks, nq, nkv, sl2, O);
-      break;
+      return launch_prefill<64>(q, k, v, offs, qblocks, n_qblocks, nq, nkv, sl2, out, stream);
     case 128:
-      attn_prefill_kernel<128><<<grid, 128, 0, stream>>>(Q, K, V, offs, qblocks, nq, nkv, sl2, O);
-      break;
+      return launch_prefill<128>(q, k, v, offs, qblocks, n_qblocks, nq, nkv, sl2, out, stream);
     default:
       return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace sgs
