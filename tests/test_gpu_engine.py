@@ -134,7 +134,7 @@ def test_tiny_top_p_sampling_end_to_end(sgs):
     assert agree >= 0.99 * total, (agree, total)
     assert greedy_same < total  # it really samples
     # same seed: the same draws.  Split-K GEMMs reduce with fp32 atomics, so the
-    # logits are reproducible only up to summation order (R20) and a
+    # logits are reproducible only up to summation order (R21) and a
     # draw that lands within rounding of a nucleus boundary may flip; require
     # almost every sample to repeat exactly.
     inst2 = sgs.Instance(shape, c.max_batch, 16 + 256, device=0, n_pages=400, weight_seed=1234,
