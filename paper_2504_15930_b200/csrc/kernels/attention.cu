@@ -90,29 +90,28 @@ __global__ void __launch_bounds__(128, 2)
   if (lane == 0)
     for (int i = pre; i < first; ++i) issue(i);
 
-  // q fragments (A operand, rows = heads of the group)
-  const int r0 = lane >> 2, r1 = r0 + 8, cq = 2 * (lane & 3);
-  uint32_t qa[HD / 16][4];
+  // Transposed formulation (tokens are the MMA's M dimension, the g <= 8
+  // query heads its N): S^T = K Q^T and O^T += V^T P^T, so a 16-token page
+  // step is 8 + 2x8 mma.m16n8k16 instead of 16 + 2x16 with heads as M.
+  // Q^T fragments (B operand): head = lane/4, hd pairs 2(lane%4) (+8).
+  const int hq = lane >> 2, cq = 2 * (lane & 3);
+  uint32_t qb[HD / 16][2];
   {
     const uint32_t* qrow = reinterpret_cast<const uint32_t*>(q + ((size_t)it.row * nq + (size_t)it.kvh * g) * HD);
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      qa[kk][0] = r0 < g ? qrow[(r0 * HD + 16 * kk + cq) >> 1] : 0u;
-      qa[kk][1] = r1 < g ? qrow[(r1 * HD + 16 * kk + cq) >> 1] : 0u;
-      qa[kk][2] = r0 < g ? qrow[(r0 * HD + 16 * kk + 8 + cq) >> 1] : 0u;
-      qa[kk][3] = r1 < g ? qrow[(r1 * HD + 16 * kk + 8 + cq) >> 1] : 0u;
+      qb[kk][0] = hq < g ? qrow[(hq * HD + 16 * kk + cq) >> 1] : 0u;
+      qb[kk][1] = hq < g ? qrow[(hq * HD + 16 * kk + 8 + cq) >> 1] : 0u;
     }
   }
-  float o[NT][4];
+  float o[HD / 16][4];  // O^T: rows hd 16 mt + lane/4 (+8), columns heads cq, cq + 1
 #pragma unroll
-  for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  for (int i = 0; i < HD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads cq, cq + 1
 
-  // per-lane ldmatrix coordinates
-  const int ktok = ((lane >> 4) << 3) + (lane & 7);  // K: matrices (t0-7,lo)(t0-7,hi)(t8-15,lo)(t8-15,hi)
-  const int kchk = (lane >> 3) & 1;
-  const int vtok = (((lane >> 3) & 1) << 3) + (lane & 7);  // V: (t0-7,c)(t8-15,c)(t0-7,c+1)(t8-15,c+1)
-  const int vchk = lane >> 4;
+  // ldmatrix lane coordinates: A fragments of K (tokens x hd) and V^T (hd x tokens)
+  const int arow = (lane & 7) + (((lane >> 3) & 1) << 3), achk = lane >> 4;         // K, non-transposed
+  const int vrow = (lane & 7) + (((lane >> 4) & 1) << 3), vchk = (lane >> 3) & 1;   // V, transposed
 
   for (int i = 0; i < n_my; ++i) {
     const int s = i % ATTN_STAGES;
@@ -121,72 +120,52 @@ __global__ void __launch_bounds__(128, 2)
     const uint32_t vbase = kbase + HALF;
     const int tok0 = (it.p0 + warp + ATTN_WARPS * i) * PAGE_T;
 
-    float sc[2][4];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};  // S^T: tokens lane/4 (+8) x heads cq, cq + 1
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      const int ch = 2 * kk + kchk;
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4(b0, b1, b2, b3, kbase + ktok * (HD * 2) + ((ch ^ kv_swz(ktok, RC)) << 4));
-      mma_bf16_16816(sc[0], qa[kk], b0, b1);
-      mma_bf16_16816(sc[1], qa[kk], b2, b3);
+      const int ch = 2 * kk + achk;
+      uint32_t a[4];
+      ldmatrix_x4(a[0], a[1], a[2], a[3], kbase + arow * (HD * 2) + ((ch ^ kv_swz(arow, RC)) << 4));
+      mma_bf16_16816(sc, a, qb[kk][0], qb[kk][1]);
     }
     // mask tokens beyond the context (only the last page is partial)
     if (tok0 + PAGE_T > L) {
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (tok0 + 8 * t + cq + (e & 1) >= L) sc[t][e] = -INFINITY;
+      if (tok0 + hq >= L) sc[0] = sc[1] = -INFINITY;
+      if (tok0 + hq + 8 >= L) sc[2] = sc[3] = -INFINITY;
     }
-    // online softmax (base 2, scores pre-scaled by log2(e)/sqrt(hd))
-    float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])) * scale_log2;
-    float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3])) * scale_log2;
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    // online softmax per head over the 16 tokens (base 2, pre-scaled scores):
+    // the tokens of a head live in lanes with equal lane % 4
+    float mx0 = fmaxf(sc[0], sc[2]) * scale_log2, mx1 = fmaxf(sc[1], sc[3]) * scale_log2;
+#pragma unroll
+    for (int x = 4; x < 32; x <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, x));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, x));
+    }
     const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
     const float a0 = exp2f(m0 - mn0), a1 = exp2f(m1 - mn1);
     m0 = mn0;
     m1 = mn1;
-    // P = P_hi + P_lo (two fp16 parts) so the softmax weights keep ~22 bits
-    uint32_t pa[4], pl[4];
-    {
-      float p[2][4];
+    const float p00 = exp2f(fmaf(sc[0], scale_log2, -mn0)), p01 = exp2f(fmaf(sc[1], scale_log2, -mn1));
+    const float p10 = exp2f(fmaf(sc[2], scale_log2, -mn0)), p11 = exp2f(fmaf(sc[3], scale_log2, -mn1));
+    l0 = l0 * a0 + (p00 + p10);
+    l1 = l1 * a1 + (p01 + p11);
+    // P^T as the B operand (tokens x heads): transpose the two 8x8 blocks
+    uint32_t h0, lo0, h1, lo1;
+    split_bf16x2(p00, p01, h0, lo0);  // tokens 0..7
+    split_bf16x2(p10, p11, h1, lo1);  // tokens 8..15
+    const uint32_t bh0 = movmatrix_trans(h0), bh1 = movmatrix_trans(h1);
+    const uint32_t bl0 = movmatrix_trans(lo0), bl1 = movmatrix_trans(lo1);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        p[t][0] = exp2f(fmaf(sc[t][0], scale_log2, -mn0));
-        p[t][1] = exp2f(fmaf(sc[t][1], scale_log2, -mn0));
-        p[t][2] = exp2f(fmaf(sc[t][2], scale_log2, -mn1));
-        p[t][3] = exp2f(fmaf(sc[t][3], scale_log2, -mn1));
-      }
-      split_f16x2(p[0][0], p[0][1], pa[0], pl[0]);
-      split_f16x2(p[0][2], p[0][3], pa[1], pl[1]);
-      split_f16x2(p[1][0], p[1][1], pa[2], pl[2]);
-      split_f16x2(p[1][2], p[1][3], pa[3], pl[3]);
-      l0 = l0 * a0 + ((p[0][0] + p[0][1]) + (p[1][0] + p[1][1]));
-      l1 = l1 * a1 + ((p[0][2] + p[0][3]) + (p[1][2] + p[1][3]));
-    }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      o[nt][0] *= a0;
-      o[nt][1] *= a0;
-      o[nt][2] *= a1;
-      o[nt][3] *= a1;
-    }
-#pragma unroll
-    for (int nn = 0; nn < HD / 16; ++nn) {
-      const int ch = 2 * nn + vchk;
-      uint32_t v0, v1, v2, v3;
-      ldmatrix_x4_trans(v0, v1, v2, v3, vbase + vtok * (HD * 2) + ((ch ^ kv_swz(vtok, RC)) << 4));
-      const uint32_t h0 = bf16x2_to_f16x2(v0), h1 = bf16x2_to_f16x2(v1);
-      const uint32_t h2 = bf16x2_to_f16x2(v2), h3 = bf16x2_to_f16x2(v3);
-      mma_f16_16816(o[2 * nn], pa, h0, h1);
-      mma_f16_16816(o[2 * nn], pl, h0, h1);
-      mma_f16_16816(o[2 * nn + 1], pa, h2, h3);
-      mma_f16_16816(o[2 * nn + 1], pl, h2, h3);
+    for (int mt = 0; mt < HD / 16; ++mt) {
+      o[mt][0] *= a0;
+      o[mt][1] *= a1;
+      o[mt][2] *= a0;
+      o[mt][3] *= a1;
+      const int ch = 2 * mt + vchk;
+      uint32_t a[4];
+      ldmatrix_x4_trans(a[0], a[1], a[2], a[3], vbase + vrow * (HD * 2) + ((ch ^ kv_swz(vrow, RC)) << 4));
+      mma_bf16_16816(o[mt], a, bh0, bh1);
+      mma_bf16_16816(o[mt], a, bl0, bl1);
     }
     __syncwarp();
     if (lane == 0 && i + ATTN_STAGES < n_my) {
@@ -194,29 +173,31 @@ __global__ void __launch_bounds__(128, 2)
       issue(i + ATTN_STAGES);
     }
   }
-  // quad-reduce the partial row sums
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  // the row sums: reduce over the lanes holding the other tokens of each head
+#pragma unroll
+  for (int x = 4; x < 32; x <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, x);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, x);
+  }
 
   // ---- merge the 4 warps through shared memory (stage buffers are idle now)
   __syncthreads();
-  float* sO = reinterpret_cast<float*>(smem);                 // [4][16][HD]
+  float* sO = reinterpret_cast<float*>(smem);                 // [4][16][HD] (rows = heads)
   float* sM = sO + ATTN_WARPS * 16 * HD;                       // [4][16]
   float* sL = sM + ATTN_WARPS * 16;                            // [4][16]
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    sO[(warp * 16 + r0) * HD + 8 * nt + cq] = o[nt][0];
-    sO[(warp * 16 + r0) * HD + 8 * nt + cq + 1] = o[nt][1];
-    sO[(warp * 16 + r1) * HD + 8 * nt + cq] = o[nt][2];
-    sO[(warp * 16 + r1) * HD + 8 * nt + cq + 1] = o[nt][3];
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    const int e0 = 16 * mt + hq;
+    sO[(warp * 16 + cq) * HD + e0] = o[mt][0];
+    sO[(warp * 16 + cq + 1) * HD + e0] = o[mt][1];
+    sO[(warp * 16 + cq) * HD + e0 + 8] = o[mt][2];
+    sO[(warp * 16 + cq + 1) * HD + e0 + 8] = o[mt][3];
   }
-  if ((lane & 3) == 0) {
-    sM[warp * 16 + r0] = m0;
-    sM[warp * 16 + r1] = m1;
-    sL[warp * 16 + r0] = l0;
-    sL[warp * 16 + r1] = l1;
+  if (lane < 4) {
+    sM[warp * 16 + cq] = m0;
+    sM[warp * 16 + cq + 1] = m1;
+    sL[warp * 16 + cq] = l0;
+    sL[warp * 16 + cq + 1] = l1;
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < g * HD; idx += blockDim.x) {
@@ -425,7 +406,7 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* bt, const 
                         float* part_ml, int* arrive, cudaStream_t stream) {
   (void)n_combs;
   if (page != PAGE_T) return cudaErrorInvalidValue;
-  if (nq % nkv != 0 || nq / nkv > 16) return cudaErrorInvalidValue;
+  if (nq % nkv != 0 || nq / nkv > 8) return cudaErrorInvalidValue;  // the g query heads are the MMA's N = 8
   if (n_items <= 0) return cudaSuccess;
   switch (hd) {
     case 32:
