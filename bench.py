@@ -155,6 +155,8 @@ def cpu_oracle_sample(shape, steps=1, warmup=0, T=8):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--weight-sync", choices=["sync", "async"], default="sync",
+                    help="sync: broadcast at the batch boundary; async: overlapped with generation (staleness 1)")
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2_7b")
@@ -195,7 +197,9 @@ def main():
 
     prof = tuple(int(x) for x in args.profile.split(",")) if args.profile else DEFAULT_PROFILES.get(cfg.model)
     inst = sgs.Instance(shape, cfg.max_batch, max_ctx, device=local, n_instances=world, instance_rank=rank,
-                        weight_seed=cfg.seed, flags=0 if args.no_kernel_timing else sgs.sgs.F_KERNEL_TIMING,
+                        weight_seed=cfg.seed,
+                        flags=(0 if args.no_kernel_timing else sgs.sgs.F_KERNEL_TIMING) |
+                        (sgs.sgs.F_SHADOW_WEIGHTS if args.weight_sync == "async" else 0),
                         dispatch=args.dispatch, profile=prof, sample_seed=cfg.seed)
     peaks0 = load_peaks()
     inst.set_roofline(peaks0["hbm_gbs"], peaks0["bf16_tflops_sustained"])
@@ -219,11 +223,20 @@ def main():
         t0 = time.perf_counter()
         ev0.record(stream)
         mine = inst.submit_trace(tr)
-        comps = inst.run()
-        # weight sync at the RL-step boundary: rank 0 is the trainer proxy
-        if rank == 0:
-            inst.load_weights_seed(cfg.seed + step + 1)
-        inst.update_weights(0)
+        if args.weight_sync == "async":
+            # fully-async pipelining: the next weights are staged and
+            # broadcast on a side stream while this batch generates; committed at the boundary
+            if rank == 0:
+                inst.stage_weights_seed(cfg.seed + step + 1)
+            inst.update_weights_begin(0)
+            comps = inst.run()
+            inst.update_weights_commit()
+        else:
+            comps = inst.run()
+            # weight sync at the RL-step boundary: rank 0 is the trainer proxy
+            if rank == 0:
+                inst.load_weights_seed(cfg.seed + step + 1)
+            inst.update_weights(0)
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -314,7 +327,8 @@ def main():
                                f"x {cfg.prompt_len} tokens, lognormal(median {cfg.median_out}, sigma {cfg.sigma}) "
                                f"forced lengths <= {cfg.max_out}, B={cfg.max_batch}, longest-first, Alg. 2 dispatch",
                    "prompts_total": n_total, "global_batch": n_total, "parallelism": f"dp{world}",
-                   "dispatch": args.dispatch, "hints": "oracle (= forced)" if args.hint_noise is None else
+                   "dispatch": args.dispatch, "weight_sync": args.weight_sync,
+                   "hints": "oracle (= forced)" if args.hint_noise is None else
                    f"noisy sigma {args.hint_noise}", "profile": list(prof) if prof else None,
                    "l2": "inputs larger than L2 (weights 15 GB, KV pool > 100 GB)"},
         "e2e": {"value": round(tokens / wall_s, 1), "unit": "tokens/s",

@@ -63,7 +63,8 @@ enum { SGS_SAMPLE_GREEDY = 0, SGS_SAMPLE_TOP_P = 1 };
 enum {
   SGS_F_KEEP_LOGITS = 1,     /* keep fp32 logits of the last iteration (teacher-forcing tests) */
   SGS_F_NO_GRAPHS = 2,       /* launch the decode iteration eagerly (no CUDA graphs) */
-  SGS_F_KERNEL_TIMING = 4    /* CUDA-event timing per kernel class (sgs_kernel_stats) */
+  SGS_F_KERNEL_TIMING = 4,   /* CUDA-event timing per kernel class (sgs_kernel_stats) */
+  SGS_F_SHADOW_WEIGHTS = 8   /* reserve a second weight buffer for the asynchronous weight sync */
 };
 
 typedef struct {
@@ -152,6 +153,25 @@ sgs_status sgs_update_weights(sgs_handle* h, int32_t root);
 /* Trainer proxy: regenerate this handle's weights from a new seed on device
  * (the root does this before sgs_update_weights). */
 sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed);
+/* Asynchronous (overlapped) weight sync -- SURVEY NEXT-1, the paper's fully
+ * asynchronous pipelining with staleness 1 over the weight
+ * transmission of P:1022-1030.  Needs SGS_F_SHADOW_WEIGHTS.  The next weights
+ * are written into the shadow buffer (by a trainer through
+ * sgs_shadow_weights, or sgs_stage_weights_seed as the trainer proxy), then
+ * sgs_update_weights_begin broadcasts the root's shadow buffer to every
+ * rank's shadow buffer on a side stream while generation continues on the
+ * current weights; sgs_update_weights_commit (RL-batch boundary: no sample in
+ * flight, SGS_E_STATE otherwise) makes the engine stream wait for the
+ * broadcast, copies shadow -> active on the device and increments the
+ * version, so the samples of the next batch are generated with the new
+ * weights and stamped with the new version.  One update may be in flight
+ * (SGS_E_STATE for a second begin or a stage during it). */
+sgs_status sgs_shadow_weights(sgs_handle* h, void** ptr, int64_t* bytes);
+sgs_status sgs_stage_weights_seed(sgs_handle* h, uint64_t seed);
+sgs_status sgs_update_weights_begin(sgs_handle* h, int32_t root);
+/* *ready = 1 once the in-flight broadcast has completed on the device. */
+sgs_status sgs_update_weights_ready(sgs_handle* h, int32_t* ready);
+sgs_status sgs_update_weights_commit(sgs_handle* h);
 /* Order-independent 64-bit checksum of one logical weight tensor (DESIGN.md
  * §3 tensor ids): sum_i bits16(w_i) * (2i+1) mod 2^64. */
 sgs_status sgs_weight_checksum(sgs_handle* h, int64_t tensor_id, uint64_t* out);

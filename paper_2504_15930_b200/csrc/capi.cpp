@@ -76,6 +76,31 @@ sgs_status sgs_update_weights(sgs_handle* h, int32_t root) {
   return h->eng.update_weights(root);
 }
 
+sgs_status sgs_shadow_weights(sgs_handle* h, void** ptr, int64_t* bytes) {
+  if (!h || !ptr || !bytes) return SGS_E_INVAL;
+  return h->eng.shadow_weights(ptr, bytes);
+}
+
+sgs_status sgs_stage_weights_seed(sgs_handle* h, uint64_t seed) {
+  if (!h) return SGS_E_INVAL;
+  return h->eng.stage_weights_seed(seed);
+}
+
+sgs_status sgs_update_weights_begin(sgs_handle* h, int32_t root) {
+  if (!h) return SGS_E_INVAL;
+  return h->eng.update_weights_begin(root);
+}
+
+sgs_status sgs_update_weights_ready(sgs_handle* h, int32_t* ready) {
+  if (!h || !ready) return SGS_E_INVAL;
+  return h->eng.update_weights_ready(ready);
+}
+
+sgs_status sgs_update_weights_commit(sgs_handle* h) {
+  if (!h) return SGS_E_INVAL;
+  return h->eng.update_weights_commit();
+}
+
 sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed) {
   if (!h) return SGS_E_INVAL;
   return h->eng.load_weights_seed(seed);

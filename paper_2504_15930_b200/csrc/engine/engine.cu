@@ -82,6 +82,7 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->off_attn = take(L->attn_bytes);
   L->off_cksum = take(64);
   L->scratch_bytes = o - s0;
+  L->off_shadow = (e.flags & SGS_F_SHADOW_WEIGHTS) ? take(L->weights_bytes) : -1;
   L->total = o;
   L->tmax = (int)tmax;
   L->max_pages = (int)max_pages;
@@ -108,6 +109,11 @@ Engine::~Engine() {
     if (tok_host_) cudaFreeHost(tok_host_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    if (st_side_) {
+      cudaStreamSynchronize(st_side_);
+      cudaStreamDestroy(st_side_);
+    }
+    if (ev_sync_) cudaEventDestroy(ev_sync_);
   }
 }
 
@@ -230,6 +236,11 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   CK(cudaMallocHost(&tok_host_, tok_host_cap_ * 4), "cudaMallocHost(tokens)");
   CK(cudaEventCreate(&ev0_), "event");
   CK(cudaEventCreate(&ev1_), "event");
+  if (L_.off_shadow >= 0) {
+    shadow_ = arena_ + L_.off_shadow;
+    CK(cudaStreamCreateWithFlags(&st_side_, cudaStreamNonBlocking), "side stream");
+    CK(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming), "event");
+  }
   // zero the KV pool (finite garbage only beyond ctx) and the small state
   CK(cudaMemsetAsync(arena_ + L_.off_kv, 0, L_.kv_bytes, st_), "memset kv");
   CK(cudaMemsetAsync(bt_, 0, (size_t)e.max_batch * L_.max_pages * 4, st_), "memset bt");
@@ -966,6 +977,10 @@ sgs_status Engine::update_weights(int root) {
     err = "weight update with samples in flight";
     return SGS_E_STATE;
   }
+  if (sync_pending_) {
+    err = "an asynchronous weight update is in flight";
+    return SGS_E_STATE;
+  }
   if (null_) {
     ++version;
     return SGS_OK;
@@ -999,6 +1014,117 @@ sgs_status Engine::update_weights(int root) {
     CK(cudaStreamSynchronize(st_), "broadcast sync");
   }
   ++version;
+  return SGS_OK;
+}
+
+// ------------------------------------------------------------------ asynchronous weight sync (NEXT-1)
+sgs_status Engine::shadow_weights(void** ptr, int64_t* bytes) {
+  if (!null_ && !shadow_) {
+    err = "engine created without SGS_F_SHADOW_WEIGHTS";
+    return SGS_E_STATE;
+  }
+  *ptr = shadow_;
+  *bytes = L_.weights_bytes;
+  return SGS_OK;
+}
+
+sgs_status Engine::stage_weights_seed(uint64_t seed) {
+  if (null_) return SGS_OK;
+  if (!shadow_) {
+    err = "engine created without SGS_F_SHADOW_WEIGHTS";
+    return SGS_E_STATE;
+  }
+  if (sync_pending_) {
+    err = "a weight update is in flight";
+    return SGS_E_STATE;
+  }
+  // the same tensors at the same offsets of the shadow buffer, on the side stream
+  for (const auto& t : tensors_) {
+    void* dst = shadow_ + (reinterpret_cast<uint8_t*>(t.ptr) - arena_);
+    CK(hash_init(dst, seed, (uint64_t)t.id, t.n, t.is_norm, st_side_, t.cols, t.blk, t.stride, t.off),
+       "hash_init(shadow)");
+  }
+  return SGS_OK;
+}
+
+sgs_status Engine::update_weights_begin(int root) {
+  if (poisoned) {
+    err = "handle poisoned";
+    return SGS_E_STATE;
+  }
+  if (sync_pending_) {
+    err = "a weight update is already in flight";
+    return SGS_E_STATE;
+  }
+  if (null_) {
+    sync_pending_ = true;
+    return SGS_OK;
+  }
+  if (!shadow_) {
+    err = "engine created without SGS_F_SHADOW_WEIGHTS";
+    return SGS_E_STATE;
+  }
+  if (nccl_world_ > 1) {
+    if (!nccl_comm_) {
+      err = "sgs_comm_init not called";
+      return SGS_E_STATE;
+    }
+    NcclApi* api = nccl();
+    const size_t total = (size_t)L_.weights_bytes;
+    const size_t chunk = 256ull << 20;
+    api->GroupStart();
+    for (size_t o = 0; o < total; o += chunk) {
+      const size_t n = std::min(chunk, total - o);
+      ncclResult_t r = api->Broadcast(shadow_ + o, shadow_ + o, n, ncclUint8, root, (ncclComm_t)nccl_comm_, st_side_);
+      if (r != ncclSuccess) {
+        api->GroupEnd();
+        err = std::string("ncclBroadcast: ") + api->GetErrorString(r);
+        poisoned = true;
+        return SGS_E_NCCL;
+      }
+    }
+    ncclResult_t r = api->GroupEnd();
+    if (r != ncclSuccess) {
+      err = std::string("ncclGroupEnd: ") + api->GetErrorString(r);
+      poisoned = true;
+      return SGS_E_NCCL;
+    }
+  }
+  CK(cudaEventRecord(ev_sync_, st_side_), "record sync");
+  sync_pending_ = true;
+  return SGS_OK;
+}
+
+sgs_status Engine::update_weights_ready(int32_t* ready) {
+  if (!sync_pending_) {
+    err = "no weight update in flight";
+    return SGS_E_STATE;
+  }
+  if (null_) {
+    *ready = 1;
+    return SGS_OK;
+  }
+  const cudaError_t q = cudaEventQuery(ev_sync_);
+  if (q != cudaSuccess && q != cudaErrorNotReady) return cuda_fail(q, "query sync");
+  *ready = q == cudaSuccess ? 1 : 0;
+  return SGS_OK;
+}
+
+sgs_status Engine::update_weights_commit() {
+  if (!sync_pending_) {
+    err = "no weight update in flight";
+    return SGS_E_STATE;
+  }
+  if (!sched.idle()) {
+    err = "weight commit with samples in flight (the swap happens at an RL-batch boundary)";
+    return SGS_E_STATE;
+  }
+  if (!null_) {
+    CK(cudaStreamWaitEvent(st_, ev_sync_, 0), "wait sync");
+    CK(cudaMemcpyAsync(arena_, shadow_, (size_t)L_.weights_bytes, cudaMemcpyDeviceToDevice, st_), "swap weights");
+  }
+  ++version;
+  sync_pending_ = false;
   return SGS_OK;
 }
 

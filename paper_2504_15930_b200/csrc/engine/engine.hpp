@@ -28,7 +28,7 @@ struct ArenaLayout {
   // offsets (bytes from arena start)
   int64_t off_kv = 0, off_h = 0, off_x = 0, off_qkv = 0, off_q = 0, off_kc = 0, off_vc = 0, off_ao = 0,
           off_gu = 0, off_mm = 0, off_logits = 0, off_rope = 0, off_bt = 0, off_last = 0, off_hist = 0,
-          off_meta = 0, off_attn = 0, off_cksum = 0;
+          off_meta = 0, off_attn = 0, off_cksum = 0, off_shadow = -1;
   int64_t meta_bytes = 0, attn_bytes = 0, meta_dec_bytes = 0;
   int tmax = 0, max_pages = 0, max_items = 0;
 };
@@ -52,6 +52,12 @@ class Engine {
   sgs_status checksum(int64_t tensor_id, uint64_t* out);
   sgs_status comm_init(const uint8_t id[128], int rank, int world);
   sgs_status update_weights(int root);
+  // asynchronous weight sync (SGS_F_SHADOW_WEIGHTS): shadow buffer, side stream
+  sgs_status shadow_weights(void** ptr, int64_t* bytes);
+  sgs_status stage_weights_seed(uint64_t seed);
+  sgs_status update_weights_begin(int root);
+  sgs_status update_weights_ready(int32_t* ready);
+  sgs_status update_weights_commit();
   sgs_status last_logits(float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap, int32_t* rows);
   sgs_status debug_forward(const int32_t* tokens, int32_t T, float* dump, int layer = -1,
                            const float* h_in = nullptr);
@@ -144,6 +150,10 @@ class Engine {
   int32_t* tok_host_ = nullptr;  // pinned, completed tokens
   int64_t tok_host_cap_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  uint8_t* shadow_ = nullptr;           // second weight buffer (SGS_F_SHADOW_WEIGHTS)
+  cudaStream_t st_side_ = nullptr;      // weight staging + broadcast, concurrent with generation
+  cudaEvent_t ev_sync_ = nullptr;       // end of the in-flight broadcast on st_side_
+  bool sync_pending_ = false;
   // prompts (host)
   std::vector<int32_t> prompt_store_;
   std::vector<uint64_t> seen_ids_;

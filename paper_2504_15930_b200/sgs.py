@@ -19,11 +19,14 @@ DISPATCH = {"skew": 0, "round_robin": 1, "random": 2}
 F_KEEP_LOGITS = 1
 F_NO_GRAPHS = 2
 F_KERNEL_TIMING = 4
+F_SHADOW_WEIGHTS = 8
 
 # every symbol include/sgs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "sgs_arena_bytes", "sgs_init", "sgs_destroy", "sgs_last_error", "sgs_submit", "sgs_step", "sgs_pending",
     "sgs_comm_unique_id", "sgs_comm_init", "sgs_update_weights", "sgs_load_weights_seed", "sgs_weight_checksum",
+    "sgs_shadow_weights", "sgs_stage_weights_seed", "sgs_update_weights_begin", "sgs_update_weights_ready",
+    "sgs_update_weights_commit",
     "sgs_weight_version", "sgs_trace", "sgs_trace_clear", "sgs_last_logits", "sgs_last_iter_ms",
     "sgs_kernel_launches", "sgs_fit_profile", "sgs_dispatch_plan", "sgs_attn_workspace_bytes",
     "sgs_op_decode_attention", "sgs_op_gemm", "sgs_op_rmsnorm", "sgs_op_rope_append", "sgs_rope_table",
@@ -99,6 +102,11 @@ def _declare(L):
     L.sgs_comm_unique_id.argtypes = [P(ctypes.c_uint8)]
     L.sgs_comm_init.argtypes = [vp, P(ctypes.c_uint8), i32, i32]
     L.sgs_update_weights.argtypes = [vp, i32]
+    L.sgs_shadow_weights.argtypes = [vp, P(vp), P(i64)]
+    L.sgs_stage_weights_seed.argtypes = [vp, u64]
+    L.sgs_update_weights_begin.argtypes = [vp, i32]
+    L.sgs_update_weights_ready.argtypes = [vp, P(i32)]
+    L.sgs_update_weights_commit.argtypes = [vp]
     L.sgs_load_weights_seed.argtypes = [vp, u64]
     L.sgs_weight_checksum.argtypes = [vp, i64, P(u64)]
     L.sgs_weight_version.argtypes = [vp, P(i32)]
@@ -284,6 +292,27 @@ class Instance:
 
     def update_weights(self, root: int = 0):
         _check(lib().sgs_update_weights(self.h, root), self.h)
+
+    # ---- asynchronous weight sync (flags |= F_SHADOW_WEIGHTS)
+    def shadow_weights(self):
+        """(device pointer, bytes) of the shadow weight buffer a trainer writes the next weights into."""
+        p, n = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib().sgs_shadow_weights(self.h, ctypes.byref(p), ctypes.byref(n)), self.h)
+        return p.value, n.value
+
+    def stage_weights_seed(self, seed: int):
+        _check(lib().sgs_stage_weights_seed(self.h, seed), self.h)
+
+    def update_weights_begin(self, root: int = 0):
+        _check(lib().sgs_update_weights_begin(self.h, root), self.h)
+
+    def update_weights_ready(self) -> bool:
+        r = ctypes.c_int32()
+        _check(lib().sgs_update_weights_ready(self.h, ctypes.byref(r)), self.h)
+        return bool(r.value)
+
+    def update_weights_commit(self):
+        _check(lib().sgs_update_weights_commit(self.h), self.h)
 
     def weight_version(self) -> int:
         v = ctypes.c_int32()

@@ -49,6 +49,73 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _async_worker(rank, world, port, q):
+    # NEXT-1: the broadcast of the next weights overlaps generation of the
+    # current batch; the batch completes on the old weights (old checksums,
+    # old version), the commit at the batch boundary installs the new ones
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2504_15930_b200 as sgs
+        shape = workload.MODELS["tiny"]
+        inst = sgs.Instance(shape, 8, 128, device=rank, n_pages=64, n_instances=world, instance_rank=rank,
+                            weight_seed=77, flags=sgs.sgs.F_SHADOW_WEIGHTS)
+        uid = [sgs.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        inst.comm_init(uid[0], rank, world)
+        tr = workload.make_trace(16, 12, 30, 0.5, 40, shape.vocab, seed=5)
+        inst.submit_trace(tr)
+        inst.step()
+        if rank == 0:
+            inst.stage_weights_seed(4242)  # trainer proxy writes the next weights into its shadow buffer
+        inst.update_weights_begin(0)
+        done = inst.run()  # generation continues while the broadcast runs on the side stream
+        old = {tid: inst.checksum(tid) for tid in (0, 16, 27)}
+        inst.update_weights_commit()
+        new = {tid: inst.checksum(tid) for tid in (0, 16, 27)}
+        tr2 = workload.make_trace(4, 12, 5, 0.5, 5, shape.vocab, seed=6, id_base=1000)
+        inst.submit_trace(tr2)
+        done2 = inst.run()
+        out = [None] * world
+        dist.all_gather_object(out, dict(rank=rank, old=old, new=new, v1={c["weight_version"] for c in done},
+                                         v2={c["weight_version"] for c in done2}, version=inst.weight_version()))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(target, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_async_weight_sync_overlaps_generation():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run with gpurun --gpus 2)")
+    res = _spawn(_async_worker, 2)
+    shape = workload.MODELS["tiny"]
+    sizes = {0: shape.vocab * shape.d_model, 16: shape.n_q_heads * shape.head_dim * shape.d_model,
+             27: shape.d_model}
+    for r in res:
+        assert r["v1"] == {0} and r["v2"] == {1} and r["version"] == 1
+        for tid, n in sizes.items():
+            assert r["old"][tid] == oracle.tensor_checksum(77, tid, n, tid == 27), (r["rank"], tid)
+            assert r["new"][tid] == oracle.tensor_checksum(4242, tid, n, tid == 27), (r["rank"], tid)
+
+
 def test_weight_sync_broadcast_bit_identical():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (run with gpurun --gpus 2)")

@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 import workload
-from paper_2504_15930_b200 import Instance, dispatch_plan, fit_profile
+from paper_2504_15930_b200 import Instance, SgsError, dispatch_plan, fit_profile
 
 PROF = (20000, 500, 128, 2000)
 
@@ -116,6 +116,37 @@ def test_capacity_and_validation_errors():
     inst.update_weights(0)
     assert inst.weight_version() == 1
     assert len(oracle.parse_iter_blob(inst.trace(0))) == n_it
+
+
+def test_async_weight_sync_state_machine():
+    # NEXT-1: one update in flight; commit only at an RL-batch
+    # boundary; samples of the batch in flight keep the old version, the next
+    # batch gets the new one (staleness 1)
+    inst = Instance(workload.MODELS["tiny"], 4, 100, device=None, n_pages=50)
+    with pytest.raises(SgsError) as e:  # nothing in flight
+        inst.update_weights_commit()
+    assert e.value.code == -3
+    tr = workload.make_trace(6, 8, 10, 0.5, 10, 512, seed=3)
+    inst.submit_trace(tr)
+    inst.step()
+    inst.update_weights_begin(0)  # overlaps generation
+    with pytest.raises(SgsError) as e:  # a second update
+        inst.update_weights_begin(0)
+    assert e.value.code == -3
+    with pytest.raises(SgsError) as e:  # the synchronous path is blocked meanwhile
+        inst.update_weights(0)
+    assert e.value.code == -3
+    assert inst.update_weights_ready()
+    with pytest.raises(SgsError) as e:  # samples in flight
+        inst.update_weights_commit()
+    assert e.value.code == -3
+    done = inst.run()
+    assert {c["weight_version"] for c in done} == {0}
+    inst.update_weights_commit()
+    assert inst.weight_version() == 1
+    tr2 = workload.make_trace(3, 8, 5, 0.5, 5, 512, seed=4, id_base=100)
+    inst.submit_trace(tr2)
+    assert {c["weight_version"] for c in inst.run()} == {1}
 
 
 def test_dispatch_bit_exact_vs_oracle():
