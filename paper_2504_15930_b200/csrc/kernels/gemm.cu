@@ -429,15 +429,21 @@ static int sm_count() {
   return n[dev];
 }
 
+// Split-K factor for launches that would leave the GPU under-filled: the
+// units (tiles x splits) fill the resident slots -- 2 CTAs per SM for decode
+// tiles (BN <= 128), 1 for the 200 KB compute-bound tiles -- up to 8 splits
+// and >= 4 k-chunks per split (tools/split_sweep.py: at T <= 128, 8 splits
+// beat 5 by 8-15%; at T = 256 the red.add traffic makes ~148/tiles optimal).
 int gemm_auto_splits(int N, int K, int T) {
   const int bn = T >= 256 ? 256 : ((T + 15) / 16) * 16;
   const int tiles = (N / GEMM_BM) * ((T + bn - 1) / bn);
+  const int slots = bn <= 128 ? 2 * 148 : 148;
   const int kc = K / GEMM_BK;
-  if (tiles >= 120) return 1;
-  int s = 148 / tiles;
-  s = s < 1 ? 1 : s;
-  int maxs = kc / 4 > 0 ? kc / 4 : 1;  // keep >= 4 K chunks per split
-  return s > maxs ? maxs : s;
+  int s = slots / tiles;
+  if (s > 8) s = 8;
+  const int maxs = kc / 4 > 0 ? kc / 4 : 1;  // keep >= 4 K chunks per split
+  if (s > maxs) s = maxs;
+  return s < 1 ? 1 : s;
 }
 
 // Launch one instantiation: PDL always, plus a 2-CTA cluster for CG == 2.
