@@ -114,6 +114,11 @@ Engine::~Engine() {
       cudaStreamDestroy(st_side_);
     }
     if (ev_sync_) cudaEventDestroy(ev_sync_);
+    for (auto& v : graphs_)
+      for (auto& g : v)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto& kv : pgraphs_)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   }
 }
 
@@ -542,9 +547,8 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     meta.insert(meta.end(), p, p + n);
     return at;
   };
-  const size_t o_bt = put(plan.bt_deltas.data(), plan.bt_deltas.size());
-  const int n_bt = (int)plan.bt_deltas.size() / 3;
-  // prefill chunks
+  // prefill chunks first (their metadata offsets then depend only on the
+  // chunks, so a prefill graph can be replayed), block-table deltas after them
   struct Chunk {
     std::vector<int32_t> idx;
     int T = 0, nqb = 0, row_base = 0;
@@ -590,6 +594,8 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     c.row_base = row_base;
     row_base += (int)c.idx.size();
   }
+  const size_t o_bt = put(plan.bt_deltas.data(), plan.bt_deltas.size());
+  const int n_bt = (int)plan.bt_deltas.size() / 3;
   // ---------------- decode rows (ascending slot) -> fixed region at the start of the metadata
   const int Bpad = (e_.max_batch + 15) / 16 * 16;
   const int Bk = (n_run + 15) / 16 * 16;  // CUDA-graph bucket; rows [n_run, Bk) are inert (slot -1)
@@ -647,9 +653,43 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
 
   // ---------------- prefill
   for (auto& c : chunks) {
-    sgs_status s = prefill_chunk(c.idx, c.row_base, MD + c.o_tok, MD + c.o_pos, MD + c.o_slot, MD + c.o_offs,
-                                 MD + c.o_qb, c.nqb, MD + c.o_last, MD + c.o_pfslot, MD + c.o_pftok, c.T);
-    if (s != SGS_OK) return s;
+    auto body = [&]() {
+      return prefill_chunk(c.idx, c.row_base, MD + c.o_tok, MD + c.o_pos, MD + c.o_slot, MD + c.o_offs,
+                           MD + c.o_qb, c.nqb, MD + c.o_last, MD + c.o_pfslot, MD + c.o_pftok, c.T);
+    };
+    if ((e_.flags & SGS_F_NO_GRAPHS) || timing_now_) {
+      sgs_status s = body();
+      if (s != SGS_OK) return s;
+      continue;
+    }
+    std::vector<int64_t> key{c.row_base, (int64_t)c.o_tok, c.T, c.nqb};
+    for (int32_t i : c.idx) key.push_back(S[i].P);
+    if (pgraphs_.size() > 64 && !pgraphs_.count(key)) {  // bounded cache
+      for (auto& kv : pgraphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      pgraphs_.clear();
+    }
+    DecodeGraph& g = pgraphs_[key];
+    if (!g.exec) {
+      if (g.uses++ == 0) {  // first use eager
+        sgs_status s = body();
+        if (s != SGS_OK) return s;
+        continue;
+      }
+      const int64_t l0 = launches;
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      sgs_status s = body();
+      cudaError_t ce = cudaStreamEndCapture(st_, &graph);
+      if (s != SGS_OK) return s;
+      CK(ce, "end capture");
+      CK(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+      g.kernels = launches - l0;
+      launches = l0;
+    }
+    CK(cudaGraphLaunch(g.exec, st_), "graph launch");
+    launches += g.kernels;
   }
   // ---------------- decode (graph replay per bucket)
   if (n_run > 0) {
@@ -768,7 +808,7 @@ sgs_status Engine::decode_body(int Bk) {
     if (on(0)) CK(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm2");
     if (on(5)) CK(gate_up(Ly.wgu, Bk), "gemm gate_up + SwiGLU");
     if (on(6)) CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
-    launches += 6;
+    launches += 4;  // rmsnorm x2, RoPE, attention; the GEMMs count themselves
   }
   if (on(0)) CK(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm f");
   if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
@@ -844,7 +884,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     CK(gate_up(Ly.wgu, T), "gemm gate_up + SwiGLU");
     CK(gemm(Ly.wd, mm_, h_, d, f, T, true), "gemm down");
     CK(save(), "dump");
-    launches += 5;
+    launches += 4;  // rmsnorm x2, RoPE, attention; the GEMMs count themselves
   }
   if (only_layer >= 0) {
     if (dump) CK(cudaMemcpyAsync(dump, h_, (size_t)T * d * 4, cudaMemcpyDeviceToHost, st_), "h_out");

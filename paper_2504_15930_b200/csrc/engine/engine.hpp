@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <deque>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -114,6 +115,10 @@ class Engine {
     std::vector<KRec> recs;
   };
   std::vector<DecodeGraph> graphs_[2];  // [timed]: variant with event-record nodes
+  // prefill chunks as CUDA graphs keyed by their metadata shape (row base,
+  // offset, prompt lengths): refills of equal-length prompts replay one graph
+  // instead of ~8 eager launches per layer (untimed iterations only)
+  std::map<std::vector<int64_t>, DecodeGraph> pgraphs_;
   bool timing_now_ = false;             // this iteration is a timing sample
   int skip_ = 0;                        // SGS_DEBUG_SKIP ablation mask (decode program)
   int64_t timing_iter_ = 0;
