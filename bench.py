@@ -151,6 +151,36 @@ def cpu_oracle_sample(shape, steps=1, warmup=0, T=8):
                       f"extrapolated to {shape.n_layers} layers (fp64, OpenMP, weights regenerated per call)"}
 
 
+def batch_roofline(rows, shape, bw_gbs, tflops):
+    """Roofline time of the executed schedule: every iteration of the
+    iteration log priced at max(bytes/HBM, flops/bf16) per GEMM, plus the KV bytes
+    of decode attention and the causal flops of prefill attention.  Prefill and
+    decode rows of a mixed iteration are separate passes, as executed.  Rows:
+    (t, b, admitted, prefill tokens, sum ctx, device us)."""
+    L, d, nq, nkv, hd, f, V = (shape.n_layers, shape.d_model, shape.n_q_heads, shape.n_kv_heads, shape.head_dim,
+                               shape.d_ffn, shape.vocab)
+    BW, F = bw_gbs * 1e9, tflops * 1e12
+    gemms = [((nq + 2 * nkv) * hd, d), (d, nq * hd), (2 * f, d), (d, f)]
+
+    def gemm_t(T):
+        return L * sum(max(N * K * 2 / BW, 2.0 * N * K * T / F) for N, K in gemms) + \
+            max(V * d * 2 / BW, 2.0 * V * d * min(T, 1 << 30) / F)
+
+    kv_bytes_per_token = 2 * nkv * hd * 2 * L
+    total = 0.0
+    for _t, b, adm, pf, sumctx, _us in rows:
+        dec = b - adm
+        if pf > 0 and adm > 0:
+            lp = pf / adm
+            attn = adm * 4.0 * nq * hd * (lp * (lp + 1) / 2) * L
+            # prefill GEMMs over the prompt tokens; the LM head only for the last token of each prompt
+            total += L * sum(max(N * K * 2 / BW, 2.0 * N * K * pf / F) for N, K in gemms) + attn / F + \
+                max(V * d * 2 / BW, 2.0 * V * d * adm / F)
+        if dec > 0:
+            total += gemm_t(dec) + (sumctx - pf) * kv_bytes_per_token / BW
+    return total
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -256,6 +286,7 @@ def main():
         pg.barrier()
     torch.cuda.synchronize()
     results = []
+    log0 = len(inst.iter_log())
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             results.append(one_step(args.warmup + k))
@@ -267,6 +298,7 @@ def main():
     wall_s = sum(r["wall_s"] for r in results)
     tokens = sum(r["tokens"] for r in results)
     stats = {cls: inst.kernel_stats(cls) for cls in range(4)}
+    timed_rows = inst.iter_log()[log0:]
     if args.iter_log and rank == 0:
         np.save(args.iter_log, inst.iter_log())
     if pg:
@@ -280,6 +312,14 @@ def main():
         pg.destroy_process_group()
         return
     peaks = load_peaks()
+    # whole-step roofline of this rank's executed schedule, vs its measured device time
+    t_roof = batch_roofline(timed_rows, shape, peaks["hbm_gbs"], peaks["bf16_tflops_sustained"])
+    t_meas = float(sum(r[5] for r in timed_rows)) / 1e6
+    batch_roof = {"roofline_s": round(t_roof, 3), "measured_s": round(t_meas, 3),
+                  "frac": round(t_roof / t_meas, 4) if t_meas > 0 else None,
+                  "definition": "sum over the executed iterations of (per GEMM max(weight bytes/HBM, "
+                                "flops/bf16 sustained) + KV bytes/HBM + prefill attention flops/bf16); "
+                                "measured = sum of the iterations' device time (this rank)"}
     roof, other = None, None
     if stats[3]["ms"] > 0:
         # per-kernel CUDA events are recorded on a 1-in-32 sample of the timed
@@ -336,6 +376,7 @@ def main():
                 "d2h_bytes_per_step": int(statistics.mean(r["d2h"] for r in results))},
         "gpu_launches": int(sum(r["launches"] for r in results)),
         "roofline": roof,
+        "batch_roofline": batch_roof,
         "kernels": other,
         "clocks": clk.summary(),
     }
