@@ -58,6 +58,16 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->off_ao = take(tmax * nq * hd * 2);
   L->off_gu = take(tmax * 2 * f * 4);
   L->off_mm = take(tmax * f * 2);
+  {
+    const int64_t Bp = (B + 15) / 16 * 16;
+    L->off_dh = take(Bp * d * 4);
+    L->off_dx = take(Bp * d * 2);
+    L->off_dqkv = take(Bp * (nq + 2 * nkv) * hd * 4);
+    L->off_dq = take(Bp * nq * hd * 2);
+    L->off_dao = take(Bp * nq * hd * 2);
+    L->off_dgu = take(Bp * 2 * f * 4);
+    L->off_dmm = take(Bp * f * 2);
+  }
   // decode rows [0, Bpad) (CUDA-graph buckets pad to 16), prefill rows after them
   const int64_t Bpad = (B + 15) / 16 * 16;
   L->off_logits = take((Bpad + B) * V * 4);
@@ -114,6 +124,12 @@ Engine::~Engine() {
       cudaStreamDestroy(st_side_);
     }
     if (ev_sync_) cudaEventDestroy(ev_sync_);
+    if (st_pf_) {
+      cudaStreamSynchronize(st_pf_);
+      cudaStreamDestroy(st_pf_);
+    }
+    if (ev_meta_) cudaEventDestroy(ev_meta_);
+    if (ev_pf_) cudaEventDestroy(ev_pf_);
     for (auto& v : graphs_)
       for (auto& g : v)
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -229,6 +245,13 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   gu_ = reinterpret_cast<float*>(arena_ + L_.off_gu);
   mm_ = arena_ + L_.off_mm;
   logits_ = reinterpret_cast<float*>(arena_ + L_.off_logits);
+  dset_.h = reinterpret_cast<float*>(arena_ + L_.off_dh);
+  dset_.x = arena_ + L_.off_dx;
+  dset_.qkv = reinterpret_cast<float*>(arena_ + L_.off_dqkv);
+  dset_.q = arena_ + L_.off_dq;
+  dset_.ao = arena_ + L_.off_dao;
+  dset_.gu = reinterpret_cast<float*>(arena_ + L_.off_dgu);
+  dset_.mm = arena_ + L_.off_dmm;
   rope_ = reinterpret_cast<float*>(arena_ + L_.off_rope);
   bt_ = reinterpret_cast<int32_t*>(arena_ + L_.off_bt);
   last_tok_ = reinterpret_cast<int32_t*>(arena_ + L_.off_last);
@@ -252,6 +275,10 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   CK(cudaMemsetAsync(last_tok_, 0, (size_t)e.max_batch * 4, st_), "memset last");
   // split-K accumulators (kept zeroed by their consumers) and the residual scratch
   CK(cudaMemsetAsync(arena_ + L_.off_h, 0, L_.off_mm - L_.off_h, st_), "memset scratch");
+  CK(cudaMemsetAsync(arena_ + L_.off_dh, 0, L_.off_dmm - L_.off_dh, st_), "memset decode scratch");
+  CK(cudaStreamCreateWithFlags(&st_pf_, cudaStreamNonBlocking), "prefill stream");
+  CK(cudaEventCreateWithFlags(&ev_meta_, cudaEventDisableTiming), "event");
+  CK(cudaEventCreateWithFlags(&ev_pf_, cudaEventDisableTiming), "event");
   CK(cudaMemsetAsync(attn_ws_, 0, L_.attn_bytes, st_), "memset attention workspace");
   // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
   {
@@ -651,7 +678,14 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   CK(apply_bt_deltas(bt_, L_.max_pages, MD + o_bt, n_bt, st_), "bt deltas");
   ++launches;
 
-  // ---------------- prefill
+  // ---------------- prefill: on its own stream and scratch, concurrent with the decode graph
+  // (disjoint rows, slots and pages); sequential in timed / graph-less iterations
+  const bool concurrent = !chunks.empty() && n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && !timing_now_;
+  if (concurrent) {
+    CK(cudaEventRecord(ev_meta_, st_), "event");
+    CK(cudaStreamWaitEvent(st_pf_, ev_meta_, 0), "wait meta");
+    std::swap(st_, st_pf_);
+  }
   for (auto& c : chunks) {
     auto body = [&]() {
       return prefill_chunk(c.idx, c.row_base, MD + c.o_tok, MD + c.o_pos, MD + c.o_slot, MD + c.o_offs,
@@ -691,11 +725,16 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     CK(cudaGraphLaunch(g.exec, st_), "graph launch");
     launches += g.kernels;
   }
+  if (concurrent) {
+    std::swap(st_, st_pf_);
+    CK(cudaEventRecord(ev_pf_, st_pf_), "event");
+  }
   // ---------------- decode (graph replay per bucket)
   if (n_run > 0) {
     sgs_status s = run_decode(n_run);
     if (s != SGS_OK) return s;
   }
+  if (concurrent) CK(cudaStreamWaitEvent(st_, ev_pf_, 0), "join prefill");
   // ---------------- completions: D2H of their tokens
   int64_t off = 0;
   std::vector<int64_t> toff;
@@ -817,7 +856,25 @@ sgs_status Engine::decode_body(int Bk) {
   return SGS_OK;
 }
 
+void Engine::swap_scratch() {
+  std::swap(h_, dset_.h);
+  std::swap(qkv_, dset_.qkv);
+  std::swap(gu_, dset_.gu);
+  std::swap(x_, dset_.x);
+  std::swap(q_, dset_.q);
+  std::swap(ao_, dset_.ao);
+  std::swap(mm_, dset_.mm);
+}
+
 sgs_status Engine::run_decode(int b) {
+  // the decode program always runs on the decode scratch set (graphs capture its pointers)
+  swap_scratch();
+  const sgs_status s = run_decode_body(b);
+  swap_scratch();
+  return s;
+}
+
+sgs_status Engine::run_decode_body(int b) {
   const int Bk = (b + 15) / 16 * 16;
   if (e_.flags & SGS_F_NO_GRAPHS) return decode_body(Bk);
   auto& gs = graphs_[timing_now_ ? 1 : 0];

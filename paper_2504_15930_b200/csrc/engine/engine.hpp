@@ -30,6 +30,8 @@ struct ArenaLayout {
   int64_t off_kv = 0, off_h = 0, off_x = 0, off_qkv = 0, off_q = 0, off_kc = 0, off_vc = 0, off_ao = 0,
           off_gu = 0, off_mm = 0, off_logits = 0, off_rope = 0, off_bt = 0, off_last = 0, off_hist = 0,
           off_meta = 0, off_attn = 0, off_cksum = 0, off_shadow = -1;
+  // decode scratch (Bpad rows), separate from the prefill scratch so the two run concurrently
+  int64_t off_dh = 0, off_dx = 0, off_dqkv = 0, off_dq = 0, off_dao = 0, off_dgu = 0, off_dmm = 0;
   int64_t meta_bytes = 0, attn_bytes = 0, meta_dec_bytes = 0;
   int tmax = 0, max_pages = 0, max_items = 0;
 };
@@ -127,6 +129,7 @@ class Engine {
   double cur_attn_bytes_ = 0, cur_attn_flops_ = 0;
   sgs_status decode_body(int Bk);
   sgs_status run_decode(int b);
+  sgs_status run_decode_body(int b);
 
   sgs_model_cfg m_{};
   sgs_engine_cfg e_{};
@@ -146,6 +149,14 @@ class Engine {
   std::vector<TensorRef> tensors_;
   // scratch
   float *h_ = nullptr, *qkv_ = nullptr, *gu_ = nullptr, *logits_ = nullptr, *rope_ = nullptr;
+  // the decode scratch set, swapped into h_/x_/qkv_/q_/ao_/gu_/mm_ while the decode program is built
+  struct ScratchSet {
+    float *h, *qkv, *gu;
+    void *x, *q, *ao, *mm;
+  } dset_{};
+  void swap_scratch();
+  cudaStream_t st_pf_ = nullptr;                     // prefill chunks, concurrent with the decode graph
+  cudaEvent_t ev_meta_ = nullptr, ev_pf_ = nullptr;  // metadata ready / prefill done
   void *x_ = nullptr, *q_ = nullptr, *kc_ = nullptr, *vc_ = nullptr, *ao_ = nullptr, *mm_ = nullptr;
   int32_t *bt_ = nullptr, *last_tok_ = nullptr, *hist_ = nullptr;
   uint8_t* meta_dev_ = nullptr;
