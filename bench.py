@@ -31,13 +31,12 @@ import workload  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 # T(b) profiles (t0_ns, k0_ps, b_star, k1_ps) used by Alg. 2's Eq. 2; fitted by tools/tb_sweep.py
-# (config 5) on B200 — profiles/r01_tb_sweep_7b.json and r01_tb_sweep_14b.json (the ctx=2048 fits);
-# 32B is the 14B fit scaled by the weight-byte ratio (x2.2) until its own sweep lands.  Only the
+# (config 5) on B200 — profiles/r01_tb_sweep_{7b,14b,32b}.json (the ctx=2048 fits).  Only the
 # dispatch (N > 1) reads them.
 DEFAULT_PROFILES = {
     "qwen2.5-7b": (3491220, 29544576, 128, 38479949),
     "qwen2.5-14b": (5987575, 73237116, 160, 71301394),
-    "qwen2.5-32b": (13172665, 161121655, 160, 156863067),
+    "qwen2.5-32b": (11988370, 88930482, 32, 107212340),
     "tiny": (200, 100, 64, 400),
 }
 
