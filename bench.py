@@ -340,7 +340,12 @@ def main():
             achieved, peak, unit = st["flops"] / (st["ms"] / 1e3) / 1e12, peaks["bf16_tflops_sustained"], "TFLOP/s"
         roof = {"kernel": names[dom], "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                 "frac": round(frac, 4), "frac_definition": "sum over timed launches of max(bytes/HBM, flops/bf16 "
-                "sustained) / measured time", "traffic": None, "peak_source": peaks["_source"],
+                "sustained) / measured time", "traffic": None,
+                "traffic_source": "per-shape ncu --set full captures in profiles/r01c_ncu_full_summary.csv "
+                                  "(one number for the mixed-shape GEMM class would not be per launch): decode "
+                                  "GEMMs read their algorithmic bytes within 3% (O-proj split-K +13%); the "
+                                  "prefill gate_up at T=8192 reads its weights ~3.4x (1.13 GB vs 0.33 GB) while "
+                                  "tensor-bound at 1.43 PF/s", "peak_source": peaks["_source"],
                 "launches_sampled": st["launches"], "share_of_step": round(st["ms"] / stats[3]["ms"], 4),
                 "timing": "CUDA events on the engine stream, 1 in 32 iterations of the timed region"}
         other = {("decode_attention" if c == 0 else "gemm" if c == 1 else "prefill_attention"):
