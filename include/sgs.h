@@ -133,13 +133,20 @@ sgs_status sgs_submit(sgs_handle* h, const sgs_prompt* prompts, int32_t n, const
 
 /* Run one continuous-batching iteration (longest-first refill under B,
  * P:996-998; prefill of admitted prompts + one decode step of the running
- * samples) and return the samples that completed in it, ascending id.  With
- * nothing queued or active: SGS_OK, *n_out = 0, no iteration is counted.
- * Completions beyond cap stay queued and are returned (before any new
- * iteration) by the next call. */
+ * samples) and return completed samples, ascending id within an iteration.
+ * The device work is pipelined with the host: a call launches its iteration
+ * and then waits for the previous call's iteration, returning that one's
+ * completions (a call with nothing new to launch drains the last one); with
+ * SGS_F_KEEP_LOGITS every call returns its own iteration's completions.  With
+ * nothing queued, active or in flight: SGS_OK, *n_out = 0, no iteration is
+ * counted.  Completions beyond cap stay queued and are returned (before any
+ * new iteration) by the next call. */
 sgs_status sgs_step(sgs_handle* h, sgs_completion* out, int32_t cap, int32_t* n_out);
 
-/* Samples queued + active on this instance. */
+/* Samples queued + active on this instance; active includes samples whose last
+ * iteration is launched but not yet returned (sgs_step pipelines: it launches
+ * iteration i+1 before waiting for iteration i, so a call returns the
+ * completions of the previous iteration). */
 sgs_status sgs_pending(const sgs_handle* h, int64_t* queued, int64_t* active);
 
 /* Weight sync: the only collective.  sgs_comm_unique_id on the

@@ -62,7 +62,8 @@ sgs_status sgs_step(sgs_handle* h, sgs_completion* out, int32_t cap, int32_t* n_
 sgs_status sgs_pending(const sgs_handle* h, int64_t* queued, int64_t* active) {
   if (!h) return SGS_E_INVAL;
   if (queued) *queued = h->eng.sched.queued();
-  if (active) *active = h->eng.sched.active();
+  // samples whose iteration is launched but not yet waited for count as active
+  if (active) *active = h->eng.sched.active() + h->eng.inflight_samples();
   return SGS_OK;
 }
 

@@ -115,10 +115,12 @@ sgs_status Engine::cuda_fail(cudaError_t e, const char* what) {
 Engine::~Engine() {
   if (!null_) {
     if (st_) cudaStreamSynchronize(st_);
-    if (meta_host_) cudaFreeHost(meta_host_);
-    if (tok_host_) cudaFreeHost(tok_host_);
-    if (ev0_) cudaEventDestroy(ev0_);
-    if (ev1_) cudaEventDestroy(ev1_);
+    for (int k = 0; k < 2; ++k) {
+      if (meta_bufs_[k]) cudaFreeHost(meta_bufs_[k]);
+      if (tok_bufs_[k]) cudaFreeHost(tok_bufs_[k]);
+      if (ev0s_[k]) cudaEventDestroy(ev0s_[k]);
+      if (ev1s_[k]) cudaEventDestroy(ev1s_[k]);
+    }
     if (st_side_) {
       cudaStreamSynchronize(st_side_);
       cudaStreamDestroy(st_side_);
@@ -259,11 +261,14 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   meta_dev_ = arena_ + L_.off_meta;
   attn_ws_ = arena_ + L_.off_attn;
   cksum_dev_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_cksum);
-  CK(cudaMallocHost(&meta_host_, L_.meta_bytes), "cudaMallocHost(meta)");
   tok_host_cap_ = (int64_t)e.max_batch * max_gen_;
-  CK(cudaMallocHost(&tok_host_, tok_host_cap_ * 4), "cudaMallocHost(tokens)");
-  CK(cudaEventCreate(&ev0_), "event");
-  CK(cudaEventCreate(&ev1_), "event");
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaMallocHost(&meta_bufs_[k], L_.meta_bytes), "cudaMallocHost(meta)");
+    CK(cudaMallocHost(&tok_bufs_[k], tok_host_cap_ * 4), "cudaMallocHost(tokens)");
+    CK(cudaEventCreate(&ev0s_[k]), "event");
+    CK(cudaEventCreate(&ev1s_[k]), "event");
+  }
+  meta_host_ = meta_bufs_[0], tok_host_ = tok_bufs_[0], ev0_ = ev0s_[0], ev1_ = ev1s_[0];
   if (L_.off_shadow >= 0) {
     shadow_ = arena_ + L_.off_shadow;
     CK(cudaStreamCreateWithFlags(&st_side_, cudaStreamNonBlocking), "side stream");
@@ -418,7 +423,13 @@ sgs_status Engine::step(sgs_completion* out, int32_t cap, int32_t* n_out) {
       return SGS_E_STATE;
     }
     if (ran) {
-      sgs_status s = run_iteration(plan);
+      sgs_status s = run_iteration(plan);  // launches; finalizes it too unless pipelined
+      if (s != SGS_OK) return s;
+    }
+    // the previous iteration (launched by the last call) is waited for only now,
+    // while the GPU already runs this one; with nothing new to run, drain
+    while (infl_.size() > (ran ? 1u : 0u)) {
+      sgs_status s = finalize_front();
       if (s != SGS_OK) return s;
     }
   }
@@ -566,6 +577,10 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   // per-kernel CUDA events on 1 in kTimingStride iterations: events between
   // kernels serialise them (no PDL overlap), so the others run untouched
   timing_now_ = (e_.flags & SGS_F_KERNEL_TIMING) && (timing_iter_++ % kTimingStride == 0);
+  // staging buffers and events of this iteration (the other pair may still be in flight)
+  cur_buf_ ^= 1;
+  meta_host_ = meta_bufs_[cur_buf_], tok_host_ = tok_bufs_[cur_buf_];
+  ev0_ = ev0s_[cur_buf_], ev1_ = ev1s_[cur_buf_];
   // ---------------- stage metadata (host, pinned) -> one H2D copy
   std::vector<int32_t> meta;
   meta.reserve(4096);
@@ -771,32 +786,52 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     for (int32_t i : plan.running) kept_ids_.push_back(S[i].id), kept_tok_.push_back(S[i].produced - 1);
   }
   CK(cudaEventRecord(ev1_, st_), "event");
-  CK(cudaStreamSynchronize(st_), "iteration sync");
-  CK(cudaEventElapsedTime(&last_ms, ev0_, ev1_), "elapsed");
-  CK(kflush(krec_, n_run), "kernel timing");
-  krec_.clear();
-  ev_used_ = 0;
-  if (n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && timing_now_) {
-    const DecodeGraph& g = graphs_[1][(n_run + 15) / 16];
-    if (g.exec) CK(kflush(g.recs, n_run), "kernel timing");
+  Inflight fl;
+  fl.buf = cur_buf_;
+  fl.t = plan.t, fl.b = plan.b, fl.adm = n_adm, fl.sumctx = plan.sumctx, fl.n_run = n_run, fl.timing = timing_now_;
+  for (auto& c : chunks) fl.pf_tok += c.T;
+  for (int32_t i : plan.completed) {
+    const Sample& s = S[i];
+    fl.comps.push_back(Completion{s.id, s.slot, s.admit_iter, s.finish_iter, version, std::vector<int32_t>(s.d)});
   }
-  if (timing_now_) {  // slot 3: device time of the sampled iterations (for the kernel shares)
-    kstat_ms[3] += last_ms;
+  fl.toff = std::move(toff);
+  infl_.push_back(std::move(fl));
+  // kernel-timing samples and logit capture need this iteration's results now
+  if (timing_now_ || (e_.flags & SGS_F_KEEP_LOGITS)) return drain();
+  return SGS_OK;
+}
+
+sgs_status Engine::finalize_front() {
+  Inflight& f = infl_.front();
+  CK(cudaEventSynchronize(ev1s_[f.buf]), "iteration sync");
+  CK(cudaEventElapsedTime(&last_ms, ev0s_[f.buf], ev1s_[f.buf]), "elapsed");
+  if (f.timing) {
+    CK(kflush(krec_, f.n_run), "kernel timing");
+    krec_.clear();
+    ev_used_ = 0;
+    if (f.n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS)) {
+      const DecodeGraph& g = graphs_[1][(f.n_run + 15) / 16];
+      if (g.exec) CK(kflush(g.recs, f.n_run), "kernel timing");
+    }
+    kstat_ms[3] += last_ms;  // slot 3: device time of the sampled iterations (for the kernel shares)
     kstat_n[3] += 1;
   }
-  {
-    int64_t pf_tok = 0;
-    for (auto& c : chunks) pf_tok += c.T;
-    iter_log.insert(iter_log.end(), {plan.t, (int64_t)plan.b, (int64_t)n_adm, pf_tok, plan.sumctx,
-                                     (int64_t)std::llround(last_ms * 1000.0)});
-  }
-  for (size_t k = 0; k < plan.completed.size(); ++k) {
-    const Sample& s = S[plan.completed[k]];
-    Completion c{s.id, s.slot, s.admit_iter, s.finish_iter, version,
-                 std::vector<int32_t>(tok_host_ + toff[k], tok_host_ + toff[k] + s.d)};
+  iter_log.insert(iter_log.end(), {f.t, f.b, f.adm, f.pf_tok, f.sumctx, (int64_t)std::llround(last_ms * 1000.0)});
+  const int32_t* tok = tok_bufs_[f.buf];
+  for (size_t k = 0; k < f.comps.size(); ++k) {
+    Completion& c = f.comps[k];
+    std::copy(tok + f.toff[k], tok + f.toff[k] + c.tokens.size(), c.tokens.begin());
     ready_.push_back(std::move(c));
   }
-  (void)n_adm;
+  infl_.pop_front();
+  return SGS_OK;
+}
+
+sgs_status Engine::drain() {
+  while (!infl_.empty()) {
+    sgs_status s = finalize_front();
+    if (s != SGS_OK) return s;
+  }
   return SGS_OK;
 }
 
@@ -968,6 +1003,10 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, 
     err = "debug_forward needs a device handle with nothing in flight";
     return SGS_E_STATE;
   }
+  {
+    sgs_status ds = drain();
+    if (ds != SGS_OK) return ds;
+  }
   const int np = (T + e_.page_size - 1) / e_.page_size;
   if (T < 1 || T > e_.max_prefill_tokens || np > n_pages_ || np > L_.max_pages) {
     err = "debug_forward: prompt too long";
@@ -1069,6 +1108,10 @@ sgs_status Engine::update_weights(int root) {
   if (poisoned) {
     err = "handle poisoned";
     return SGS_E_STATE;
+  }
+  if (sched.idle()) {
+    sgs_status ds = drain();  // the last launched iteration finishes on the old weights
+    if (ds != SGS_OK) return ds;
   }
   if (!sched.idle()) {
     err = "weight update with samples in flight";
@@ -1211,6 +1254,10 @@ sgs_status Engine::update_weights_commit() {
   if (!sync_pending_) {
     err = "no weight update in flight";
     return SGS_E_STATE;
+  }
+  if (sched.idle()) {
+    sgs_status ds = drain();
+    if (ds != SGS_OK) return ds;
   }
   if (!sched.idle()) {
     err = "weight commit with samples in flight (the swap happens at an RL-batch boundary)";

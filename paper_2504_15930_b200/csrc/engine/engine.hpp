@@ -160,12 +160,38 @@ class Engine {
   void *x_ = nullptr, *q_ = nullptr, *kc_ = nullptr, *vc_ = nullptr, *ao_ = nullptr, *mm_ = nullptr;
   int32_t *bt_ = nullptr, *last_tok_ = nullptr, *hist_ = nullptr;
   uint8_t* meta_dev_ = nullptr;
-  uint8_t* meta_host_ = nullptr;  // pinned
+  uint8_t* meta_host_ = nullptr;  // pinned (the current one of meta_bufs_)
   uint8_t* attn_ws_ = nullptr;
   unsigned long long* cksum_dev_ = nullptr;
-  int32_t* tok_host_ = nullptr;  // pinned, completed tokens
+  int32_t* tok_host_ = nullptr;  // pinned, completed tokens (the current one of tok_bufs_)
   int64_t tok_host_cap_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  // Host/device pipelining: iteration i+1 is planned and launched before
+  // iteration i is waited for, so the GPU never idles on host work; each
+  // in-flight iteration owns one of two pinned staging/token buffers and event
+  // pairs.  Off with SGS_F_KEEP_LOGITS and on kernel-timing samples.
+  struct Inflight {
+    int buf = 0;
+    int64_t t = 0, b = 0, adm = 0, pf_tok = 0, sumctx = 0;
+    int n_run = 0;
+    bool timing = false;
+    std::vector<Completion> comps;  // tokens filled when finalized
+    std::vector<int64_t> toff;
+  };
+  std::deque<Inflight> infl_;
+  uint8_t* meta_bufs_[2] = {nullptr, nullptr};
+  int32_t* tok_bufs_[2] = {nullptr, nullptr};
+  cudaEvent_t ev0s_[2] = {nullptr, nullptr}, ev1s_[2] = {nullptr, nullptr};
+  int cur_buf_ = 0;
+  sgs_status finalize_front();
+ public:
+  sgs_status drain();  // finalize every in-flight iteration (before weight updates, debug calls, ...)
+  int64_t inflight_samples() const {
+    int64_t n = 0;
+    for (const auto& f : infl_) n += (int64_t)f.comps.size();
+    return n;
+  }
+ private:
   uint8_t* shadow_ = nullptr;           // second weight buffer (SGS_F_SHADOW_WEIGHTS)
   cudaStream_t st_side_ = nullptr;      // weight staging + broadcast, concurrent with generation
   cudaEvent_t ev_sync_ = nullptr;       // end of the in-flight broadcast on st_side_
