@@ -702,6 +702,12 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     std::swap(st_, st_pf_);
   }
   for (auto& c : chunks) {
+    {
+      // causal self-attention of whole prompts: QK^T and PV over P(P+1)/2 pairs each
+      double pairs = 0;
+      for (int32_t i : c.idx) pairs += 0.5 * (double)S[i].P * (S[i].P + 1);
+      cur_pf_attn_flops_ = 4.0 * nq * hd * pairs;
+    }
     auto body = [&]() {
       return prefill_chunk(c.idx, c.row_base, MD + c.o_tok, MD + c.o_pos, MD + c.o_slot, MD + c.o_offs,
                            MD + c.o_qb, c.nqb, MD + c.o_last, MD + c.o_pfslot, MD + c.o_pftok, c.T);
@@ -969,7 +975,8 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     KRec kr;
     ktic(&kr, 2);
     CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
-    ktoc(&kr, 0.0, 0.0, 0.0, T);
+    // algorithmic bytes: q, k, v in and o out once per row (bf16); flops from the chunk's prompts
+    ktoc(&kr, 0.0, 2.0 * hd * (2.0 * nq + 2.0 * nkv), cur_pf_attn_flops_ / std::max(T, 1), T);
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
     CK(save(), "dump");
     CK(rmsnorm(h_, Ly.n2, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm2");
@@ -1032,6 +1039,7 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, 
   CK(cudaMemcpyAsync(meta_dev_, meta_host_, meta.size() * 4, cudaMemcpyHostToDevice, st_), "meta");
   CK(apply_bt_deltas(bt_, L_.max_pages, MD, np, st_), "bt");
   std::vector<int32_t> idx(1, 0);
+  cur_pf_attn_flops_ = 2.0 * m_.n_q_heads * m_.head_dim * (double)T * (T + 1);
   sgs_status s = prefill_chunk(idx, 0, MD + o_tok, MD + o_pos, MD + o_slot, MD + o_offs, MD + o_qb, (T + 63) / 64,
                                MD + o_last, MD + o_last + 1, MD + o_last + 2, T, dump, layer, h_in);
   if (s != SGS_OK) return s;

@@ -127,6 +127,7 @@ class Engine {
   static constexpr int kTimingStride = 32;  // 1 in 32 iterations carries the per-kernel events
   std::vector<KRec>* rec_target_ = nullptr;  // non-null while capturing
   double cur_attn_bytes_ = 0, cur_attn_flops_ = 0;
+  double cur_pf_attn_flops_ = 0;  // causal attention flops of the prefill chunk being issued
   sgs_status decode_body(int Bk);
   sgs_status run_decode(int b);
   sgs_status run_decode_body(int b);
