@@ -27,7 +27,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // G query heads that read them (GQA).  Key/value tiles of 64 tokens are
 // double-buffered with cp.async (zero-filled past the prompt end).
 template <int HD>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                         const __nv_bfloat16* __restrict__ v, const int32_t* __restrict__ offs,
                         const int32_t* __restrict__ qblocks, int nq, int nkv, float scale_log2,

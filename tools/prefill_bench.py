@@ -20,11 +20,11 @@ k = torch.randn(T, nkv, hd, device="cuda").bfloat16()
 v = torch.randn(T, nkv, hd, device="cuda").bfloat16()
 offs = torch.arange(0, T + 1, L, dtype=torch.int32, device="cuda")
 out = torch.empty_like(q)
-for _ in range(3):
+for _ in range(10):
     sgs.op_prefill_attention(q, k, v, offs, out)
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-reps = 10
+reps = 50
 a.record()
 for _ in range(reps):
     sgs.op_prefill_attention(q, k, v, offs, out)
