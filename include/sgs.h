@@ -64,7 +64,9 @@ enum {
   SGS_F_KEEP_LOGITS = 1,     /* keep fp32 logits of the last iteration (teacher-forcing tests) */
   SGS_F_NO_GRAPHS = 2,       /* launch the decode iteration eagerly (no CUDA graphs) */
   SGS_F_KERNEL_TIMING = 4,   /* CUDA-event timing per kernel class (sgs_kernel_stats) */
-  SGS_F_SHADOW_WEIGHTS = 8   /* reserve a second weight buffer for the asynchronous weight sync */
+  SGS_F_SHADOW_WEIGHTS = 8,  /* reserve a second weight buffer for the asynchronous weight sync */
+  SGS_F_TRACE = 16           /* keep the schedule trace (sgs_trace) and every sample record; off by
+                                default: without it the host state is bounded by the samples in flight */
 };
 
 typedef struct {
@@ -115,9 +117,36 @@ typedef struct {
 sgs_status sgs_arena_bytes(const sgs_model_cfg* m, const sgs_engine_cfg* e, int64_t n_pages,
                            int64_t* fixed_bytes, int64_t* kv_page_bytes);
 
+/* Weights in the canonical tensor order: index 0 embed [V, d],
+ * 1 lm_head [V, d], 2 final norm [d]; then per layer l, at 3 + 12 l:
+ * +0 Wq [nq hd, d], +1 Wk [nkv hd, d], +2 Wv [nkv hd, d], +3 bq [nq hd],
+ * +4 bk [nkv hd], +5 bv [nkv hd], +6 Wo [d, nq hd], +7 Wgate [f, d],
+ * +8 Wup [f, d], +9 Wdown [d, f], +10 attention norm [d], +11 MLP norm [d].
+ * Every tensor is bf16, row-major in that logical shape (a PyTorch
+ * Linear.weight is [out, in]).  ptrs[i] may be host or device memory (CUDA
+ * unified addressing decides the copy direction); the library copies the
+ * values into its own layout (gate/up interleaved in 64-row blocks) before
+ * the call returns, so the caller keeps ownership.  sgs_weight_tensors lists
+ * the order, logical ids and shapes. */
+typedef struct {
+  const void* const* ptrs;   /* n pointers, canonical order */
+  int32_t n;                 /* 3 + 12 * n_layers */
+} sgs_weights;
+
+/* Canonical weight order of a model: for i < *n (<= cap): ids[i] = the
+ * logical tensor id (0, 1, 2, 16 + 16 l + k: the ids sgs_weight_checksum
+ * takes), rows[i] x cols[i] = its shape (cols = 1 for vectors).  Any output
+ * pointer may be NULL. */
+sgs_status sgs_weight_tensors(const sgs_model_cfg* m, int64_t* ids, int64_t* rows, int64_t* cols, int32_t cap,
+                              int32_t* n);
+
 /* Create an instance.  weights == NULL: hash-initialise every tensor on the
- * device from e->weight_seed.  Null-device mode ignores arena. */
-sgs_status sgs_init(const sgs_model_cfg* m, const sgs_engine_cfg* e, sgs_handle** out);
+ * device from e->weight_seed; otherwise copy the caller's
+ * weights (SGS_E_INVAL if weights->n or a pointer is wrong).  Null-device
+ * mode ignores arena and weights.  Shapes the sm_100a kernels cannot run
+ * (page != 16, head_dim not in {32, 64, 128}, GQA group nq/nkv > 8, model
+ * dims not multiples of 128) fail here with SGS_E_UNSUPPORTED. */
+sgs_status sgs_init(const sgs_model_cfg* m, const sgs_engine_cfg* e, const sgs_weights* weights, sgs_handle** out);
 void sgs_destroy(sgs_handle* h);
 const char* sgs_last_error(const sgs_handle* h); /* h may be NULL (init errors) */
 
@@ -125,7 +154,9 @@ const char* sgs_last_error(const sgs_handle* h); /* h may be NULL (init errors) 
  * output lengths.  Every instance receives the SAME full batch;
  * Alg. 2 runs identically on each and the handle keeps the samples
  * dispatched to its instance_rank (no communication).  Validation: P >= 1,
- * hint >= 1, forced >= 1, tokens in [0, vocab), unique ids; violations ->
+ * hint >= 1, forced >= 1, tokens in [0, vocab), ids unique within the batch
+ * and among the samples still queued or active on this handle (DESIGN.md
+ * R22: an id may be reused once its sample has completed); violations ->
  * SGS_E_INVAL with no effect; a sample that can never fit -> SGS_E_CAPACITY.
  * n_mine (optional) receives how many samples this instance kept. */
 sgs_status sgs_submit(sgs_handle* h, const sgs_prompt* prompts, int32_t n, const int32_t* output_len_hint,
@@ -149,14 +180,24 @@ sgs_status sgs_step(sgs_handle* h, sgs_completion* out, int32_t cap, int32_t* n_
  * completions of the previous iteration). */
 sgs_status sgs_pending(const sgs_handle* h, int64_t* queued, int64_t* active);
 
-/* Weight sync: the only collective.  sgs_comm_unique_id on the
- * root, share the 128 bytes (e.g. torch.distributed), sgs_comm_init on every
- * rank, then sgs_update_weights broadcasts the root's weights to all ranks
- * (ncclBroadcast over NVLink) and increments the weight version.  Requires no
+/* Host-side state of the handle: sample records held, scheduler queue
+ * entries held (consumed prefix included until compacted), and ids reserved
+ * (queued or active).  Without SGS_F_TRACE all three stay bounded by the
+ * samples in flight plus one batch, however many batches are served. */
+sgs_status sgs_host_state(const sgs_handle* h, int64_t* records, int64_t* queue_entries, int64_t* live_ids);
+
+/* Weight sync (SGS "update(weights)" P:595-596): the only
+ * collective.  sgs_comm_unique_id on the root, share the 128 bytes (e.g.
+ * torch.distributed), sgs_comm_init on every rank, then sgs_update_weights
+ * on every rank: the root first copies src (the trainer's new weights,
+ * canonical order, host or device; NULL = keep the root's current weights)
+ * into its arena, then the root's weights are broadcast to all ranks
+ * (ncclBroadcast over NVLink; at world size 1 the copy alone) and the weight
+ * version increments.  Non-root ranks must pass src = NULL.  Requires no
  * sample in flight (SGS_E_STATE otherwise). */
 sgs_status sgs_comm_unique_id(uint8_t out[128]);
 sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int32_t world);
-sgs_status sgs_update_weights(sgs_handle* h, int32_t root);
+sgs_status sgs_update_weights(sgs_handle* h, const sgs_weights* src, int32_t root);
 /* Trainer proxy: regenerate this handle's weights from a new seed on device
  * (the root does this before sgs_update_weights). */
 sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed);
@@ -172,9 +213,17 @@ sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed);
  * broadcast, copies shadow -> active on the device and increments the
  * version, so the samples of the next batch are generated with the new
  * weights and stamped with the new version.  One update may be in flight
- * (SGS_E_STATE for a second begin or a stage during it). */
+ * (SGS_E_STATE for a second begin or a stage during it).  Ordering: staging
+ * and the broadcast run on the library's side stream, which waits for the
+ * previous commit's shadow -> active copy, so a stage or begin may follow a
+ * commit immediately; a caller that writes the shadow buffer directly
+ * (through sgs_shadow_weights) must first synchronise the handle's stream
+ * after a commit. */
 sgs_status sgs_shadow_weights(sgs_handle* h, void** ptr, int64_t* bytes);
 sgs_status sgs_stage_weights_seed(sgs_handle* h, uint64_t seed);
+/* Trainer path of the asynchronous sync: copy src (canonical order, host or
+ * device) into the shadow buffer on the side stream. */
+sgs_status sgs_stage_weights(sgs_handle* h, const sgs_weights* src);
 sgs_status sgs_update_weights_begin(sgs_handle* h, int32_t root);
 /* *ready = 1 once the in-flight broadcast has completed on the device. */
 sgs_status sgs_update_weights_ready(sgs_handle* h, int32_t* ready);
@@ -282,9 +331,13 @@ sgs_status sgs_rope_table(float* host_out, int32_t max_pos, int32_t hd, double t
 
 /* a4/K10: causal prefill attention.  q device bf16 [T, nq, hd]; k, v device
  * bf16 [T, nkv, hd] (contiguous, not paged); prompt p spans rows
- * [offs[p], offs[p+1]) (offs device int32 [n_prompts+1]); out bf16 [T, nq, hd]. */
+ * [offs[p], offs[p+1]) (offs device int32 [n_prompts+1]); out bf16 [T, nq, hd].
+ * workspace: device, >= sgs_prefill_workspace_bytes(T, n_prompts) bytes (the
+ * 64-query block list); SGS_E_NOMEM when smaller.  Synchronises stream. */
+int64_t sgs_prefill_workspace_bytes(int32_t T, int32_t n_prompts);
 sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
-                                    int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out, void* stream);
+                                    int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out,
+                                    void* workspace, int64_t workspace_bytes, void* stream);
 
 /* a10 epilogue: m[t, i] = bf16(SiLU(gu[t, i]) * gu[t, f + i]); gu fp32 [T, 2f], m bf16 [T, f].
  * gu is zeroed after it is read. */

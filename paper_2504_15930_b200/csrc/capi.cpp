@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -30,10 +31,30 @@ sgs_status sgs_arena_bytes(const sgs_model_cfg* m, const sgs_engine_cfg* e, int6
   return SGS_OK;
 }
 
-sgs_status sgs_init(const sgs_model_cfg* m, const sgs_engine_cfg* e, sgs_handle** out) {
+sgs_status sgs_weight_tensors(const sgs_model_cfg* m, int64_t* ids, int64_t* rows, int64_t* cols, int32_t cap,
+                              int32_t* n) {
+  if (!m || !n || cap < 0 || m->n_layers < 0) return SGS_E_INVAL;
+  const int64_t d = m->d_model, hd = m->head_dim, nq = m->n_q_heads, nkv = m->n_kv_heads, f = m->d_ffn,
+                V = m->vocab;
+  std::vector<std::array<int64_t, 3>> t{{0, V, d}, {1, V, d}, {2, d, 1}};
+  const int64_t shapes[12][2] = {{nq * hd, d}, {nkv * hd, d}, {nkv * hd, d}, {nq * hd, 1}, {nkv * hd, 1},
+                                 {nkv * hd, 1}, {d, nq * hd},  {f, d},       {f, d},       {d, f},
+                                 {d, 1},        {d, 1}};
+  for (int64_t l = 0; l < m->n_layers; ++l)
+    for (int k = 0; k < 12; ++k) t.push_back({16 + 16 * l + k, shapes[k][0], shapes[k][1]});
+  *n = (int32_t)t.size();
+  for (int32_t i = 0; i < std::min<int32_t>(cap, *n); ++i) {
+    if (ids) ids[i] = t[i][0];
+    if (rows) rows[i] = t[i][1];
+    if (cols) cols[i] = t[i][2];
+  }
+  return SGS_OK;
+}
+
+sgs_status sgs_init(const sgs_model_cfg* m, const sgs_engine_cfg* e, const sgs_weights* weights, sgs_handle** out) {
   if (!m || !e || !out) return SGS_E_INVAL;
   auto* h = new sgs_handle();
-  sgs_status s = h->eng.init(*m, *e);
+  sgs_status s = h->eng.init(*m, *e, weights);
   if (s != SGS_OK) {
     g_init_err = h->eng.err;
     delete h;
@@ -67,14 +88,27 @@ sgs_status sgs_pending(const sgs_handle* h, int64_t* queued, int64_t* active) {
   return SGS_OK;
 }
 
+sgs_status sgs_host_state(const sgs_handle* h, int64_t* records, int64_t* queue_entries, int64_t* live_ids) {
+  if (!h) return SGS_E_INVAL;
+  if (records) *records = (int64_t)h->eng.sched.records();
+  if (queue_entries) *queue_entries = h->eng.sched.queue_entries();
+  if (live_ids) *live_ids = h->eng.live_ids();
+  return SGS_OK;
+}
+
 sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int32_t world) {
   if (!h || !id || world < 1 || rank < 0 || rank >= world) return SGS_E_INVAL;
   return h->eng.comm_init(id, rank, world);
 }
 
-sgs_status sgs_update_weights(sgs_handle* h, int32_t root) {
+sgs_status sgs_update_weights(sgs_handle* h, const sgs_weights* src, int32_t root) {
   if (!h) return SGS_E_INVAL;
-  return h->eng.update_weights(root);
+  return h->eng.update_weights(src, root);
+}
+
+sgs_status sgs_stage_weights(sgs_handle* h, const sgs_weights* src) {
+  if (!h || !src) return SGS_E_INVAL;
+  return h->eng.stage_weights(src);
 }
 
 sgs_status sgs_shadow_weights(sgs_handle* h, void** ptr, int64_t* bytes) {
@@ -301,8 +335,14 @@ sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t*
                                       nullptr, nullptr, T, nq, nkv, hd, page, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int64_t sgs_prefill_workspace_bytes(int32_t T, int32_t n_prompts) {
+  // one (prompt, 64-query block) pair per block: sum ceil(len/64) <= T/64 + n_prompts
+  return 8 * ((int64_t)(T > 0 ? T : 0) / 64 + (n_prompts > 0 ? n_prompts : 0) + 1);
+}
+
 sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
-                                    int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out, void* stream) {
+                                    int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out,
+                                    void* workspace, int64_t workspace_bytes, void* stream) {
   if (!q || !k || !v || !offs || !out || n_prompts < 0 || nq <= 0 || nkv <= 0 || nq % nkv) return SGS_E_INVAL;
   if (n_prompts == 0) return SGS_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -314,13 +354,12 @@ sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v,
   for (int p = 0; p < n_prompts; ++p)
     for (int b = 0; b < (ho[p + 1] - ho[p] + 63) / 64; ++b) qb.push_back(p), qb.push_back(b);
   if (qb.empty()) return SGS_OK;
-  int32_t* d_qb = nullptr;
-  if (cudaMallocAsync(&d_qb, qb.size() * 4, st) != cudaSuccess) return SGS_E_CUDA;
+  if (!workspace || (int64_t)qb.size() * 4 > workspace_bytes) return SGS_E_NOMEM;
+  int32_t* d_qb = reinterpret_cast<int32_t*>(workspace);
   cudaError_t e = cudaMemcpyAsync(d_qb, qb.data(), qb.size() * 4, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
     e = sgs::attn_prefill(q, k, v, offs, d_qb, (int)qb.size() / 2, nq, nkv, hd, out, st);
-  cudaFreeAsync(d_qb, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host block list dies here
   return cuda_status(e);
 }
 

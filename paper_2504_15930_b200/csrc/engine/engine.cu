@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "nccl.h"
 
@@ -126,6 +127,7 @@ Engine::~Engine() {
       cudaStreamDestroy(st_side_);
     }
     if (ev_sync_) cudaEventDestroy(ev_sync_);
+    if (ev_commit_) cudaEventDestroy(ev_commit_);
     if (st_pf_) {
       cudaStreamSynchronize(st_pf_);
       cudaStreamDestroy(st_pf_);
@@ -166,7 +168,7 @@ void Engine::build_tensor_table() {
   }
 }
 
-sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
+sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const sgs_weights* w) {
   m_ = m;
   e_ = e;
   if (e_.max_prefill_tokens <= 0) e_.max_prefill_tokens = 16384;
@@ -180,6 +182,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
   null_ = e.device < 0;
   if (const char* sk = std::getenv("SGS_DEBUG_SKIP")) skip_ = std::atoi(sk);
   max_gen_ = e.max_ctx + 1;
+  sched.tracing = (e.flags & SGS_F_TRACE) != 0;
   if (null_) {
     n_pages_ = e.n_pages;
     if (n_pages_ <= 0) {
@@ -187,13 +190,14 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
       return SGS_E_INVAL;
     }
     sched.init(e.max_batch, e.page_size, n_pages_);
+    sched.tracing = (e.flags & SGS_F_TRACE) != 0;
     return SGS_OK;
   }
   // ---- device mode: shape support of the sm_100a kernels
   if (e.page_size != 16 || !(m.head_dim == 32 || m.head_dim == 64 || m.head_dim == 128) ||
-      m.n_q_heads / m.n_kv_heads > 16 || m.d_model % 128 || m.d_ffn % 128 || m.vocab % 128 ||
+      m.n_q_heads / m.n_kv_heads > 8 || m.d_model % 128 || m.d_ffn % 128 || m.vocab % 128 ||
       ((m.n_q_heads + 2 * m.n_kv_heads) * m.head_dim) % 128 || (m.n_q_heads * m.head_dim) % 64) {
-    err = "shape not supported by the sm_100a kernels (page 16, hd 32/64/128, dims multiple of 128)";
+    err = "shape not supported by the sm_100a kernels (page 16, hd 32/64/128, GQA group <= 8, dims multiple of 128)";
     return SGS_E_UNSUPPORTED;
   }
   CK(cudaSetDevice(e.device), "cudaSetDevice");
@@ -273,6 +277,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
     shadow_ = arena_ + L_.off_shadow;
     CK(cudaStreamCreateWithFlags(&st_side_, cudaStreamNonBlocking), "side stream");
     CK(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming), "event");
+    CK(cudaEventCreateWithFlags(&ev_commit_, cudaEventDisableTiming), "event");
   }
   // zero the KV pool (finite garbage only beyond ctx) and the small state
   CK(cudaMemsetAsync(arena_ + L_.off_kv, 0, L_.kv_bytes, st_), "memset kv");
@@ -293,10 +298,42 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
     CK(cudaMemcpy(rope_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice), "rope table");
   }
   build_tensor_table();
-  sgs_status s = load_weights_seed(e.weight_seed);
+  sgs_status s = w ? load_weights(w, arena_, st_) : load_weights_seed(e.weight_seed);
   if (s != SGS_OK) return s;
   CK(cudaStreamSynchronize(st_), "init sync");
   sched.init(e.max_batch, e.page_size, n_pages_);
+  sched.tracing = (e.flags & SGS_F_TRACE) != 0;
+  return SGS_OK;
+}
+
+// Canonical order (sgs.h): embed, lm_head, final norm, then per layer Wq, Wk,
+// Wv, bq, bk, bv, Wo, Wgate, Wup, Wdown, attention norm, MLP norm -- exactly
+// the order of tensors_ (build_tensor_table).
+sgs_status Engine::load_weights(const sgs_weights* w, uint8_t* base, cudaStream_t st) {
+  if (null_) return SGS_OK;
+  if (!w || !w->ptrs || w->n != (int32_t)tensors_.size()) {
+    err = "sgs_weights: expected " + std::to_string(tensors_.size()) + " tensors in canonical order";
+    return SGS_E_INVAL;
+  }
+  for (size_t i = 0; i < tensors_.size(); ++i)
+    if (!w->ptrs[i]) {
+      err = "sgs_weights: null tensor pointer at index " + std::to_string(i);
+      return SGS_E_INVAL;
+    }
+  for (size_t i = 0; i < tensors_.size(); ++i) {
+    const TensorRef& t = tensors_[i];
+    uint8_t* dst = base + (reinterpret_cast<uint8_t*>(t.ptr) - arena_);
+    if (t.blk == 0) {
+      CK(cudaMemcpyAsync(dst, w->ptrs[i], (size_t)t.n * 2, cudaMemcpyDefault, st), "weight copy");
+    } else {
+      // rows of 64 gate (or up) rows land every 128 rows of the fused matrix
+      const size_t rowb = (size_t)t.cols * 2, rows = (size_t)(t.n / t.cols);
+      CK(cudaMemcpy2DAsync(dst + (size_t)t.off * rowb, (size_t)t.stride * rowb, w->ptrs[i], (size_t)t.blk * rowb,
+                           (size_t)t.blk * rowb, rows / t.blk, cudaMemcpyDefault, st),
+         "weight copy (gate/up)");
+    }
+  }
+  CK(cudaStreamSynchronize(st), "weight copy sync");  // the caller may free its buffers on return
   return SGS_OK;
 }
 
@@ -364,8 +401,8 @@ sgs_status Engine::submit(const sgs_prompt* prompts, int32_t n, const int32_t* h
       return SGS_E_INVAL;
     }
     for (uint64_t id : s)
-      if (std::binary_search(seen_ids_.begin(), seen_ids_.end(), id)) {
-        err = "id already submitted to this handle";
+      if (live_ids_.count(id)) {
+        err = "id of a sample still queued or active on this handle";
         return SGS_E_INVAL;
       }
   }
@@ -392,12 +429,10 @@ sgs_status Engine::submit(const sgs_prompt* prompts, int32_t n, const int32_t* h
     s.d = forced[i];
     s.hint = hint[i];
     s.batch = batch_counter_;
-    s.tok_off = (int64_t)prompt_store_.size();
-    prompt_store_.insert(prompt_store_.end(), prompts[i].tokens, prompts[i].tokens + P[i]);
+    s.prompt.assign(prompts[i].tokens, prompts[i].tokens + P[i]);
+    live_ids_.insert(s.id);
     mine.push_back(std::move(s));
   }
-  for (uint64_t id : ids) seen_ids_.push_back(id);
-  std::sort(seen_ids_.begin(), seen_ids_.end());
   if (n_mine) *n_mine = (int32_t)mine.size();
   sched.submit(std::move(mine));
   ++batch_counter_;
@@ -562,6 +597,17 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   auto& S = sched.samples();
   const int n_adm = (int)plan.admitted.size();
   const int n_run = (int)plan.running.size();
+  // the prompt tokens are needed only to stage this iteration's prefill; a
+  // completed sample's id may be submitted again (R22)
+  struct Release {
+    std::vector<Sample>& S;
+    const IterPlan& plan;
+    std::unordered_set<uint64_t>& live;
+    ~Release() {
+      for (int32_t i : plan.admitted) std::vector<int32_t>().swap(S[i].prompt);
+      for (int32_t i : plan.completed) live.erase(S[i].id);
+    }
+  } release{S, plan, live_ids_};
   if (null_) {
     for (int32_t i : plan.completed) {
       const Sample& s = S[i];
@@ -614,7 +660,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     std::vector<int32_t> tok, pos, slot, offs(1, 0), qb, last, pfs, pft, pfid;
     for (size_t k = 0; k < c.idx.size(); ++k) {
       const Sample& s = S[c.idx[k]];
-      tok.insert(tok.end(), prompt_store_.begin() + s.tok_off, prompt_store_.begin() + s.tok_off + s.P);
+      tok.insert(tok.end(), s.prompt.begin(), s.prompt.end());
       for (int j = 0; j < s.P; ++j) pos.push_back(j), slot.push_back(s.slot);
       offs.push_back(offs.back() + s.P);
       for (int b = 0; b < (s.P + 63) / 64; ++b) qb.push_back((int32_t)k), qb.push_back(b);
@@ -1112,7 +1158,7 @@ sgs_status Engine::comm_init(const uint8_t id[128], int rank, int world) {
   return SGS_OK;
 }
 
-sgs_status Engine::update_weights(int root) {
+sgs_status Engine::update_weights(const sgs_weights* src, int root) {
   if (poisoned) {
     err = "handle poisoned";
     return SGS_E_STATE;
@@ -1129,9 +1175,18 @@ sgs_status Engine::update_weights(int root) {
     err = "an asynchronous weight update is in flight";
     return SGS_E_STATE;
   }
+  const int me = nccl_world_ > 1 ? nccl_rank_ : 0;
+  if (src && me != root) {
+    err = "only the root passes the new weights";
+    return SGS_E_INVAL;
+  }
   if (null_) {
     ++version;
     return SGS_OK;
+  }
+  if (src) {
+    sgs_status ls = load_weights(src, arena_, st_);
+    if (ls != SGS_OK) return ls;
   }
   if (nccl_world_ > 1) {
     if (!nccl_comm_) {
@@ -1186,6 +1241,8 @@ sgs_status Engine::stage_weights_seed(uint64_t seed) {
     err = "a weight update is in flight";
     return SGS_E_STATE;
   }
+  // the previous commit may still be copying shadow -> active on st_
+  CK(cudaStreamWaitEvent(st_side_, ev_commit_, 0), "wait commit");
   // the same tensors at the same offsets of the shadow buffer, on the side stream
   for (const auto& t : tensors_) {
     void* dst = shadow_ + (reinterpret_cast<uint8_t*>(t.ptr) - arena_);
@@ -1193,6 +1250,20 @@ sgs_status Engine::stage_weights_seed(uint64_t seed) {
        "hash_init(shadow)");
   }
   return SGS_OK;
+}
+
+sgs_status Engine::stage_weights(const sgs_weights* src) {
+  if (null_) return SGS_OK;
+  if (!shadow_) {
+    err = "engine created without SGS_F_SHADOW_WEIGHTS";
+    return SGS_E_STATE;
+  }
+  if (sync_pending_) {
+    err = "a weight update is in flight";
+    return SGS_E_STATE;
+  }
+  CK(cudaStreamWaitEvent(st_side_, ev_commit_, 0), "wait commit");
+  return load_weights(src, shadow_, st_side_);
 }
 
 sgs_status Engine::update_weights_begin(int root) {
@@ -1212,6 +1283,8 @@ sgs_status Engine::update_weights_begin(int root) {
     err = "engine created without SGS_F_SHADOW_WEIGHTS";
     return SGS_E_STATE;
   }
+  // the previous commit may still be copying shadow -> active on st_
+  CK(cudaStreamWaitEvent(st_side_, ev_commit_, 0), "wait commit");
   if (nccl_world_ > 1) {
     if (!nccl_comm_) {
       err = "sgs_comm_init not called";
@@ -1274,6 +1347,7 @@ sgs_status Engine::update_weights_commit() {
   if (!null_) {
     CK(cudaStreamWaitEvent(st_, ev_sync_, 0), "wait sync");
     CK(cudaMemcpyAsync(arena_, shadow_, (size_t)L_.weights_bytes, cudaMemcpyDeviceToDevice, st_), "swap weights");
+    CK(cudaEventRecord(ev_commit_, st_), "record commit");
   }
   ++version;
   sync_pending_ = false;

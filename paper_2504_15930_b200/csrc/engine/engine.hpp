@@ -7,6 +7,7 @@
 #include <deque>
 #include <map>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "../../../include/sgs.h"
@@ -47,14 +48,16 @@ struct Completion {
 class Engine {
  public:
   ~Engine();
-  sgs_status init(const sgs_model_cfg& m, const sgs_engine_cfg& e);
+  sgs_status init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const sgs_weights* w);
   sgs_status submit(const sgs_prompt* prompts, int32_t n, const int32_t* hint, const int32_t* forced,
                     int32_t* n_mine);
   sgs_status step(sgs_completion* out, int32_t cap, int32_t* n_out);
   sgs_status load_weights_seed(uint64_t seed);
   sgs_status checksum(int64_t tensor_id, uint64_t* out);
   sgs_status comm_init(const uint8_t id[128], int rank, int world);
-  sgs_status update_weights(int root);
+  sgs_status update_weights(const sgs_weights* src, int root);
+  sgs_status load_weights(const sgs_weights* w, uint8_t* base, cudaStream_t st);
+  sgs_status stage_weights(const sgs_weights* src);
   // asynchronous weight sync (SGS_F_SHADOW_WEIGHTS): shadow buffer, side stream
   sgs_status shadow_weights(void** ptr, int64_t* bytes);
   sgs_status stage_weights_seed(uint64_t seed);
@@ -187,6 +190,7 @@ class Engine {
   sgs_status finalize_front();
  public:
   sgs_status drain();  // finalize every in-flight iteration (before weight updates, debug calls, ...)
+  int64_t live_ids() const { return (int64_t)live_ids_.size(); }
   int64_t inflight_samples() const {
     int64_t n = 0;
     for (const auto& f : infl_) n += (int64_t)f.comps.size();
@@ -196,10 +200,10 @@ class Engine {
   uint8_t* shadow_ = nullptr;           // second weight buffer (SGS_F_SHADOW_WEIGHTS)
   cudaStream_t st_side_ = nullptr;      // weight staging + broadcast, concurrent with generation
   cudaEvent_t ev_sync_ = nullptr;       // end of the in-flight broadcast on st_side_
+  cudaEvent_t ev_commit_ = nullptr;     // end of the last commit's shadow -> active copy (on st_)
   bool sync_pending_ = false;
   // prompts (host)
-  std::vector<int32_t> prompt_store_;
-  std::vector<uint64_t> seen_ids_;
+  std::unordered_set<uint64_t> live_ids_;  // ids queued or active (R22)
   int batch_counter_ = 0;
   std::deque<Completion> ready_;
   std::vector<Completion> handed_;  // storage for the completions returned by the last step

@@ -64,10 +64,23 @@ void Scheduler::init(int max_batch, int page, int64_t n_pages) {
 static inline int64_t reservation(const Sample& s, int page) { return ((int64_t)s.P + s.d - 1 + page - 1) / page; }
 
 void Scheduler::submit(std::vector<Sample>&& batch) {
-  const int32_t base = (int32_t)samples_.size();
-  std::vector<int32_t> idx(batch.size());
-  std::iota(idx.begin(), idx.end(), base);
-  for (auto& s : batch) samples_.push_back(std::move(s));
+  // drop the consumed queue prefix once it dominates the queue
+  if (qhead_ >= 1024 && 2 * qhead_ >= queue_.size()) {
+    queue_.erase(queue_.begin(), queue_.begin() + (std::ptrdiff_t)qhead_);
+    qhead_ = 0;
+  }
+  std::vector<int32_t> idx;
+  idx.reserve(batch.size());
+  for (auto& s : batch) {
+    if (!tracing && !free_idx_.empty()) {
+      idx.push_back(free_idx_.back());
+      free_idx_.pop_back();
+      samples_[idx.back()] = std::move(s);
+    } else {
+      idx.push_back((int32_t)samples_.size());
+      samples_.push_back(std::move(s));
+    }
+  }
   std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
     const Sample &x = samples_[a], &y = samples_[b];
     if (x.hint != y.hint) return x.hint > y.hint;
@@ -84,6 +97,11 @@ bool Scheduler::plan(IterPlan* p) {
   p->alloc_log.clear();
   p->free_log.clear();
   if (idle()) return false;
+  // records of the samples completed by the previous plan are free from now on
+  if (!tracing) {
+    free_idx_.insert(free_idx_.end(), retire_.begin(), retire_.end());
+    retire_.clear();
+  }
   p->t = t_;
   // running samples are those active before admission
   for (int s = 0; s < B_; ++s)
@@ -149,6 +167,7 @@ bool Scheduler::plan(IterPlan* p) {
     slot_of_[s.slot] = -1;
     reserved_ -= reservation(s, page_);
     --active_;
+    if (!tracing) retire_.push_back(i);
   }
   if (tracing) {
     auto& o = trace_iters;

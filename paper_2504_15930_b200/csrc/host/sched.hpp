@@ -29,7 +29,7 @@ struct Sample {
   uint64_t id;
   int32_t P, d, hint;
   int32_t batch;
-  int64_t tok_off;  // offset of the prompt in the token store
+  std::vector<int32_t> prompt;  // prompt tokens; released once the prefill metadata is staged
   // runtime
   int32_t slot = -1;
   int32_t produced = 0;
@@ -63,10 +63,15 @@ class Scheduler {
   const std::vector<Sample>& samples() const { return samples_; }
   int page() const { return page_; }
   int64_t pool_pages() const { return pages_.capacity(); }
-  // trace (DESIGN.md §5 format)
+  // trace (DESIGN.md §5 format).  Without tracing the host state is bounded
+  // by the samples in flight: completed sample records are recycled (one
+  // iteration after their completion, so the engine can still read them while
+  // it stages that iteration) and the consumed queue prefix is dropped.
   std::vector<int64_t> trace_iters;
-  bool tracing = true;
+  bool tracing = false;
   void sample_trace(std::vector<int64_t>* out) const;
+  size_t records() const { return samples_.size(); }
+  int64_t queue_entries() const { return (int64_t)queue_.size(); }
 
  private:
   int B_ = 0, page_ = 16;
@@ -75,6 +80,7 @@ class Scheduler {
   std::vector<int32_t> queue_;    // sample indices in admission order (FIFO by batch, LF within)
   size_t qhead_ = 0;
   std::vector<int32_t> slot_of_;  // slot -> sample index or -1
+  std::vector<int32_t> free_idx_, retire_;  // recyclable sample records (tracing off)
   int64_t reserved_ = 0;
   int32_t active_ = 0;
   int64_t t_ = 0;

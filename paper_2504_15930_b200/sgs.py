@@ -20,6 +20,7 @@ F_KEEP_LOGITS = 1
 F_NO_GRAPHS = 2
 F_KERNEL_TIMING = 4
 F_SHADOW_WEIGHTS = 8
+F_TRACE = 16
 
 # every symbol include/sgs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
@@ -32,6 +33,7 @@ EXPORTS = [
     "sgs_op_decode_attention", "sgs_op_gemm", "sgs_op_rmsnorm", "sgs_op_rope_append", "sgs_rope_table",
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
     "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer", "sgs_op_sample_top_p",
+    "sgs_weight_tensors", "sgs_stage_weights", "sgs_prefill_workspace_bytes", "sgs_host_state",
 ]
 
 
@@ -63,6 +65,10 @@ class EngineCfg(ctypes.Structure):
                 ("flags", ctypes.c_int32)]
 
 
+class Weights(ctypes.Structure):
+    _fields_ = [("ptrs", ctypes.POINTER(ctypes.c_void_p)), ("n", ctypes.c_int32)]
+
+
 class Prompt(ctypes.Structure):
     _fields_ = [("id", ctypes.c_uint64), ("tokens", ctypes.POINTER(ctypes.c_int32)), ("len", ctypes.c_int32)]
 
@@ -91,7 +97,12 @@ def _declare(L):
     vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     P = ctypes.POINTER
     L.sgs_arena_bytes.argtypes = [P(ModelCfg), P(EngineCfg), i64, P(i64), P(i64)]
-    L.sgs_init.argtypes = [P(ModelCfg), P(EngineCfg), P(vp)]
+    L.sgs_init.argtypes = [P(ModelCfg), P(EngineCfg), P(Weights), P(vp)]
+    L.sgs_weight_tensors.argtypes = [P(ModelCfg), P(i64), P(i64), P(i64), i32, P(i32)]
+    L.sgs_stage_weights.argtypes = [vp, P(Weights)]
+    L.sgs_host_state.argtypes = [vp, P(i64), P(i64), P(i64)]
+    L.sgs_prefill_workspace_bytes.argtypes = [i32, i32]
+    L.sgs_prefill_workspace_bytes.restype = i64
     L.sgs_destroy.argtypes = [vp]
     L.sgs_destroy.restype = None
     L.sgs_last_error.argtypes = [vp]
@@ -101,7 +112,7 @@ def _declare(L):
     L.sgs_pending.argtypes = [vp, P(i64), P(i64)]
     L.sgs_comm_unique_id.argtypes = [P(ctypes.c_uint8)]
     L.sgs_comm_init.argtypes = [vp, P(ctypes.c_uint8), i32, i32]
-    L.sgs_update_weights.argtypes = [vp, i32]
+    L.sgs_update_weights.argtypes = [vp, P(Weights), i32]
     L.sgs_shadow_weights.argtypes = [vp, P(vp), P(i64)]
     L.sgs_stage_weights_seed.argtypes = [vp, u64]
     L.sgs_update_weights_begin.argtypes = [vp, i32]
@@ -135,10 +146,10 @@ def _declare(L):
     L.sgs_op_sample_top_p.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, u64, vp, vp, vp, vp]
     L.sgs_op_silu_mul.argtypes = [vp, vp, i32, i32, vp]
     L.sgs_debug_forward.argtypes = [vp, P(i32), i32, P(ctypes.c_float)]
-    L.sgs_op_prefill_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
+    L.sgs_op_prefill_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, i64, vp]
     for name in EXPORTS:
         f = getattr(L, name)
-        if name not in ("sgs_destroy", "sgs_last_error", "sgs_attn_workspace_bytes"):
+        if name not in ("sgs_destroy", "sgs_last_error", "sgs_attn_workspace_bytes", "sgs_prefill_workspace_bytes"):
             f.restype = ctypes.c_int
 
 
@@ -156,6 +167,29 @@ def model_cfg(shape) -> ModelCfg:
                     shape.vocab, shape.rms_eps, shape.rope_theta)
 
 
+def weight_tensors(shape):
+    """Canonical weight order of a model: list of (tensor id, rows, cols) (sgs_weight_tensors)."""
+    m = model_cfg(shape)
+    n = ctypes.c_int32()
+    _check(lib().sgs_weight_tensors(ctypes.byref(m), None, None, None, 0, ctypes.byref(n)))
+    ids, rows, cols = (np.zeros(n.value, np.int64) for _ in range(3))
+    P = ctypes.POINTER(ctypes.c_int64)
+    _check(lib().sgs_weight_tensors(ctypes.byref(m), ids.ctypes.data_as(P), rows.ctypes.data_as(P),
+                                    cols.ctypes.data_as(P), n.value, ctypes.byref(n)))
+    return [(int(a), int(b), int(c)) for a, b, c in zip(ids, rows, cols)]
+
+
+def make_weights(tensors):
+    """sgs_weights over a list of bf16 tensors (torch CPU/CUDA or numpy uint16 views) in canonical
+    order; the returned object keeps the pointer array alive."""
+    ptrs = (ctypes.c_void_p * max(len(tensors), 1))()
+    for i, t in enumerate(tensors):
+        ptrs[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+    w = Weights(ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), len(tensors))
+    w._keep = (ptrs, tensors)
+    return w
+
+
 def _stream_ptr(stream):
     if stream is None:
         return None
@@ -170,7 +204,10 @@ class Instance:
                  instance_rank: int = 0, dispatch: str = "skew", alpha_pct: int = 20, score: int = 0,
                  tail_ceil: int = 0, profile=(2000, 1000, 208, 5000), weight_seed: int = 1234,
                  sample_seed: int = 0, flags: int = 0, max_prefill_tokens: int = 16384, stream=None,
-                 top_p: float | None = None, temperature: float = 1.0):
+                 top_p: float | None = None, temperature: float = 1.0, trace: bool = True, weights=None):
+        """weights: None (hash-init from weight_seed) or a list of bf16 tensors in the
+        canonical order of weight_tensors(shape).  trace: keep the schedule trace
+        (SGS_F_TRACE; the C default is off, bench.py turns it off)."""
         L = lib()
         self.shape = shape
         self.m = model_cfg(shape)
@@ -181,7 +218,7 @@ class Instance:
         e.dispatch, e.alpha_pct, e.score, e.tail_ceil = DISPATCH[dispatch], alpha_pct, score, tail_ceil
         e.profile = TbProfile(*profile)
         e.sampling, e.temperature, e.top_p = (1 if top_p is not None else 0), temperature, (top_p or 1.0)
-        e.sample_seed, e.weight_seed, e.flags = sample_seed, weight_seed, flags
+        e.sample_seed, e.weight_seed, e.flags = sample_seed, weight_seed, flags | (F_TRACE if trace else 0)
         self.arena = None
         self.stream = None
         if device is None:
@@ -211,7 +248,9 @@ class Instance:
         self.n_pages = e.n_pages
         self.e = e
         h = ctypes.c_void_p()
-        _check(L.sgs_init(ctypes.byref(self.m), ctypes.byref(e), ctypes.byref(h)))
+        wts = make_weights(weights) if weights is not None else None
+        _check(L.sgs_init(ctypes.byref(self.m), ctypes.byref(e), ctypes.byref(wts) if wts is not None else None,
+                          ctypes.byref(h)))
         self.h = h
         self._cap = max(64, max_batch * 2)
         self._comp = (Completion * self._cap)()
@@ -249,7 +288,7 @@ class Instance:
 
     def step(self, cap: int | None = None):
         """One iteration; returns a list of completion dicts (ascending id)."""
-        cap = self._cap if cap is None else cap
+        cap = self._cap if cap is None else min(int(cap), self._cap)  # the C side writes <= cap records
         n = ctypes.c_int32()
         _check(lib().sgs_step(self.h, self._comp, cap, ctypes.byref(n)), self.h)
         out = []
@@ -259,6 +298,12 @@ class Instance:
             out.append(dict(id=int(c.id), instance=c.instance, tokens=toks, admit_iter=c.admit_iter,
                             finish_iter=c.finish_iter, weight_version=c.weight_version, slot=c.slot))
         return out
+
+    def host_state(self):
+        """(sample records, queue entries, live ids) held on the host."""
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().sgs_host_state(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), self.h)
+        return a.value, b.value, c.value
 
     def pending(self):
         q, a = ctypes.c_int64(), ctypes.c_int64()
@@ -290,8 +335,16 @@ class Instance:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib().sgs_comm_init(self.h, buf, rank, world), self.h)
 
-    def update_weights(self, root: int = 0):
-        _check(lib().sgs_update_weights(self.h, root), self.h)
+    def update_weights(self, root: int = 0, weights=None):
+        """Weight sync: the root copies `weights` (canonical order, or None = keep its
+        current weights) and broadcasts; other ranks pass None."""
+        wts = make_weights(weights) if weights is not None else None
+        _check(lib().sgs_update_weights(self.h, ctypes.byref(wts) if wts is not None else None, root), self.h)
+
+    def stage_weights(self, weights):
+        """Asynchronous sync, trainer path: copy weights into the shadow buffer (side stream)."""
+        wts = make_weights(weights)
+        _check(lib().sgs_stage_weights(self.h, ctypes.byref(wts)), self.h)
 
     # ---- asynchronous weight sync (flags |= F_SHADOW_WEIGHTS; DESIGN.md §10)
     def shadow_weights(self):
@@ -483,11 +536,15 @@ def op_argmax(logits, ids):
     _check(lib().sgs_op_argmax(_ptr(logits), rows, V, _ptr(ids), _cur_stream(logits)))
 
 
-def op_prefill_attention(q, k, v, offs, out):
+def op_prefill_attention(q, k, v, offs, out, workspace=None):
+    import torch
     T, nq, hd = q.shape
     nkv = k.shape[1]
+    need = lib().sgs_prefill_workspace_bytes(T, offs.numel() - 1)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     _check(lib().sgs_op_prefill_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(offs), offs.numel() - 1, nq, nkv, hd,
-                                          _ptr(out), _cur_stream(q)))
+                                          _ptr(out), _ptr(workspace), workspace.numel(), _cur_stream(q)))
 
 
 def op_decode_attention(q, kv, block_table, ctx, out, page=16, split_pages=0, workspace=None):

@@ -242,3 +242,17 @@ def test_decoder_layer_composes_to_forward():
     dump = oracle.decoder_dump(shape, 9, toks)
     for l in range(shape.n_layers):
         assert np.array_equal(oracle.decoder_layer(shape, 9, l, dump[2 * l]), dump[2 * l + 2])
+
+
+def test_top_p_nucleus_golden():
+    # tests/golden/top_p_nucleus.json: equal logits make every prefix mass exact,
+    # so the ">=" of "smallest prefix with mass >= top_p" (R18), the ascending-id
+    # tie order and the renormalisation of u by the nucleus mass are each decided
+    # by a hand-derived draw from a Random123 Philox known-answer counter.
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "top_p_nucleus.json")))
+    for c in g["cases"]:
+        got = oracle.sample_top_p(np.zeros(c["V"], np.float32), 1.0, c["top_p"], c["seed"], c["sample_id"],
+                                  c["step"])
+        assert got == c["expect"], c["name"]

@@ -345,3 +345,31 @@ def test_dispatch_degenerate():
     h66 = np.array([200] * 2 + [100] * 64)
     assert _disp(np.arange(66), np.full(66, 8), h66, 2, tail_ceil=1)["n_tail"] == 14
     assert _disp(np.arange(66), np.full(66, 8), h66, 2)["n_tail"] == 13
+
+
+# ----------------------------------------------------------------- hand-derived goldens (pins)
+def test_sched_reservation_binds_golden():
+    # tests/golden/sched_reservation_binds.json: the queue head is blocked by its
+    # page reservation ceil((P+d-1)/page) (reading R3) while a later,
+    # smaller sample would fit; strict LF order means no backfill.
+    # A reservation of ceil((P+d)/page) or a backfilling admission fails this.
+    g = json.load(open(os.path.join(GOLD, "sched_reservation_binds.json")))
+    s = np.array(g["samples"])
+    r = oracle.sched_sim(s[:, 0], s[:, 1], s[:, 2], s[:, 3], g["B"], g["page"], g["pool"])
+    assert r["iters"] == g["iters"]
+    assert {str(k): v for k, v in r["samples"].items()} == g["per_sample"]
+
+
+@pytest.mark.parametrize("mode,key", [(0, "expect_sum"), (1, "expect_max")])
+def test_dispatch_eq2_argmin_n4_memory_cap_golden(mode, key):
+    # tests/golden/dispatch_eq2_n4_memcap.json: N = 4, every N_l's Eq. 2 score
+    # computed by hand with the memory-capped BS binding for both groups
+    # (P:969-978); argmin and the tie (max mode) resolve to N_l = 2.
+    g = json.load(open(os.path.join(GOLD, "dispatch_eq2_n4_memcap.json")))
+    r = oracle.dispatch(g["ids"], g["prompt_len"], g["hint"], g["N"], g["B"], g["page"], g["pool"], g["profile"],
+                        alpha_pct=g["alpha_pct"], score_max=mode)
+    e = g[key]
+    assert (r["n_tail"], r["L_alpha"], r["L_r"]) == (8, 1000, 120)
+    assert r["scores"] == e["scores"]
+    assert r["n_l"] == e["n_l"]
+    assert r["instance"].tolist() == e["instance"]
