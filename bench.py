@@ -112,42 +112,86 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    import oracle
     cfg = workload.CONFIGS[args.config]
     shape = workload.MODELS[cfg.model]
-    res = cpu_oracle_sample(shape, steps=args.steps, warmup=args.warmup)
-    line = {"metric": "generated_tokens_per_s", "value": res["value"], "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+    samples = [cpu_oracle_sample(shape, cfg, warm=(i == 0)) for i in range(args.warmup + args.steps)][args.warmup:]
+    ms = [s["ms"] for s in samples]
+    tok = sum(s["tokens"] for s in samples)
+    value = tok / (sum(ms) / 1e3)
+    line = {"metric": "generated_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(ms),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.config}: {cfg.model}-shaped, {cfg.n_prompts} prompts x {cfg.prompt_len}"},
-            "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"], "kind": "oracle",
-                             "sample": res["sample"]},
-            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": samples[0]["cores"], "kind": "oracle",
+                             "sample": samples[0]["sample"]},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_oracle_sample(shape, steps=1, warmup=0, T=8):
-    """Time the oracle decoder (as it stands) on a bounded sample of the workload:
-    T positions of one sample through layer subsets of the full model, extrapolated
-    to all layers (t_full = t_lmhead + L * (t_1layer - t_lmhead))."""
+def cpu_oracle_sample(shape, cfg, warm=True, P0=4, K=12):
+    """One bounded, measured step of the oracle decoder (as it stands: fp64,
+    OpenMP, no KV cache, no batching) on this workload's model at b = 1: one
+    teacher-forced forward over P0 prompt + K positions, whose K + 1 logits rows
+    are the sample's generated tokens (the prefill of the P0 prefix is inside
+    the timed step).  Weights are built once (oracle.weight_cache memoises the
+    generator's output, same values), so the step times the decoder arithmetic.
+    When the fp32 weight copy would not fit in 40% of host RAM, the step runs
+    0- and 1-layer instances of the shape and extrapolates linearly to L layers
+    (said in the sample text)."""
     import dataclasses
     import oracle
-    toks = np.random.default_rng(0).integers(0, shape.vocab, size=T).astype(np.int32)
-    times = []
-    for i in range(warmup + steps):
+    oracle.weight_cache(True)
+    toks = np.random.default_rng(0).integers(0, shape.vocab, size=P0 + K).astype(np.int32)
+    ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    full = 4.0 * shape.params() <= 0.4 * ram
+    if full:
+        if warm:
+            oracle.decoder_forward(shape, 1, toks[:2], 1)  # builds (caches) the weights, untimed
         t0 = time.perf_counter()
-        oracle.decoder_forward(dataclasses.replace(shape, n_layers=0), 1, toks, T - 1)
-        t1 = time.perf_counter()
-        oracle.decoder_forward(dataclasses.replace(shape, n_layers=1), 1, toks, T - 1)
-        t2 = time.perf_counter()
-        if i >= warmup:
-            t_lm, t_layer = t1 - t0, (t2 - t1) - (t1 - t0)
-            times.append(t_lm + shape.n_layers * max(t_layer, 0.0))
-    t_full = statistics.median(times)
-    return {"value": T / t_full, "ms_per_step": 1e3 * t_full, "cores": os.cpu_count(),
-            "sample": f"{T} teacher-forced positions of one sample; 0- and 1-layer {shape.name} runs timed, "
-                      f"extrapolated to {shape.n_layers} layers (fp64, OpenMP, weights regenerated per call)"}
+        oracle.decoder_forward(shape, 1, toks, P0 - 1)
+        t = time.perf_counter() - t0
+        how = f"full {shape.n_layers}-layer model"
+    else:
+        ts = []
+        for nl in (0, 1):
+            sh = dataclasses.replace(shape, n_layers=nl)
+            if warm:
+                oracle.decoder_forward(sh, 1, toks[:2], 1)
+            t0 = time.perf_counter()
+            oracle.decoder_forward(sh, 1, toks, P0 - 1)
+            ts.append(time.perf_counter() - t0)
+        t = ts[0] + shape.n_layers * max(ts[1] - ts[0], 0.0)
+        how = f"0- and 1-layer instances extrapolated to {shape.n_layers} layers (fp32 weights > 40% of RAM)"
+    n = K + 1
+    return {"tokens": n, "ms": 1e3 * t, "per_token_s": t / n, "cores": os.cpu_count(),
+            "b_B_iteration_s": t / n * cfg.max_batch,
+            "sample": f"one teacher-forced forward of {P0}+{K} positions of {shape.name} at b=1 ({how}; "
+                      f"{n} logits rows = generated tokens, prefix prefill included), weights built once "
+                      f"(memoised), fp64, OpenMP on {os.cpu_count()} cores; the oracle has no batching: a "
+                      f"b={cfg.max_batch} iteration is {cfg.max_batch} such samples"}
+
+
+def host_plane_timing(tr, cfg, pool, shape):
+    """Scheduler + dispatch on the host: the oracle (sched_sim + dispatch) and the
+    product's control plane alone (null-device mode: the same C++ scheduler,
+    page allocator and Alg. 2 the GPU run uses, no kernels), us per iteration."""
+    import oracle
+    import paper_2504_15930_b200 as sgs
+    t0 = time.perf_counter()
+    oracle.dispatch(tr.ids, tr.prompt_len, tr.hint, 1, cfg.max_batch, cfg.page_size, pool,
+                    DEFAULT_PROFILES.get(cfg.model, (1, 1, 1, 1)))
+    r = oracle.sched_sim(tr.ids, tr.prompt_len, tr.forced_len, tr.hint, cfg.max_batch, cfg.page_size, pool)
+    t_or = time.perf_counter() - t0
+    inst = sgs.Instance(shape, cfg.max_batch, cfg.prompt_len + cfg.max_out, device=None, n_pages=pool, trace=False)
+    t0 = time.perf_counter()
+    inst.submit_trace(tr)
+    inst.run()
+    t_pr = time.perf_counter() - t0
+    n = r["n_iters"]
+    return {"iterations": n, "oracle_us_per_iter": round(1e6 * t_or / n, 2),
+            "product_us_per_iter": round(1e6 * t_pr / n, 2),
+            "note": "single-threaded host work per iteration; the product number includes the ctypes step loop"}
 
 
 def batch_roofline(rows, shape, bw_gbs, tflops):
@@ -178,6 +222,68 @@ def batch_roofline(rows, shape, bw_gbs, tflops):
         if dec > 0:
             total += gemm_t(dec) + (sumctx - pf) * kv_bytes_per_token / BW
     return total
+
+
+CLASSES = {0: "decode_attention", 1: "decode_gemm", 2: "prefill_attention", 4: "prefill_gemm", 5: "decode_other"}
+CLASS_DESC = {0: "decode attention (K1+K2, paged split-K, merge in-kernel)",
+              1: "decode tcgen05 GEMMs (QKV / O / gate-up+SwiGLU / down / LM head)",
+              2: "prefill attention (causal)", 4: "prefill tcgen05 GEMMs",
+              5: "decode RMSNorm / RoPE+append / embedding / sampler"}
+NCU_WINDOW = os.path.join(ROOT, "profiles", "r02_ncu_windows.json")
+
+
+def kernel_roofline(inst, stats, peaks, n_iters, dev_s):
+    """Per-class device time from CUDA events on the engine stream, recorded on
+    ~1 in 64 timed iterations chosen by a hash of the iteration counter (so the
+    sample is not aliased with the schedule).  The classes are disjoint
+    intervals of the sampled iterations (prefill runs sequentially in them), so
+    their sum cannot exceed the sampled iterations' device time: asserted.
+    Events between kernels remove the PDL overlap, so sampled iterations run
+    slower than production ones; shares (class / sampled iteration time) are
+    what carries over, reported next to the uninstrumented ncu launch window."""
+    it = stats[3]
+    if it["ms"] <= 0:
+        return None, None
+    tot = sum(stats[c]["ms"] for c in CLASSES)
+    assert tot <= 1.001 * it["ms"], f"kernel classes {tot:.1f} ms exceed the sampled iterations' {it['ms']:.1f} ms"
+    kernels = {}
+    for c, name in CLASSES.items():
+        st = stats[c]
+        kernels[name] = {"ms_sampled": round(st["ms"], 1), "launches_sampled": st["launches"],
+                         "share": round(st["ms"] / it["ms"], 4),
+                         "est_s_per_step_production": round(st["ms"] / it["ms"] * dev_s, 3),
+                         "roofline_frac": round(inst.kernel_roofline_ms(c) / max(st["ms"], 1e-9), 4),
+                         "GB/s": round(st["bytes"] / max(st["ms"], 1e-9) / 1e6, 1),
+                         "TFLOP/s": round(st["flops"] / max(st["ms"], 1e-9) / 1e9, 1)}
+    kernels["_sampled_iterations"] = {"n": it["launches"], "of": n_iters, "ms": round(it["ms"], 1),
+                                      "classes_ms": round(tot, 1),
+                                      "instrumentation_slowdown": round(it["ms"] * n_iters / max(it["launches"], 1)
+                                                                        / (1e3 * dev_s), 3)}
+    # the same shares within the b >= 129 and the b <= 32 iterations (compare with the ncu windows)
+    for ph, tag in ((1, "b>=129"), (2, "b<=32")):
+        itp = stats[3 + 6 * ph]
+        if itp["ms"] > 0:
+            kernels[f"_shares_{tag}"] = {"iterations": itp["launches"],
+                                         **{name: round(stats[c + 6 * ph]["ms"] / itp["ms"], 4)
+                                            for c, name in CLASSES.items()}}
+    if os.path.exists(NCU_WINDOW):
+        kernels["_ncu_windows"] = json.load(open(NCU_WINDOW))
+    dom = max(CLASSES, key=lambda c: stats[c]["ms"])
+    st = stats[dom]
+    roof_ms = inst.kernel_roofline_ms(dom)
+    hbm_share = st["bytes"] / (peaks["hbm_gbs"] * 1e6) / max(roof_ms, 1e-9)
+    bound = "hbm" if hbm_share >= 0.5 else "tensor"
+    if bound == "hbm":
+        achieved, peak, unit = st["bytes"] / (st["ms"] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"
+    else:
+        achieved, peak, unit = st["flops"] / (st["ms"] / 1e3) / 1e12, peaks["bf16_tflops_sustained"], "TFLOP/s"
+    roof = {"kernel": CLASS_DESC[dom], "class": CLASSES[dom], "bound": bound, "achieved": round(achieved, 1),
+            "peak": peak, "unit": unit, "frac": round(roof_ms / st["ms"], 4),
+            "frac_definition": "sum over the class's sampled launches of max(algorithmic bytes/HBM, flops/bf16 "
+                               "sustained) / their measured time (CUDA events on the engine stream)",
+            "traffic": None, "traffic_source": "ncu --set full per-launch DRAM bytes: profiles/README.md (r02)",
+            "peak_source": peaks["_source"], "share_of_step": round(st["ms"] / it["ms"], 4)}
+    return roof, kernels
 
 
 # ------------------------------------------------------------------ our arm
@@ -229,7 +335,7 @@ def main():
                         weight_seed=cfg.seed,
                         flags=(0 if args.no_kernel_timing else sgs.sgs.F_KERNEL_TIMING) |
                         (sgs.sgs.F_SHADOW_WEIGHTS if args.weight_sync == "async" else 0),
-                        dispatch=args.dispatch, profile=prof, sample_seed=cfg.seed)
+                        dispatch=args.dispatch, profile=prof, sample_seed=cfg.seed, trace=False)
     peaks0 = load_peaks()
     inst.set_roofline(peaks0["hbm_gbs"], peaks0["bf16_tflops_sustained"])
     if world > 1:
@@ -279,7 +385,7 @@ def main():
 
     for w in range(args.warmup):
         one_step(w)
-    for cls in range(4):
+    for cls in range(18):
         inst.kernel_stats(cls, reset=True)
     if pg:
         pg.barrier()
@@ -296,7 +402,7 @@ def main():
     dev_s = sum(r["dev_s"] for r in results)
     wall_s = sum(r["wall_s"] for r in results)
     tokens = sum(r["tokens"] for r in results)
-    stats = {cls: inst.kernel_stats(cls) for cls in range(4)}
+    stats = {cls: inst.kernel_stats(cls) for cls in range(18)}
     timed_rows = inst.iter_log()[log0:]
     if args.iter_log and rank == 0:
         np.save(args.iter_log, inst.iter_log())
@@ -319,40 +425,7 @@ def main():
                   "definition": "sum over the executed iterations of (per GEMM max(weight bytes/HBM, "
                                 "flops/bf16 sustained) + KV bytes/HBM + prefill attention flops/bf16); "
                                 "measured = sum of the iterations' device time (this rank)"}
-    roof, other = None, None
-    if stats[3]["ms"] > 0:
-        # per-kernel CUDA events are recorded on a 1-in-32 sample of the timed
-        # iterations (events between kernels would defeat the PDL overlap);
-        # shares are relative to the device time of those same iterations
-        names = {0: "decode_attention (K1+K2, paged split-K)", 1: "tcgen05 GEMMs (QKV/O/gate-up/down/LM head)"}
-        dom = max((0, 1), key=lambda c: stats[c]["ms"])
-        st = stats[dom]
-        # The GEMM class spans both regimes (weight streaming at small b, tensor
-        # bound at b ~ 256 and in prefill): each timed launch's roofline time is
-        # max(bytes / HBM, flops / sustained bf16); frac = sum(roofline) / sum(measured).
-        roof_ms = inst.kernel_roofline_ms(dom)
-        frac = roof_ms / st["ms"]
-        hbm_share = st["bytes"] / (peaks["hbm_gbs"] * 1e6) / max(roof_ms, 1e-9)
-        bound = "hbm" if hbm_share >= 0.5 else "tensor"
-        if bound == "hbm":
-            achieved, peak, unit = st["bytes"] / (st["ms"] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"
-        else:
-            achieved, peak, unit = st["flops"] / (st["ms"] / 1e3) / 1e12, peaks["bf16_tflops_sustained"], "TFLOP/s"
-        roof = {"kernel": names[dom], "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
-                "frac": round(frac, 4), "frac_definition": "sum over timed launches of max(bytes/HBM, flops/bf16 "
-                "sustained) / measured time", "traffic": None,
-                "traffic_source": "per-shape ncu --set full captures in profiles/r01c_ncu_full_summary.csv "
-                                  "(one number for the mixed-shape GEMM class would not be per launch): decode "
-                                  "GEMMs read their algorithmic bytes within 3% (O-proj split-K +13%); the "
-                                  "prefill gate_up at T=8192 reads its weights ~3.4x (1.13 GB vs 0.33 GB) while "
-                                  "tensor-bound at 1.43 PF/s", "peak_source": peaks["_source"],
-                "launches_sampled": st["launches"], "share_of_step": round(st["ms"] / stats[3]["ms"], 4),
-                "timing": "CUDA events on the engine stream, 1 in 32 iterations of the timed region"}
-        other = {("decode_attention" if c == 0 else "gemm" if c == 1 else "prefill_attention"):
-                 {"ms_sampled": round(stats[c]["ms"], 1), "share": round(stats[c]["ms"] / stats[3]["ms"], 4),
-                  "roofline_frac": round(inst.kernel_roofline_ms(c) / max(stats[c]["ms"], 1e-9), 4),
-                  "GB/s": round(stats[c]["bytes"] / max(stats[c]["ms"], 1e-9) / 1e6, 1),
-                  "TFLOP/s": round(stats[c]["flops"] / max(stats[c]["ms"], 1e-9) / 1e9, 1)} for c in range(3)}
+    roof, kernels = kernel_roofline(inst, stats, peaks, len(timed_rows), dev_s)
     line = {
         "metric": "generated_tokens_per_s",
         "value": round(tokens / dev_s, 1),
@@ -381,13 +454,15 @@ def main():
         "gpu_launches": int(sum(r["launches"] for r in results)),
         "roofline": roof,
         "batch_roofline": batch_roof,
-        "kernels": other,
+        "kernels": kernels,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
-        cb = cpu_oracle_sample(shape)
-        line["cpu_baseline"] = {"value": round(cb["value"], 4), "unit": "tokens/s", "cores": cb["cores"],
-                                "kind": "oracle", "sample": cb["sample"]}
+        cb = cpu_oracle_sample(shape, cfg)
+        line["cpu_baseline"] = {"value": round(1.0 / cb["per_token_s"], 4), "unit": "tokens/s", "cores": cb["cores"],
+                                "kind": "oracle", "sample": cb["sample"],
+                                "b_B_iteration_s": round(cb["b_B_iteration_s"], 2),
+                                "host_plane": host_plane_timing(make_batch(0), cfg, inst.n_pages, shape)}
     print(json.dumps(line), flush=True)
     if pg:
         pg.destroy_process_group()

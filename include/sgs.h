@@ -65,8 +65,12 @@ enum {
   SGS_F_NO_GRAPHS = 2,       /* launch the decode iteration eagerly (no CUDA graphs) */
   SGS_F_KERNEL_TIMING = 4,   /* CUDA-event timing per kernel class (sgs_kernel_stats) */
   SGS_F_SHADOW_WEIGHTS = 8,  /* reserve a second weight buffer for the asynchronous weight sync */
-  SGS_F_TRACE = 16           /* keep the schedule trace (sgs_trace) and every sample record; off by
+  SGS_F_TRACE = 16,          /* keep the schedule trace (sgs_trace) and every sample record; off by
                                 default: without it the host state is bounded by the samples in flight */
+  SGS_F_DETERMINISTIC = 32,  /* no split-K in the GEMMs: bitwise run-to-run reproducible results
+                                (split-K's fp32 red.add order is the only variation, R21) */
+  SGS_F_SKIP_PREFILL = 64    /* T(b) profiling only (config 5): admitted prompts are not prefilled (stale
+                                KV, garbage tokens); decode iterations and their timing are unchanged */
 };
 
 typedef struct {
@@ -255,12 +259,19 @@ sgs_status sgs_debug_forward(sgs_handle* h, const int32_t* tokens, int32_t T, fl
 /* Layer-local parity hook: run decoder layer `layer` of the CUDA path (prefill
  * form, positions 0..T-1, slot 0, idle handle only) on the fp32 residual
  * stream h_in (host [T x d_model]) and return the stream after the layer's
- * MLP residual add in h_out (host [T x d_model]). */
+ * MLP residual add in h_out (host [T x d_model]).  layer == n_layers runs the
+ * final RMSNorm + LM head on h_in instead: h_out is then fp32 logits
+ * (host [T x vocab]). */
 sgs_status sgs_debug_layer(sgs_handle* h, int32_t layer, const float* h_in, int32_t T, float* h_out);
 
 /* Device-side timing of the last iteration's kernels (CUDA events), ms. */
 sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms);
-/* Per kernel class (0 decode attention K1+K2, 1 GEMMs, 2 prefill attention),
+/* Per kernel class (0 decode attention K1+K2, 1 decode GEMMs, 2 prefill
+ * attention, 3 device time of the timed iterations, 4 prefill GEMMs, 5 other
+ * decode kernels: RMSNorm, RoPE + KV append, embedding, sampler; the timed
+ * iterations are ~1 in 64, chosen by a hash of the iteration counter); add 6
+ * for the timed iterations with >= 129 decode rows only, 12 for those with
+ * 1..32,
  * accumulated with SGS_F_KERNEL_TIMING: device ms (CUDA events on the
  * launching stream), algorithmic bytes and flops, launches.  reset != 0 clears. */
 sgs_status sgs_kernel_stats(sgs_handle* h, int32_t cls, double* ms, double* bytes, double* flops, int64_t* launches,
@@ -307,6 +318,17 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
                                    int32_t b, int32_t nq, int32_t nkv, int32_t hd, int32_t page,
                                    int32_t max_pages_per_seq, int32_t max_ctx_hint, void* out, int32_t out_fp32,
                                    void* workspace, int64_t workspace_bytes, int32_t split_pages, void* stream);
+
+/* Config-5 measurement of the same kernel (no data-dependent host work in the
+ * timed region): plans the work list once, launches the kernel reps times on
+ * stream with CUDA events around each launch, writing l2_flush_bytes of
+ * l2_flush (device scratch, may be NULL/0) between launches so that each
+ * launch reads its KV from HBM; *ms = mean device time per launch. */
+sgs_status sgs_op_decode_attention_timed(const void* q, const void* kv, const int32_t* block_table,
+                                         const int32_t* ctx, int32_t b, int32_t nq, int32_t nkv, int32_t hd,
+                                         int32_t page, int32_t max_pages_per_seq, void* out, void* workspace,
+                                         int64_t workspace_bytes, int32_t reps, void* l2_flush,
+                                         int64_t l2_flush_bytes, float* ms, void* stream);
 
 /* K3/K4: tcgen05 bf16 GEMM, C[t, n] (+)= sum_k X[t, k] * W[n, k].
  * W device bf16 [N, K] row-major; X device bf16 [T, K]; C device fp32 [T, ldc].

@@ -12,6 +12,7 @@ Functions and the paper passages they follow (PAPER.md line numbers):
   min_merge_gain   C3  lemma T(x+y) < T(x)+T(y)
   brute_force      C4  LF vs all admission orders
   attention        C7  naive softmax attention, fp64
+  decoder_layer/head  C6  one layer / final norm + LM head    (chained layer-local parity)
   decoder_forward  C6  teacher-forced Qwen2.5-shaped decoder   P:1032-1049  (parity unpinned end to end;
                                                                               components pinned)
   gen_tensor       K11 counter-based weight generator
@@ -93,6 +94,8 @@ def _declare(L):
     L.oracle_decoder_dump.argtypes = [P_i32, P_f64, ctypes.c_uint64, P_i32, ctypes.c_int32, P_f64]
     L.oracle_decoder_dump.restype = ctypes.c_int32
     L.oracle_decoder_layer.argtypes = [P_i32, P_f64, ctypes.c_uint64, ctypes.c_int32, P_f64, ctypes.c_int32, P_f64]
+    L.oracle_weight_cache.argtypes = [ctypes.c_int32]
+    L.oracle_decoder_head.argtypes = [P_i32, P_f64, ctypes.c_uint64, P_f64, ctypes.c_int32, P_f64]
     L.oracle_rmsnorm.argtypes = [P_f64, P_f32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P_f64]
     L.oracle_rope.argtypes = [P_f64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
     L.oracle_argmax.argtypes = [P_f32, ctypes.c_int64]
@@ -320,6 +323,22 @@ def decoder_layer(shape, seed: int, layer: int, h_in):
     out = np.zeros_like(h)
     lib().oracle_decoder_layer(_p(ci, P_i32), _p(cd, P_f64), seed, layer, _p(h, P_f64), h.shape[0], _p(out, P_f64))
     return out
+
+
+def decoder_head(shape, seed: int, h_in):
+    """Final RMSNorm + LM head on the residual stream h_in [T, d] -> logits [T, V] float64."""
+    h = np.ascontiguousarray(h_in, np.float64)
+    ci = np.array([shape.n_layers, shape.d_model, shape.n_q_heads, shape.n_kv_heads, shape.head_dim,
+                   shape.d_ffn, shape.vocab], np.int32)
+    cd = np.array([shape.rms_eps, shape.rope_theta], np.float64)
+    out = np.zeros((h.shape[0], shape.vocab), np.float64)
+    lib().oracle_decoder_head(_p(ci, P_i32), _p(cd, P_f64), seed, _p(h, P_f64), h.shape[0], _p(out, P_f64))
+    return out
+
+
+def weight_cache(on: bool):
+    """Memoise generated weight tensors (same values; timing runs build the weights once)."""
+    lib().oracle_weight_cache(int(on))
 
 
 def argmax(x) -> int:

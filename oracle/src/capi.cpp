@@ -161,6 +161,15 @@ int32_t oracle_decoder_dump(const int32_t* cfg_i, const double* cfg_d, uint64_t 
   }
 }
 
+void oracle_weight_cache(int32_t on) { weight_cache(on); }
+
+int32_t oracle_decoder_head(const int32_t* cfg_i, const double* cfg_d, uint64_t seed, const double* h_in, int32_t T,
+                            double* logits) {
+  ModelCfg c{cfg_i[0], cfg_i[1], cfg_i[2], cfg_i[3], cfg_i[4], cfg_i[5], cfg_i[6], cfg_d[0], cfg_d[1]};
+  decoder_head(c, seed, h_in, T, logits);
+  return 0;
+}
+
 int32_t oracle_decoder_layer(const int32_t* cfg_i, const double* cfg_d, uint64_t seed, int32_t layer,
                              const double* h_in, int32_t T, double* h_out) {
   ModelCfg c{cfg_i[0], cfg_i[1], cfg_i[2], cfg_i[3], cfg_i[4], cfg_i[5], cfg_i[6], cfg_d[0], cfg_d[1]};

@@ -114,6 +114,8 @@ void decoder_forward(const ModelCfg& c, uint64_t seed, const int32_t* tokens, in
 
 // one layer (layer-local parity): h_out = layer(h_in), positions 0..T-1
 void decoder_layer(const ModelCfg& c, uint64_t seed, int layer, const double* h_in, int T, double* h_out);
+void weight_cache(int on);
+void decoder_head(const ModelCfg& c, uint64_t seed, const double* h_in, int T, double* logits);
 int32_t argmax_lowest(const float* x, int64_t n);
 void philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 int32_t sample_top_p(const float* logits, int64_t V, float temperature, float top_p, uint64_t seed,

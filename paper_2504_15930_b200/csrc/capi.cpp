@@ -185,7 +185,7 @@ sgs_status sgs_debug_forward(sgs_handle* h, const int32_t* tokens, int32_t T, fl
 }
 
 sgs_status sgs_debug_layer(sgs_handle* h, int32_t layer, const float* h_in, int32_t T, float* h_out) {
-  if (!h || !h_in || !h_out || layer < 0) return SGS_E_INVAL;
+  if (!h || !h_in || !h_out || layer < 0 || layer > h->eng.n_layers()) return SGS_E_INVAL;
   return h->eng.debug_forward(nullptr, T, h_out, layer, h_in);
 }
 
@@ -197,7 +197,7 @@ sgs_status sgs_last_iter_ms(sgs_handle* h, float* ms) {
 
 sgs_status sgs_kernel_stats(sgs_handle* h, int32_t cls, double* ms, double* bytes, double* flops, int64_t* launches,
                             int32_t reset) {
-  if (!h || cls < 0 || cls > 3) return SGS_E_INVAL;
+  if (!h || cls < 0 || cls >= sgs::Engine::kClasses * sgs::Engine::kPhases) return SGS_E_INVAL;
   auto& E = h->eng;
   if (ms) *ms = E.kstat_ms[cls];
   if (bytes) *bytes = E.kstat_bytes[cls];
@@ -215,7 +215,7 @@ sgs_status sgs_set_roofline(sgs_handle* h, double bw_gbs, double tflops) {
 }
 
 sgs_status sgs_kernel_roofline_ms(const sgs_handle* h, int32_t cls, double* ms) {
-  if (!h || !ms || cls < 0 || cls > 3) return SGS_E_INVAL;
+  if (!h || !ms || cls < 0 || cls >= sgs::Engine::kClasses * sgs::Engine::kPhases) return SGS_E_INVAL;
   *ms = h->eng.kstat_roof_ms[cls];
   return SGS_OK;
 }
@@ -309,6 +309,65 @@ sgs_status sgs_op_decode_attention(const void* q, const void* kv, const int32_t*
                                    (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, out_fp32,
                                    part_o, part_ml, arrive, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host plan vectors die here
+  return cuda_status(e);
+}
+
+sgs_status sgs_op_decode_attention_timed(const void* q, const void* kv, const int32_t* block_table,
+                                         const int32_t* ctx, int32_t b, int32_t nq, int32_t nkv, int32_t hd,
+                                         int32_t page, int32_t max_pages_per_seq, void* out, void* workspace,
+                                         int64_t workspace_bytes, int32_t reps, void* l2_flush,
+                                         int64_t l2_flush_bytes, float* ms, void* stream) {
+  if (b <= 0 || reps <= 0 || !ms) return SGS_E_INVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<int32_t> hctx(b);
+  if (cudaMemcpyAsync(hctx.data(), ctx, (size_t)b * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return SGS_E_CUDA;
+  for (int i = 0; i < b; ++i)
+    if (hctx[i] < 1 || (hctx[i] + page - 1) / page > max_pages_per_seq) return SGS_E_INVAL;
+  sgs::AttnPlan plan;
+  sgs::attn_plan(hctx.data(), nullptr, b, nkv, page, 0, &plan);
+  const int g = nq / nkv;
+  if (sgs::attn_workspace_bytes((int)plan.items.size(), plan.n_parts, g, hd) > workspace_bytes) return SGS_E_NOMEM;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  auto* d_items = reinterpret_cast<sgs::AttnItem*>(ws);
+  auto* d_combs = reinterpret_cast<sgs::AttnComb*>(ws + plan.items.size() * sizeof(sgs::AttnItem));
+  size_t off = plan.items.size() * sizeof(sgs::AttnItem) + plan.combs.size() * sizeof(sgs::AttnComb);
+  off = (off + 255) / 256 * 256;
+  float* part_o = reinterpret_cast<float*>(ws + off);
+  float* part_ml = part_o + (size_t)std::max(plan.n_parts, 1) * g * hd;
+  int* arrive = reinterpret_cast<int*>(part_ml + (size_t)std::max(plan.n_parts, 1) * g * 2);
+  cudaError_t e = cudaMemcpyAsync(d_items, plan.items.data(), plan.items.size() * sizeof(sgs::AttnItem),
+                                  cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !plan.combs.empty())
+    e = cudaMemcpyAsync(d_combs, plan.combs.data(), plan.combs.size() * sizeof(sgs::AttnComb),
+                        cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !plan.combs.empty()) e = cudaMemsetAsync(arrive, 0, plan.combs.size() * sizeof(int), st);
+  auto launch = [&]() {
+    return sgs::attn_decode(q, kv, block_table, nullptr, d_items, (int)plan.items.size(), d_combs,
+                            (int)plan.combs.size(), nq, nkv, hd, page, max_pages_per_seq, out, 0, part_o, part_ml,
+                            arrive, st);
+  };
+  if (e == cudaSuccess) e = launch();  // warm-up
+  std::vector<cudaEvent_t> ev(2 * (size_t)reps, nullptr);
+  for (auto& x : ev)
+    if (e == cudaSuccess) e = cudaEventCreate(&x);
+  for (int r = 0; r < reps && e == cudaSuccess; ++r) {
+    if (l2_flush && l2_flush_bytes > 0) e = cudaMemsetAsync(l2_flush, r & 0xff, (size_t)l2_flush_bytes, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2 * r], st);
+    if (e == cudaSuccess) e = launch();
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2 * r + 1], st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  float tot = 0.f;
+  for (int r = 0; r < reps && e == cudaSuccess; ++r) {
+    float t = 0.f;
+    e = cudaEventElapsedTime(&t, ev[2 * r], ev[2 * r + 1]);
+    tot += t;
+  }
+  for (auto& x : ev)
+    if (x) cudaEventDestroy(x);
+  *ms = tot / reps;
   return cuda_status(e);
 }
 

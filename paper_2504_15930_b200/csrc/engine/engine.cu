@@ -530,23 +530,28 @@ cudaError_t Engine::kflush(const std::vector<KRec>& recs, int rows) {
     cudaError_t e = cudaEventElapsedTime(&ms, r.a, r.b);
     if (e != cudaSuccess) return e;
     const int n = r.rows < 0 ? rows : r.rows;
-    kstat_ms[r.cls] += ms;
-    kstat_bytes[r.cls] += r.bfix < 0 ? cur_attn_bytes_ : r.bfix + r.brow * n;
     const double by = r.bfix < 0 ? cur_attn_bytes_ : r.bfix + r.brow * n;
     const double fl = r.bfix < 0 ? cur_attn_flops_ : r.frow * n;
-    kstat_flops[r.cls] += fl;
-    if (roof_bw_gbs > 0 && roof_tflops > 0)
-      kstat_roof_ms[r.cls] += std::max(by / (roof_bw_gbs * 1e6), fl / (roof_tflops * 1e9));
-    kstat_n[r.cls] += 1;
+    auto add = [&](int k) {
+      kstat_ms[k] += ms;
+      kstat_bytes[k] += by;
+      kstat_flops[k] += fl;
+      if (roof_bw_gbs > 0 && roof_tflops > 0)
+        kstat_roof_ms[k] += std::max(by / (roof_bw_gbs * 1e6), fl / (roof_tflops * 1e9));
+      kstat_n[k] += 1;
+    };
+    add(r.cls);
+    if (cur_phase_) add(r.cls + kClasses * cur_phase_);
   }
   return cudaSuccess;
 }
 
 cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate) {
-  const int splits = gemm_auto_splits(N, K, T);
+  // SGS_F_DETERMINISTIC: no split-K (the fp32 red.add order is the only run-to-run variation, R21)
+  const int splits = (e_.flags & SGS_F_DETERMINISTIC) ? 1 : gemm_auto_splits(N, K, T);
   cudaError_t e;
   KRec kr;
-  ktic(&kr, 1);
+  ktic(&kr, gemm_cls_);
   if (splits > 1) {
     // qkv_ and gu_ are kept zeroed by their consumers (rope_append, silu_mul)
     if (!accumulate && C != qkv_ && C != gu_) {
@@ -579,14 +584,14 @@ cudaError_t Engine::sample(const float* logits, int rows, const uint32_t* sid, c
 // 148 tiles), else the fp32 GEMM + the silu_mul kernel.
 cudaError_t Engine::gate_up(const void* W, int T) {
   const int d = m_.d_model, f = m_.d_ffn;
-  if (gemm_auto_splits(2 * f, d, T) > 1) {
+  if (!(e_.flags & SGS_F_DETERMINISTIC) && gemm_auto_splits(2 * f, d, T) > 1) {
     cudaError_t e = gemm(W, x_, gu_, 2 * f, d, T, false);
     if (e != cudaSuccess) return e;
     ++launches;
     return silu_mul(gu_, mm_, T, f, st_);
   }
   KRec kr;
-  ktic(&kr, 1);
+  ktic(&kr, gemm_cls_);
   cudaError_t e = gemm_bf16(W, x_, reinterpret_cast<float*>(mm_), 2 * f, d, T, f, 3, 1, st_);
   ktoc(&kr, 2.0 * 2 * f * d, 2.0 * d + 2.0 * f, 2.0 * 2 * f * d, T);
   ++launches;
@@ -622,7 +627,13 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   (void)qkvN, (void)f, (void)d, (void)n_adm;
   // per-kernel CUDA events on 1 in kTimingStride iterations: events between
   // kernels serialise them (no PDL overlap), so the others run untouched
-  timing_now_ = (e_.flags & SGS_F_KERNEL_TIMING) && (timing_iter_++ % kTimingStride == 0);
+  {
+    uint64_t z = (uint64_t)timing_iter_++ + 0x9E3779B97F4A7C15ull;  // splitmix64 of the counter
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    timing_now_ = (e_.flags & SGS_F_KERNEL_TIMING) && (z % kTimingStride == 0);
+  }
   // staging buffers and events of this iteration (the other pair may still be in flight)
   cur_buf_ ^= 1;
   meta_host_ = meta_bufs_[cur_buf_], tok_host_ = tok_bufs_[cur_buf_];
@@ -747,6 +758,10 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     CK(cudaStreamWaitEvent(st_pf_, ev_meta_, 0), "wait meta");
     std::swap(st_, st_pf_);
   }
+  // SGS_F_SKIP_PREFILL (T(b) profiling only): the admitted prompts' prefill is
+  // not computed; their pages keep stale KV and the first token is whatever
+  // the token history holds -- decode iterations run unchanged
+  if (e_.flags & SGS_F_SKIP_PREFILL) chunks.clear();
   for (auto& c : chunks) {
     {
       // causal self-attention of whole prompts: QK^T and PV over P(P+1)/2 pairs each
@@ -858,6 +873,7 @@ sgs_status Engine::finalize_front() {
   CK(cudaEventSynchronize(ev1s_[f.buf]), "iteration sync");
   CK(cudaEventElapsedTime(&last_ms, ev0s_[f.buf], ev1s_[f.buf]), "elapsed");
   if (f.timing) {
+    cur_phase_ = f.n_run >= 129 ? 1 : (f.n_run >= 1 && f.n_run <= 32 ? 2 : 0);
     CK(kflush(krec_, f.n_run), "kernel timing");
     krec_.clear();
     ev_used_ = 0;
@@ -867,6 +883,7 @@ sgs_status Engine::finalize_front() {
     }
     kstat_ms[3] += last_ms;  // slot 3: device time of the sampled iterations (for the kernel shares)
     kstat_n[3] += 1;
+    if (cur_phase_) kstat_ms[3 + kClasses * cur_phase_] += last_ms, kstat_n[3 + kClasses * cur_phase_] += 1;
   }
   iter_log.insert(iter_log.end(), {f.t, f.b, f.adm, f.pf_tok, f.sumctx, (int64_t)std::llround(last_ms * 1000.0)});
   const int32_t* tok = tok_bufs_[f.buf];
@@ -913,15 +930,26 @@ sgs_status Engine::decode_body(int Bk) {
   // SGS_DEBUG_SKIP (timing ablation only; results are garbage): bit k skips
   // kernel class k of the decode program
   auto on = [&](int bit) { return !(skip_ & (1 << bit)); };
-  if (on(9)) CK(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), "embed");
+  // class-5 timing of the small kernels: algorithmic bytes per row
+  auto other = [&](cudaError_t e, KRec* kr, double brow) {
+    ktoc(kr, 0.0, brow, 0.0, Bk);
+    return e;
+  };
+  gemm_cls_ = 1;
+  KRec ko;
+  ktic(&ko, 5);
+  if (on(9)) CK(other(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), &ko, 6.0 * d), "embed");
   ++launches;
   for (int l = 0; l < m_.n_layers; ++l) {
     const Layer& Ly = layers_[l];
-    if (on(0)) CK(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm1");
+    ktic(&ko, 5);
+    if (on(0)) CK(other(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm1");
     if (on(1)) CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false), "gemm qkv");
+    ktic(&ko, 5);
     if (on(2))
-      CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, Bk, nq,
-                     nkv, hd, e_.page_size, st_),
+      CK(other(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, Bk,
+                           nq, nkv, hd, e_.page_size, st_),
+               &ko, 6.0 * qkvN),
          "rope_append");
     KRec kr;
     ktic(&kr, 0);
@@ -931,14 +959,17 @@ sgs_status Engine::decode_body(int Bk) {
          "attn_decode");
     ktoc(&kr, -1.0, 0.0, 0.0, 0);
     if (on(4)) CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
-    if (on(0)) CK(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm2");
+    ktic(&ko, 5);
+    if (on(0)) CK(other(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm2");
     if (on(5)) CK(gate_up(Ly.wgu, Bk), "gemm gate_up + SwiGLU");
     if (on(6)) CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
     launches += 4;  // rmsnorm x2, RoPE, attention; the GEMMs count themselves
   }
-  if (on(0)) CK(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), "rmsnorm f");
+  ktic(&ko, 5);
+  if (on(0)) CK(other(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm f");
   if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
-  if (on(8)) CK(sample(logits_, Bk, d_sid, d_slot, d_tok), "sampler");
+  ktic(&ko, 5);
+  if (on(8)) CK(other(sample(logits_, Bk, d_sid, d_slot, d_tok), &ko, 4.0 * V), "sampler");
   launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }
@@ -997,6 +1028,11 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
             V = m_.vocab;
   const int qkvN = (nq + 2 * nkv) * hd;
   const int np = (int)idx.size();
+  gemm_cls_ = 4;
+  struct Restore {
+    int& c;
+    ~Restore() { c = 1; }
+  } restore_cls{gemm_cls_};
   int n_dump = 0;
   auto save = [&]() -> cudaError_t {
     if (!dump || only_layer >= 0) return cudaSuccess;  // layer-local mode returns only the final h
@@ -1046,6 +1082,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
 // Standalone prefill forward of one prompt in slot 0 (idle handle only) with
 // the residual stream dumped after the embedding and every residual add.
 sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, int layer, const float* h_in) {
+  if (layer == m_.n_layers && h_in && dump && !null_ && T > 0) return debug_head(h_in, T, dump);
   if (layer >= m_.n_layers || (layer >= 0 && !h_in) || (layer < 0 && !tokens)) {
     err = "debug_forward: bad layer / input";
     return SGS_E_INVAL;
@@ -1090,6 +1127,30 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, 
                                MD + o_last, MD + o_last + 1, MD + o_last + 2, T, dump, layer, h_in);
   if (s != SGS_OK) return s;
   CK(cudaStreamSynchronize(st_), "debug sync");
+  return SGS_OK;
+}
+
+// Final RMSNorm + LM head of the CUDA path on a given fp32 residual stream
+// (host [T x d]) -> fp32 logits (host [T x V]), in chunks of the logits buffer.
+sgs_status Engine::debug_head(const float* h_in, int32_t T, float* logits) {
+  if (!sched.idle()) {
+    err = "debug_head needs an idle handle";
+    return SGS_E_STATE;
+  }
+  {
+    sgs_status ds = drain();
+    if (ds != SGS_OK) return ds;
+  }
+  const int d = m_.d_model, V = m_.vocab;
+  const int R = std::min(L_.tmax, (e_.max_batch + 15) / 16 * 16 + e_.max_batch);
+  for (int r0 = 0; r0 < T; r0 += R) {
+    const int n = std::min(R, T - r0);
+    CK(cudaMemcpyAsync(h_, h_in + (size_t)r0 * d, (size_t)n * d * 4, cudaMemcpyHostToDevice, st_), "h_in");
+    CK(rmsnorm(h_, nf_, x_, nullptr, n, d, m_.rms_eps, st_), "rmsnorm f");
+    CK(gemm(lm_head_, x_, logits_, V, d, n, false), "gemm lm_head");
+    CK(cudaMemcpyAsync(logits + (size_t)r0 * V, logits_, (size_t)n * V * 4, cudaMemcpyDeviceToHost, st_), "logits");
+    CK(cudaStreamSynchronize(st_), "debug head sync");
+  }
   return SGS_OK;
 }
 

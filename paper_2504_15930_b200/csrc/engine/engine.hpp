@@ -64,6 +64,7 @@ class Engine {
   sgs_status update_weights_begin(int root);
   sgs_status update_weights_ready(int32_t* ready);
   sgs_status update_weights_commit();
+  sgs_status debug_head(const float* h_in, int32_t T, float* logits);
   sgs_status last_logits(float* logits, uint64_t* ids, int32_t* tok_idx, int32_t cap, int32_t* rows);
   sgs_status debug_forward(const int32_t* tokens, int32_t T, float* dump, int layer = -1,
                            const float* h_in = nullptr);
@@ -75,13 +76,21 @@ class Engine {
   Scheduler sched;
   float last_ms = 0.f;
   // kernel-class timing (SGS_F_KERNEL_TIMING) and I/O accounting
-  double kstat_ms[4] = {0}, kstat_bytes[4] = {0}, kstat_flops[4] = {0};
-  int64_t kstat_n[4] = {0};
+  // classes: 0 decode attention, 1 decode GEMMs, 2 prefill attention, 3 device
+  // time of the sampled iterations, 4 prefill GEMMs, 5 other decode kernels
+  // (RMSNorm, RoPE + KV append, embedding, sampler)
+  // (index cls + kClasses * phase; phase 0 every sampled iteration, 1 those
+  // with >= 129 decode rows, 2 those with 1..32)
+  static constexpr int kClasses = 6, kPhases = 3;
+  double kstat_ms[kClasses * kPhases] = {0}, kstat_bytes[kClasses * kPhases] = {0},
+         kstat_flops[kClasses * kPhases] = {0};
+  int64_t kstat_n[kClasses * kPhases] = {0};
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   // per-iteration log (T(b) profiling, a16): t, b, admitted, prefill tokens, sum ctx, device us
   std::vector<int64_t> iter_log;
   // roofline time of the timed launches: sum_k max(bytes_k / BW, flops_k / F) (sgs_set_roofline)
-  double roof_bw_gbs = 0, roof_tflops = 0, kstat_roof_ms[4] = {0};
+  double roof_bw_gbs = 0, roof_tflops = 0, kstat_roof_ms[kClasses * kPhases] = {0};
+  int cur_phase_ = 0;
   int64_t launches = 0;
   int32_t version = 0;
 
@@ -127,7 +136,11 @@ class Engine {
   bool timing_now_ = false;             // this iteration is a timing sample
   int skip_ = 0;                        // SGS_DEBUG_SKIP ablation mask (decode program)
   int64_t timing_iter_ = 0;
-  static constexpr int kTimingStride = 32;  // 1 in 32 iterations carries the per-kernel events
+  // about 1 in 64 iterations carries the per-kernel events, chosen by a hash of
+  // the iteration counter (a fixed stride would alias with the schedule: every
+  // config-2 batch has a multiple of 32 iterations, so t = 0 would always be sampled)
+  static constexpr int kTimingStride = 64;
+  int gemm_cls_ = 1;  // 1 while the decode program is issued, 4 in prefill chunks
   std::vector<KRec>* rec_target_ = nullptr;  // non-null while capturing
   double cur_attn_bytes_ = 0, cur_attn_flops_ = 0;
   double cur_pf_attn_flops_ = 0;  // causal attention flops of the prefill chunk being issued
@@ -190,6 +203,7 @@ class Engine {
   sgs_status finalize_front();
  public:
   sgs_status drain();  // finalize every in-flight iteration (before weight updates, debug calls, ...)
+  int n_layers() const { return m_.n_layers; }
   int64_t live_ids() const { return (int64_t)live_ids_.size(); }
   int64_t inflight_samples() const {
     int64_t n = 0;

@@ -21,6 +21,8 @@ F_NO_GRAPHS = 2
 F_KERNEL_TIMING = 4
 F_SHADOW_WEIGHTS = 8
 F_TRACE = 16
+F_DETERMINISTIC = 32
+F_SKIP_PREFILL = 64
 
 # every symbol include/sgs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
@@ -34,6 +36,7 @@ EXPORTS = [
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
     "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer", "sgs_op_sample_top_p",
     "sgs_weight_tensors", "sgs_stage_weights", "sgs_prefill_workspace_bytes", "sgs_host_state",
+    "sgs_op_decode_attention_timed",
 ]
 
 
@@ -132,6 +135,8 @@ def _declare(L):
     L.sgs_attn_workspace_bytes.restype = i64
     L.sgs_op_decode_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, i32, vp, i64, i32,
                                           vp]
+    L.sgs_op_decode_attention_timed.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, i64, i32, vp,
+                                                i64, P(ctypes.c_float), vp]
     L.sgs_op_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp]
     L.sgs_op_rmsnorm.argtypes = [vp, vp, vp, i32, i32, ctypes.c_float, vp]
     L.sgs_op_rope_append.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
@@ -412,6 +417,14 @@ class Instance:
                                      out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))), self.h)
         return out
 
+    def debug_head(self, h_in) -> np.ndarray:
+        """Final RMSNorm + LM head of the CUDA path on h_in [T, d] -> fp32 logits [T, V]."""
+        h = np.ascontiguousarray(h_in, np.float32)
+        out = np.zeros((h.shape[0], self.shape.vocab), np.float32)
+        _check(lib().sgs_debug_layer(self.h, self.shape.n_layers, h.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                     h.shape[0], out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))), self.h)
+        return out
+
     def last_iter_ms(self) -> float:
         v = ctypes.c_float()
         _check(lib().sgs_last_iter_ms(self.h, ctypes.byref(v)), self.h)
@@ -559,6 +572,23 @@ def op_decode_attention(q, kv, block_table, ctx, out, page=16, split_pages=0, wo
     _check(lib().sgs_op_decode_attention(_ptr(q), _ptr(kv), _ptr(block_table), _ptr(ctx), b, nq, nkv, hd, page, maxp,
                                          0, _ptr(out), out_fp32, _ptr(workspace), workspace.numel(), split_pages,
                                          _cur_stream(q)))
+
+
+def op_decode_attention_timed(q, kv, block_table, ctx, out, reps=10, l2_flush=None, page=16, workspace=None):
+    """Mean device ms per launch of the decode-attention kernel (plan built once)."""
+    import torch
+    b, nq, hd = q.shape
+    nkv = kv.shape[1]
+    maxp = block_table.shape[1]
+    need = lib().sgs_attn_workspace_bytes(b, nq, nkv, hd, maxp)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    ms = ctypes.c_float()
+    _check(lib().sgs_op_decode_attention_timed(_ptr(q), _ptr(kv), _ptr(block_table), _ptr(ctx), b, nq, nkv, hd, page,
+                                               maxp, _ptr(out), _ptr(workspace), workspace.numel(), reps,
+                                               _ptr(l2_flush), 0 if l2_flush is None else l2_flush.numel(),
+                                               ctypes.byref(ms), _cur_stream(q)))
+    return ms.value
 
 
 # -------------------------------------------------------------------- KV page layout (DESIGN.md §6)

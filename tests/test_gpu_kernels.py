@@ -89,6 +89,8 @@ def _rel_err(got, ref):
     (4, 2, 32, [1, 15, 16, 17, 255, 272]),            # tiny
     (28, 4, 128, [1, 16, 33, 500, 1024, 4097]),       # 7B (g = 7)
     (40, 8, 128, [7, 300, 2048, 8704]),               # 14B/32B (g = 5)
+    (28, 4, 128, [16896, 32768]),                     # config-4 / config-5 long contexts (7B heads)
+    (40, 8, 128, [16896, 32768, 1]),                  # config-4 shape (14B/32B heads)
 ])
 @pytest.mark.parametrize("split", [0, 1, 3])
 def test_decode_attention_vs_fp64(sgs, nq, nkv, hd, ctxs, split):

@@ -242,6 +242,9 @@ def test_decoder_layer_composes_to_forward():
     dump = oracle.decoder_dump(shape, 9, toks)
     for l in range(shape.n_layers):
         assert np.array_equal(oracle.decoder_layer(shape, 9, l, dump[2 * l]), dump[2 * l + 2])
+    # and the head on the final stream is the forward's logits
+    assert np.array_equal(oracle.decoder_head(shape, 9, dump[-1]),
+                          oracle.decoder_forward(shape, 9, toks.astype(np.int32), first_row=0))
 
 
 def test_top_p_nucleus_golden():
