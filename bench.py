@@ -30,13 +30,14 @@ import numpy as np  # noqa: E402
 import workload  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-# T(b) profiles (t0_ns, k0_ps, b_star, k1_ps) used by Alg. 2's Eq. 2; fitted by tools/tb_sweep.py
-# (config 5) on B200 — profiles/r01_tb_sweep_{7b,14b,32b}.json (the ctx=2048 fits).  Only the
-# dispatch (N > 1) reads them.
+# T(b) profiles (t0_ns, k0_ps, b_star, k1_ps) used by Alg. 2's Eq. 2: the r02 config-5 sweeps on the
+# current kernels (profiles/r02/tb_sweep_*.json, tools/tb_sweep.py), each the valid fit (R24) at the
+# grid context nearest the workload's mean context (R23; tools/pick_profiles.py).  Only the dispatch
+# (N > 1) reads them.
 DEFAULT_PROFILES = {
-    "qwen2.5-7b": (3491220, 29544576, 128, 38479949),
-    "qwen2.5-14b": (5987575, 73237116, 160, 71301394),
-    "qwen2.5-32b": (11988370, 88930482, 32, 107212340),
+    "qwen2.5-7b": (2737741, 15064935, 192, 19922457),     # ctx 1024
+    "qwen2.5-14b": (5245282, 39388098, 128, 61477016),    # ctx 1024
+    "qwen2.5-32b": (11387520, 59009897, 16, 99386761),    # ctx 2048
     "tiny": (200, 100, 64, 400),
 }
 

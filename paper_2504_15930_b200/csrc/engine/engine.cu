@@ -92,6 +92,7 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->attn_bytes = max_items * (nq / nkv) * (hd + 2) * 4 + max_items * 4;  // partials + arrival counters
   L->off_attn = take(L->attn_bytes);
   L->off_cksum = take(64);
+  L->off_amax = take(((B + 15) / 16 * 16) * 8 + 64);
   L->scratch_bytes = o - s0;
   L->off_shadow = (e.flags & SGS_F_SHADOW_WEIGHTS) ? take(L->weights_bytes) : -1;
   L->total = o;
@@ -265,6 +266,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   meta_dev_ = arena_ + L_.off_meta;
   attn_ws_ = arena_ + L_.off_attn;
   cksum_dev_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_cksum);
+  amax_keys_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_amax);
   tok_host_cap_ = (int64_t)e.max_batch * max_gen_;
   for (int k = 0; k < 2; ++k) {
     CK(cudaMallocHost(&meta_bufs_[k], L_.meta_bytes), "cudaMallocHost(meta)");
@@ -290,6 +292,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   CK(cudaEventCreateWithFlags(&ev_meta_, cudaEventDisableTiming), "event");
   CK(cudaEventCreateWithFlags(&ev_pf_, cudaEventDisableTiming), "event");
   CK(cudaMemsetAsync(attn_ws_, 0, L_.attn_bytes, st_), "memset attention workspace");
+  CK(cudaMemsetAsync(amax_keys_, 0, ((e.max_batch + 15) / 16 * 16) * 8 + 64, st_), "memset argmax keys");
   // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
   {
     const int half = m.head_dim / 2;
@@ -967,9 +970,25 @@ sgs_status Engine::decode_body(int Bk) {
   }
   ktic(&ko, 5);
   if (on(0)) CK(other(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm f");
-  if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
-  ktic(&ko, 5);
-  if (on(8)) CK(other(sample(logits_, Bk, d_sid, d_slot, d_tok), &ko, 4.0 * V), "sampler");
+  if (e_.sampling == SGS_SAMPLE_GREEDY) {
+    // LM head with greedy sampling fused into its epilogue (GEMM mode 4): no
+    // fp32 logits round trip and no sampler launch; the logits are still
+    // written for SGS_F_KEEP_LOGITS (same values, so the tests see the argmax
+    // of exactly what was sampled)
+    const bool keep = (e_.flags & SGS_F_KEEP_LOGITS) != 0;
+    const int Bpad = (e_.max_batch + 15) / 16 * 16;
+    ArgmaxArgs am{amax_keys_, reinterpret_cast<unsigned int*>(amax_keys_ + Bpad), d_slot, d_tok, last_tok_, hist_,
+                  max_gen_};
+    KRec kr;
+    ktic(&kr, gemm_cls_);
+    if (on(7)) CK(gemm_bf16(lm_head_, x_, keep ? logits_ : nullptr, V, d, Bk, V, 4, 1, st_, &am), "gemm lm_head");
+    ktoc(&kr, 2.0 * V * d, 2.0 * d + (keep ? 4.0 * V : 0.0), 2.0 * V * d, Bk);
+    launches += 1;
+  } else {
+    if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
+    ktic(&ko, 5);
+    if (on(8)) CK(other(sample(logits_, Bk, d_sid, d_slot, d_tok), &ko, 4.0 * V), "sampler");
+  }
   launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }

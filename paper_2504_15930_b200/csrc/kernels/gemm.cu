@@ -12,6 +12,7 @@
 // tcgen05.mma, four epilogue warps read TMEM (tcgen05.ld) and write fp32
 // rows of C (coalesced: lane = output feature).  Split-K over gridDim.z with
 // fp32 red.add when mode == 1.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
                         int chunks_per_split, int tmem_cols, int n_acc, int acc_stride, int num_mp, int num_n,
-                        int units, int nbuf, int xbufs) {
+                        int units, int nbuf, int xbufs, const ArgmaxArgs am) {
   constexpr int mode = MODE, kcs = KCS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -265,6 +266,35 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[j]);
         }
+        if (mode == 4) {
+          // fused greedy sampling: per token, the (value desc, vocab index asc)
+          // maximum over this warp's 32 rows, then over the 4 epilogue warps
+          // (shared memory), then one 64-bit atomicMax per token and tile
+          const int feat = m0 + 32 * e + lane;
+          // [4][16] keys, after the exchange buffers (the store path below reuses those)
+          unsigned long long* sk = reinterpret_cast<unsigned long long*>(xch + (size_t)xbufs * 4 * 32 * 17);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t u = __float_as_uint(acc[j]);
+            const uint32_t ord = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+            unsigned long long key = ((unsigned long long)ord << 32) | (uint32_t)(~(uint32_t)feat);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+              key = ok > key ? ok : key;
+            }
+            if (lane == j) sk[e * 16 + j] = key;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (e == 0 && lane < 16 && n0 + c + lane < T) {
+            unsigned long long k = sk[lane];
+#pragma unroll
+            for (int w = 1; w < 4; ++w) k = sk[w * 16 + lane] > k ? sk[w * 16 + lane] : k;
+            atomicMax(am.keys + n0 + c + lane, k);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (C == nullptr) continue;
+        }
         if (mode == 3) {
           // fused SwiGLU: tile rows 0..63 are gate rows and 64..127 the up rows
           // of the same 64 features (warps 0-1: g, warps 2-3: u).  All four
@@ -304,7 +334,7 @@ __global__ void __launch_bounds__(256, 1)
             v.x = xt[(4 * qd + 0) * 17 + j], v.y = xt[(4 * qd + 1) * 17 + j];
             v.z = xt[(4 * qd + 2) * 17 + j], v.w = xt[(4 * qd + 3) * 17 + j];
             float* p = C + (size_t)t * ldc + m0 + 32 * e + 4 * qd;
-            if (mode == 0) {
+            if (mode == 0 || mode == 4) {
               *reinterpret_cast<float4*>(p) = v;
             } else if (mode == 1) {
               red_add_v4(p, v);
@@ -339,6 +369,29 @@ __global__ void __launch_bounds__(256, 1)
       tmem_dealloc_2sm(tmem, tmem_cols);
     else
       tmem_dealloc(tmem, tmem_cols);
+  }
+  if (mode == 4) {
+    // the last CTA to arrive turns the packed keys into tokens (all atomics of
+    // every CTA precede its fenced arrival)
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(am.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const unsigned long long k = atomicExch(am.keys + t, 0ull);
+        const int s = am.slot[t];
+        if (s >= 0) {
+          const int32_t tok = (int32_t)(~(uint32_t)k);
+          am.last_tok[s] = tok;
+          am.hist[(size_t)s * am.max_gen + am.tok_idx[t]] = tok;
+        }
+      }
+      if (threadIdx.x == 0) *am.done = 0u;
+    }
   }
 }
 
@@ -472,15 +525,19 @@ static cudaError_t launch_gemm(Kern kern, int cg, dim3 grid, size_t smem, cudaSt
 }
 
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, const ArgmaxArgs* am) {
   if (T <= 0) return cudaSuccess;
   if (N % GEMM_BM != 0 || K % GEMM_BK != 0) return cudaErrorInvalidValue;
-  const int BN = T >= 256 ? 256 : ((T + 15) / 16) * 16;
+  // SGS_GEMM_BN_CAP (experiments, tools/gemm_explore.py): largest token tile
+  static const int bn_cap = std::getenv("SGS_GEMM_BN_CAP") ? std::atoi(std::getenv("SGS_GEMM_BN_CAP")) : 256;
+  const int BN = std::min(bn_cap, T >= 256 ? 256 : ((T + 15) / 16) * 16);
   // CTA pairs for compute-bound token tiles (BN >= 128) when the 256-row pair tiles N
   const int CG = (BN >= 128 && N % (2 * GEMM_BM) == 0) ? 2 : 1;
   const int kc = K / GEMM_BK;
   if (splits <= 0) splits = mode == 1 ? gemm_auto_splits(N, K, T) : 1;
   if (splits > 1 && mode != 1) return cudaErrorInvalidValue;
+  if (mode == 4 && !am) return cudaErrorInvalidValue;
+  const ArgmaxArgs amv = am ? *am : ArgmaxArgs{};
   // decode-sized tiles (BN <= 128) use half the shared memory and TMEM so two
   // CTAs fit on an SM: the next tile (or the next GEMM, via PDL) streams its
   // weights while the current one drains
@@ -500,11 +557,12 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (stages > 12) stages = 12;
   const int kst = kc / kcs;  // stages-worth of chunks in the whole K
   if (stages > kst) stages = kst < 2 ? 2 : kst;
-  if (ldc % 4 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return cudaErrorInvalidValue;  // float4 epilogue
+  if (C && (ldc % 4 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0)) return cudaErrorInvalidValue;  // float4 epilogue
   // epilogue exchange: double-buffered for compute-bound tiles (mode 3 then
   // needs one barrier per 16-token chunk); decode tiles keep the smem for stages
   const int xbufs = small ? 1 : 2;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + (size_t)xbufs * 4 * 32 * 17 * 4;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + (size_t)xbufs * 4 * 32 * 17 * 4 +
+                      (mode == 4 ? 4 * 16 * 8 : 0);
   // persistent grid: one CTA (pair) per resident slot, at most one per unit
   const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
   const int units = num_mp * num_n * splits;
@@ -526,15 +584,17 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (nbuf == 2 && tmem_cols / 2 < n_acc * acc_stride) tmem_cols <<= 1;
   if (tmem_cols > 512) return cudaErrorInvalidValue;
   const dim3 grid(pairs * CG);
-  switch ((CG - 1) * 8 + mode * 2 + (kcs - 1)) {
+  switch ((CG - 1) * 10 + mode * 2 + (kcs - 1)) {
 #define SGS_GEMM_CASE(cg, md, kk)                                                                                     \
-  case (cg - 1) * 8 + md * 2 + (kk - 1):                                                                            \
+  case (cg - 1) * 10 + md * 2 + (kk - 1):                                                                           \
     return launch_gemm(gemm_bf16_tc_kernel<cg, md, kk>, cg, grid, smem, stream, tw, tx, C, T, ldc, BN, stages, kc, \
-                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs);
+                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs, amv);
     SGS_GEMM_CASE(1, 0, 1) SGS_GEMM_CASE(1, 0, 2) SGS_GEMM_CASE(1, 1, 1) SGS_GEMM_CASE(1, 1, 2)
     SGS_GEMM_CASE(1, 2, 1) SGS_GEMM_CASE(1, 2, 2) SGS_GEMM_CASE(1, 3, 1) SGS_GEMM_CASE(1, 3, 2)
+    SGS_GEMM_CASE(1, 4, 1) SGS_GEMM_CASE(1, 4, 2)
     SGS_GEMM_CASE(2, 0, 1) SGS_GEMM_CASE(2, 0, 2) SGS_GEMM_CASE(2, 1, 1) SGS_GEMM_CASE(2, 1, 2)
     SGS_GEMM_CASE(2, 2, 1) SGS_GEMM_CASE(2, 2, 2) SGS_GEMM_CASE(2, 3, 1) SGS_GEMM_CASE(2, 3, 2)
+    SGS_GEMM_CASE(2, 4, 1) SGS_GEMM_CASE(2, 4, 2)
 #undef SGS_GEMM_CASE
     default:
       return cudaErrorInvalidValue;

@@ -10,8 +10,23 @@ namespace sgs {
 // ---- GEMM (gemm.cu): C[t, n] (+)= X[t, :] . W[n, :]; mode 0 store, 1 atomic add, 2 add
 // mode 3: fused SwiGLU epilogue for gate/up weights in the interleaved
 // layout; C is then bf16 [T, ldc] with ldc = N/2 (requires splits == 1).
+// mode 4: greedy sampling fused into the epilogue (LM head): every CTA folds
+// its tile's (max logit, lowest vocab index) per token into keys[t] (packed
+// 64-bit atomicMax); the last CTA to finish writes the argmax of row t to
+// last_tok[slot[t]] and hist[slot[t] * max_gen + tok_idx[t]] (slot < 0: padding
+// row) and re-zeroes keys and the arrival counter.  C (may be NULL) also gets
+// the fp32 logits as in mode 0.
+struct ArgmaxArgs {
+  unsigned long long* keys;  // [>= T], zero between launches
+  unsigned int* done;        // arrival counter, zero between launches
+  const int32_t* slot;
+  const int32_t* tok_idx;
+  int32_t* last_tok;
+  int32_t* hist;
+  int max_gen;
+};
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
-                      cudaStream_t stream);
+                      cudaStream_t stream, const ArgmaxArgs* am = nullptr);
 int gemm_auto_splits(int N, int K, int T);
 
 // ---- decode attention (attention.cu)

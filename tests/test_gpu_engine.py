@@ -417,13 +417,26 @@ def test_c2_scale_pipelined_engine(sgs):
     srt = np.sort(ref, 1)
     clear = (srt[:, -1] - srt[:, -2]) > 2 * TOL_7B_28L
     assert np.array_equal(ref.argmax(1)[clear], gen[clear])
-    # pipelined (bench) run vs logits run: identical tokens except where split-K's
-    # summation order flips a near-tie; the first differing position must be one
-    same = [i for i in toks_a if np.array_equal(toks_a[i], toks_b[i])]
-    assert len(same) >= 0.9 * len(toks_a), (len(same), len(toks_a))
+    # pipelined (bench) run vs logits run: split-K's fp32 summation order (R21)
+    # perturbs the 28-layer logits by up to the R17 floor, so with random
+    # weights' near-uniform logits many samples take another token somewhere;
+    # wherever they first differ the logits run's top-2 gap must lie within
+    # 2x the tolerance (a genuine divergence would show at clear positions)
     for i in toks_a:
-        if i in same:
-            continue
-        j = int(np.flatnonzero(toks_a[i] != toks_b[i])[0])
-        assert gaps[(i, j)] < 0.05, (i, j, gaps[(i, j)])
+        d = np.flatnonzero(toks_a[i] != toks_b[i])
+        if len(d):
+            assert gaps[(i, int(d[0]))] < 2 * TOL_7B_28L, (i, int(d[0]), gaps[(i, int(d[0]))])
     inst.close()
+    del inst
+    # with SGS_F_DETERMINISTIC (no split-K) the pipelined run and the logits run
+    # of the same 256-row production configuration must agree bit for bit
+    runs = []
+    for flags in (sgs.sgs.F_DETERMINISTIC, sgs.sgs.F_DETERMINISTIC | sgs.sgs.F_KEEP_LOGITS):
+        inst = sgs.Instance(shape, 256, 512 + 64, device=0, n_pages=pool, weight_seed=seed, flags=flags)
+        inst.submit_trace(full)
+        c = inst.run()
+        assert np.array_equal(inst.trace(0), o["iter_blob"])
+        runs.append({x["id"]: tuple(x["tokens"]) for x in c})
+        inst.close()
+        del inst
+    assert runs[0] == runs[1]

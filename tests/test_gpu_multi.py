@@ -139,3 +139,50 @@ def test_weight_sync_broadcast_bit_identical():
         assert r["version"] == 1
         for tid, v in r["sums"].items():
             assert v == oracle.tensor_checksum(4242, tid, sizes[tid], tid in norm), (r["rank"], tid)
+
+
+def _src_worker(rank, world, port, q):
+    # the trainer path of sgs_update_weights (P:595-596 update(weights)): the root
+    # passes the new weights (host tensors, canonical order) and every rank ends
+    # with them bit for bit; non-root ranks pass no source
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2504_15930_b200 as sgs
+        shape = workload.MODELS["tiny"]
+        inst = sgs.Instance(shape, 8, 128, device=rank, n_pages=64, n_instances=world, instance_rank=rank,
+                            weight_seed=3000 + rank)
+        uid = [sgs.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        inst.comm_init(uid[0], rank, world)
+        w = None
+        if rank == 0:
+            w = []
+            for tid, rows, cols in sgs.weight_tensors(shape):
+                norm = tid == 2 or (tid >= 16 and (tid - 16) % 16 >= 10)
+                w.append(torch.from_numpy(oracle.gen_tensor(555, tid, rows * cols, norm)).to(torch.bfloat16))
+        inst.update_weights(0, weights=w)
+        sums = {tid: inst.checksum(tid) for tid in (0, 1, 2, 16, 23, 24, 27, 32 + 9)}
+        out = [None] * world
+        dist.all_gather_object(out, dict(rank=rank, sums=sums, version=inst.weight_version()))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_weight_sync_from_trainer_source():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run with gpurun --gpus 2)")
+    res = _spawn(_src_worker, 2)
+    shape = workload.MODELS["tiny"]
+    sizes = {0: shape.vocab * shape.d_model, 1: shape.vocab * shape.d_model, 2: shape.d_model,
+             16: shape.n_q_heads * shape.head_dim * shape.d_model, 23: shape.d_ffn * shape.d_model,
+             24: shape.d_ffn * shape.d_model, 27: shape.d_model, 41: shape.d_model * shape.d_ffn}
+    for r in res:
+        assert r["version"] == 1
+        for tid, v in r["sums"].items():
+            assert v == oracle.tensor_checksum(555, tid, sizes[tid], tid in {2, 27}), (r["rank"], tid)
