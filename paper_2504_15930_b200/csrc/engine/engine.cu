@@ -93,6 +93,7 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->off_attn = take(L->attn_bytes);
   L->off_cksum = take(64);
   L->off_amax = take(((B + 15) / 16 * 16) * 8 + 64);
+  L->off_nbar = take((2 * m.n_layers + 1) * 2 * 4 + 64);
   L->scratch_bytes = o - s0;
   L->off_shadow = (e.flags & SGS_F_SHADOW_WEIGHTS) ? take(L->weights_bytes) : -1;
   L->total = o;
@@ -267,6 +268,8 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   attn_ws_ = arena_ + L_.off_attn;
   cksum_dev_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_cksum);
   amax_keys_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_amax);
+  norm_bar_ = reinterpret_cast<unsigned int*>(arena_ + L_.off_nbar);
+  if (const char* nf = std::getenv("SGS_NO_FUSED_NORM")) fused_norm_ = std::atoi(nf) == 0;
   tok_host_cap_ = (int64_t)e.max_batch * max_gen_;
   for (int k = 0; k < 2; ++k) {
     CK(cudaMallocHost(&meta_bufs_[k], L_.meta_bytes), "cudaMallocHost(meta)");
@@ -293,6 +296,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   CK(cudaEventCreateWithFlags(&ev_pf_, cudaEventDisableTiming), "event");
   CK(cudaMemsetAsync(attn_ws_, 0, L_.attn_bytes, st_), "memset attention workspace");
   CK(cudaMemsetAsync(amax_keys_, 0, ((e.max_batch + 15) / 16 * 16) * 8 + 64, st_), "memset argmax keys");
+  CK(cudaMemsetAsync(norm_bar_, 0, (2 * m.n_layers + 1) * 2 * 4 + 64, st_), "memset norm barriers");
   // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
   {
     const int half = m.head_dim / 2;
@@ -549,7 +553,8 @@ cudaError_t Engine::kflush(const std::vector<KRec>& recs, int rows) {
   return cudaSuccess;
 }
 
-cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate) {
+cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate,
+                         const PreNorm* pn) {
   // SGS_F_DETERMINISTIC: no split-K (the fp32 red.add order is the only run-to-run variation, R21)
   const int splits = (e_.flags & SGS_F_DETERMINISTIC) ? 1 : gemm_auto_splits(N, K, T);
   cudaError_t e;
@@ -561,9 +566,9 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
       e = cudaMemsetAsync(C, 0, (size_t)T * N * 4, st_);
       if (e != cudaSuccess) return e;
     }
-    e = gemm_bf16(W, X, C, N, K, T, N, 1, splits, st_);
+    e = gemm_bf16(W, X, C, N, K, T, N, 1, splits, st_, nullptr, pn);
   } else {
-    e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_);
+    e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_, nullptr, pn);
   }
   // algorithmic bytes: weights + per row activations in + fp32 out (read-modify-write when accumulating)
   ktoc(&kr, 2.0 * N * K, 2.0 * K + (accumulate ? 8.0 : 4.0) * N, 2.0 * N * K, T);
@@ -585,17 +590,17 @@ cudaError_t Engine::sample(const float* logits, int rows, const uint32_t* sid, c
 // m = bf16(SiLU(x Wg^T) * (x Wu^T)): one GEMM with the SwiGLU epilogue when
 // the gate/up GEMM needs no split-K (always at the model shapes: 2 f / 128 >=
 // 148 tiles), else the fp32 GEMM + the silu_mul kernel.
-cudaError_t Engine::gate_up(const void* W, int T) {
+cudaError_t Engine::gate_up(const void* W, int T, const PreNorm* pn) {
   const int d = m_.d_model, f = m_.d_ffn;
   if (!(e_.flags & SGS_F_DETERMINISTIC) && gemm_auto_splits(2 * f, d, T) > 1) {
-    cudaError_t e = gemm(W, x_, gu_, 2 * f, d, T, false);
+    cudaError_t e = gemm(W, x_, gu_, 2 * f, d, T, false, pn);
     if (e != cudaSuccess) return e;
     ++launches;
     return silu_mul(gu_, mm_, T, f, st_);
   }
   KRec kr;
   ktic(&kr, gemm_cls_);
-  cudaError_t e = gemm_bf16(W, x_, reinterpret_cast<float*>(mm_), 2 * f, d, T, f, 3, 1, st_);
+  cudaError_t e = gemm_bf16(W, x_, reinterpret_cast<float*>(mm_), 2 * f, d, T, f, 3, 1, st_, nullptr, pn);
   ktoc(&kr, 2.0 * 2 * f * d, 2.0 * d + 2.0 * f, 2.0 * 2 * f * d, T);
   ++launches;
   return e;
@@ -722,7 +727,8 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     poisoned = true;
     return SGS_E_NOMEM;
   }
-  D[0] = (int32_t)ap.items.size(), D[1] = (int32_t)ap.combs.size(), D[2] = n_run, D[3] = 0;
+  D[0] = (int32_t)ap.items.size(), D[1] = (int32_t)ap.combs.size(), D[2] = n_run;
+  D[3] = n_run > 0 ? (int32_t)(dec_launch_++ & 1) : 0;  // PreNorm barrier parity of this decode launch
   AttnComb* hcombs = reinterpret_cast<AttnComb*>(D + 4 + 6 * Bpad);
   AttnItem* hitems = reinterpret_cast<AttnItem*>(hcombs + L_.max_items);
   std::memcpy(hcombs, ap.combs.data(), ap.combs.size() * sizeof(AttnComb));
@@ -943,11 +949,17 @@ sgs_status Engine::decode_body(int Bk) {
   ktic(&ko, 5);
   if (on(9)) CK(other(embed(embed_, nullptr, d_slot, last_tok_, h_, Bk, d, st_), &ko, 6.0 * d), "embed");
   ++launches;
+  // RMSNorm fused into the QKV / gate-up / LM-head GEMMs (PreNorm: rows
+  // normalised by the GEMM's own CTAs before a grid barrier); the barrier
+  // parity is this decode launch's, read from the metadata (D[3])
+  const bool fuse = fused_norm_ && on(0);
+  auto pnorm = [&](const void* w, int site) { return PreNorm{h_, w, nullptr, m_.rms_eps, norm_bar_, site, counts + 3}; };
   for (int l = 0; l < m_.n_layers; ++l) {
     const Layer& Ly = layers_[l];
-    ktic(&ko, 5);
-    if (on(0)) CK(other(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm1");
-    if (on(1)) CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false), "gemm qkv");
+    const PreNorm pn1 = pnorm(Ly.n1, 2 * l), pn2 = pnorm(Ly.n2, 2 * l + 1);
+    if (!fuse) ktic(&ko, 5);
+    if (on(0) && !fuse) CK(other(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm1");
+    if (on(1)) CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false, fuse ? &pn1 : nullptr), "gemm qkv");
     ktic(&ko, 5);
     if (on(2))
       CK(other(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, nullptr, nullptr, Bk,
@@ -962,14 +974,15 @@ sgs_status Engine::decode_body(int Bk) {
          "attn_decode");
     ktoc(&kr, -1.0, 0.0, 0.0, 0);
     if (on(4)) CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
-    ktic(&ko, 5);
-    if (on(0)) CK(other(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm2");
-    if (on(5)) CK(gate_up(Ly.wgu, Bk), "gemm gate_up + SwiGLU");
+    if (!fuse) ktic(&ko, 5);
+    if (on(0) && !fuse) CK(other(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm2");
+    if (on(5)) CK(gate_up(Ly.wgu, Bk, fuse ? &pn2 : nullptr), "gemm gate_up + SwiGLU");
     if (on(6)) CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
-    launches += 4;  // rmsnorm x2, RoPE, attention; the GEMMs count themselves
+    launches += fuse ? 2 : 4;  // (rmsnorm x2,) RoPE, attention; the GEMMs count themselves
   }
-  ktic(&ko, 5);
-  if (on(0)) CK(other(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm f");
+  const PreNorm pnf = pnorm(nf_, 2 * m_.n_layers);
+  if (!fuse) ktic(&ko, 5);
+  if (on(0) && !fuse) CK(other(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm f");
   if (e_.sampling == SGS_SAMPLE_GREEDY) {
     // LM head with greedy sampling fused into its epilogue (GEMM mode 4): no
     // fp32 logits round trip and no sampler launch; the logits are still
@@ -981,11 +994,13 @@ sgs_status Engine::decode_body(int Bk) {
                   max_gen_};
     KRec kr;
     ktic(&kr, gemm_cls_);
-    if (on(7)) CK(gemm_bf16(lm_head_, x_, keep ? logits_ : nullptr, V, d, Bk, V, 4, 1, st_, &am), "gemm lm_head");
+    if (on(7))
+      CK(gemm_bf16(lm_head_, x_, keep ? logits_ : nullptr, V, d, Bk, V, 4, 1, st_, &am, fuse ? &pnf : nullptr),
+         "gemm lm_head");
     ktoc(&kr, 2.0 * V * d, 2.0 * d + (keep ? 4.0 * V : 0.0), 2.0 * V * d, Bk);
     launches += 1;
   } else {
-    if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false), "gemm lm_head");
+    if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false, fuse ? &pnf : nullptr), "gemm lm_head");
     ktic(&ko, 5);
     if (on(8)) CK(other(sample(logits_, Bk, d_sid, d_slot, d_tok), &ko, 4.0 * V), "sampler");
   }

@@ -30,7 +30,7 @@ struct ArenaLayout {
   // offsets (bytes from arena start)
   int64_t off_kv = 0, off_h = 0, off_x = 0, off_qkv = 0, off_q = 0, off_kc = 0, off_vc = 0, off_ao = 0,
           off_gu = 0, off_mm = 0, off_logits = 0, off_rope = 0, off_bt = 0, off_last = 0, off_hist = 0,
-          off_meta = 0, off_attn = 0, off_cksum = 0, off_shadow = -1, off_amax = 0;
+          off_meta = 0, off_attn = 0, off_cksum = 0, off_shadow = -1, off_amax = 0, off_nbar = 0;
   // decode scratch (Bpad rows), separate from the prefill scratch so the two run concurrently
   int64_t off_dh = 0, off_dx = 0, off_dqkv = 0, off_dq = 0, off_dao = 0, off_dgu = 0, off_dmm = 0;
   int64_t meta_bytes = 0, attn_bytes = 0, meta_dec_bytes = 0;
@@ -102,8 +102,9 @@ class Engine {
                            const int32_t* d_qblocks, int n_qblocks, const int32_t* d_last_rows,
                            const int32_t* d_pf_slot, const int32_t* d_pf_tok, int T, float* dump = nullptr,
                            int only_layer = -1, const float* h_in = nullptr);
-  cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate);
-  cudaError_t gate_up(const void* W, int T);
+  cudaError_t gemm(const void* W, const void* X, float* C, int N, int K, int T, bool accumulate,
+                   const PreNorm* pn = nullptr);
+  cudaError_t gate_up(const void* W, int T, const PreNorm* pn = nullptr);
   cudaError_t sample(const float* logits, int rows, const uint32_t* sid, const int32_t* slot, const int32_t* tok_idx);
   void build_tensor_table();
   // kernel-class timing record: bytes = bfix + brow * rows (bfix < 0: the
@@ -181,6 +182,9 @@ class Engine {
   uint8_t* attn_ws_ = nullptr;
   unsigned long long* cksum_dev_ = nullptr;
   unsigned long long* amax_keys_ = nullptr;  // fused greedy sampling (GEMM mode 4): [Bpad] keys + counter
+  unsigned int* norm_bar_ = nullptr;          // PreNorm grid barriers: 2 per site (2 per layer + final)
+  bool fused_norm_ = true;                    // RMSNorm fused into the decode GEMMs (SGS_NO_FUSED_NORM=1: off)
+  int64_t dec_launch_ = 0;                    // decode-program launches (PreNorm barrier parity)
   int32_t* tok_host_ = nullptr;  // pinned, completed tokens (the current one of tok_bufs_)
   int64_t tok_host_cap_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

@@ -19,6 +19,7 @@
 //   o = sum_j 2^(m_j - M) O_j / sum_j 2^(m_j - M) l_j.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -335,11 +336,13 @@ void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page
   // gets floor(296 np / total) parts, so the items never spill into a second,
   // nearly empty wave; parts keep >= 2 pages per warp and there are at most
   // ATTN_SPLIT_CAP of them (the last-arriving CTA merges them serially).
-  constexpr int64_t kSlots = 2 * 148;
+  // SGS_ATTN_SLOTS / SGS_ATTN_MINPG: planner experiments (tools/attn_sweep.py)
+  static const int64_t kSlots = std::getenv("SGS_ATTN_SLOTS") ? std::atoll(std::getenv("SGS_ATTN_SLOTS")) : 2 * 148;
+  static const int kMinPg = std::getenv("SGS_ATTN_MINPG") ? std::atoi(std::getenv("SGS_ATTN_MINPG")) : 2 * ATTN_WARPS;
   constexpr int ATTN_SPLIT_CAP = 32;
   auto parts = [&](int np) {
     int nch = (int)(kSlots * np / total);
-    const int by_pages = np / (2 * ATTN_WARPS);
+    const int by_pages = np / kMinPg;
     if (nch > by_pages) nch = by_pages;
     if (nch > ATTN_SPLIT_CAP) nch = ATTN_SPLIT_CAP;
     return nch < 1 ? 1 : nch;

@@ -44,12 +44,67 @@ constexpr int GEMM_GROUP = 16;  // weight tiles (pairs) per rasterisation group
 // kernel carries only its own producer and epilogue code, which keeps it
 // under the ~40 KB instruction-cache knee (a 46 KB all-modes kernel measured
 // 14% slower on decode-sized GEMMs).
+// ---- fused RMSNorm pre-phase (PreNorm) helpers
+__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// epilogue warps (128 threads, e = warp - 4): X rows of this CTA, then one arrival
+__device__ __forceinline__ void prenorm_rows(const PreNorm& pn, __nv_bfloat16* __restrict__ X, int T, int d, int e,
+                                             int lane, double* red) {
+  const int tid = e * 32 + lane;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    const float* hr = pn.h + (size_t)t * d;
+    double ss = 0.0;
+    for (int i = 4 * tid; i < d; i += 512) {
+      const float4 v = *reinterpret_cast<const float4*>(hr + i);
+      ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[e] = ss;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const double r = 1.0 / sqrt((red[0] + red[1] + red[2] + red[3]) / (double)d + (double)pn.eps);
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // red[] is reused by the next row
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(pn.w);
+    for (int i = 4 * tid; i < d; i += 512) {
+      const float4 v = *reinterpret_cast<const float4*>(hr + i);
+      const uint32_t w0 = w[i >> 1], w1 = w[(i >> 1) + 1];
+      auto f = [&](float x, uint32_t wbits) { return (float)((double)x * r * (double)__uint_as_float(wbits)); };
+      uint2 o;
+      o.x = pack_bf16x2(f(v.x, w0 << 16), f(v.y, w0 & 0xffff0000u));
+      o.y = pack_bf16x2(f(v.z, w1 << 16), f(v.w, w1 & 0xffff0000u));
+      *reinterpret_cast<uint2*>(X + (size_t)t * d + i) = o;
+    }
+  }
+  fence_proxy_async_global();  // X is read by other CTAs' TMA (async proxy)
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (tid == 0) {
+    const int p = *pn.parity & 1;
+    unsigned int* cnt = pn.bar + 2 * pn.site + p;
+    if (atomicAdd(cnt, 1u) == gridDim.x - 1) pn.bar[2 * pn.site + (p ^ 1)] = 0u;  // re-arm the other parity
+  }
+}
+// the activation producer: wait until every CTA wrote its X rows
+__device__ __forceinline__ void prenorm_wait(const PreNorm& pn) {
+  const unsigned int* cnt = pn.bar + 2 * pn.site + (*pn.parity & 1);
+  while (ld_acquire_u32(cnt) < gridDim.x) __nanosleep(32);
+  fence_proxy_async_global();
+}
+
+// <= 128 registers per thread: two decode-tile CTAs (and their PreNorm grid
+// barrier) must be co-resident on an SM
 template <int CG, int MODE, int KCS>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
                         int chunks_per_split, int tmem_cols, int n_acc, int acc_stride, int num_mp, int num_n,
-                        int units, int nbuf, int xbufs, const ArgmaxArgs am) {
+                        int units, int nbuf, int xbufs, const ArgmaxArgs am, const PreNorm pn, int K) {
   constexpr int mode = MODE, kcs = KCS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -153,6 +208,7 @@ __global__ void __launch_bounds__(256, 1)
           load_a(i, i);
         }
         pdl_wait();
+        if (pn.h) prenorm_wait(pn);
         for (int i = 0; i < pre; ++i) load_b(i, i);
         i0 = pre;
         it = pre;
@@ -174,7 +230,10 @@ __global__ void __launch_bounds__(256, 1)
     const bool is_w = warp == 0;
     const CUtensorMap* tm = is_w ? &tmW : &tmX;
     prefetch_tmap(tm);
-    if (!is_w) pdl_wait();
+    if (!is_w) {
+      pdl_wait();
+      if (pn.h) prenorm_wait(pn);
+    }
     const uint32_t tx = (uint32_t)CG * (is_w ? a_stage : b_stage);
     uint8_t* base = is_w ? sA : sB;
     const int sbytes = is_w ? a_stage : b_stage;
@@ -241,6 +300,10 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- epilogue: TMEM -> registers -> global (lane = output feature)
     const int e = warp - 4;
     pdl_wait();  // C may still be read by the predecessor (write-after-read)
+    if (pn.h) {
+      double* red = reinterpret_cast<double*>(xch + (size_t)xbufs * 4 * 32 * 17 + 128);  // past the mode-4 keys
+      prenorm_rows(pn, reinterpret_cast<__nv_bfloat16*>(pn.x), T, K, e, lane, red);
+    }
     int tc = 0;
     for (int u = pair; u < units; u += npairs, ++tc) {
       int m0, n0, kc0, nk;
@@ -373,13 +436,15 @@ __global__ void __launch_bounds__(256, 1)
   if (mode == 4) {
     // the last CTA to arrive turns the packed keys into tokens (all atomics of
     // every CTA precede its fenced arrival)
-    __shared__ int s_last;
+    // (no static shared memory in this kernel: the dynamic allocation takes the
+    // full 227 KB; tmem_slot[2] is a free word of the dynamic area)
+    volatile uint32_t* s_last = tmem_slot + 2;
     if (threadIdx.x == 0) {
       __threadfence();
-      s_last = atomicAdd(am.done, 1u) == gridDim.x - 1;
+      *s_last = atomicAdd(am.done, 1u) == gridDim.x - 1 ? 1u : 0u;
     }
     __syncthreads();
-    if (s_last) {
+    if (*s_last) {
       __threadfence();
       for (int t = threadIdx.x; t < T; t += blockDim.x) {
         const unsigned long long k = atomicExch(am.keys + t, 0ull);
@@ -499,13 +564,45 @@ int gemm_auto_splits(int N, int K, int T) {
   return s < 1 ? 1 : s;
 }
 
+template <int CG, int MODE, int KCS>
+static int occupancy_of(size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<size_t, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(smem);
+  if (it != cache.end()) return it->second;
+  auto kern = gemm_bf16_tc_kernel<CG, MODE, KCS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, smem) != cudaSuccess) n = 0;
+  cache.emplace(smem, n);
+  return n;
+}
+
+static int gemm_occupancy(int cg, int mode, int kcs, size_t smem) {
+  switch ((cg - 1) * 10 + mode * 2 + (kcs - 1)) {
+#define SGS_OCC_CASE(c, md, kk) \
+  case (c - 1) * 10 + md * 2 + (kk - 1): return occupancy_of<c, md, kk>(smem);
+    SGS_OCC_CASE(1, 0, 1) SGS_OCC_CASE(1, 0, 2) SGS_OCC_CASE(1, 1, 1) SGS_OCC_CASE(1, 1, 2)
+    SGS_OCC_CASE(1, 2, 1) SGS_OCC_CASE(1, 2, 2) SGS_OCC_CASE(1, 3, 1) SGS_OCC_CASE(1, 3, 2)
+    SGS_OCC_CASE(1, 4, 1) SGS_OCC_CASE(1, 4, 2)
+    SGS_OCC_CASE(2, 0, 1) SGS_OCC_CASE(2, 0, 2) SGS_OCC_CASE(2, 1, 1) SGS_OCC_CASE(2, 1, 2)
+    SGS_OCC_CASE(2, 2, 1) SGS_OCC_CASE(2, 2, 2) SGS_OCC_CASE(2, 3, 1) SGS_OCC_CASE(2, 3, 2)
+    SGS_OCC_CASE(2, 4, 1) SGS_OCC_CASE(2, 4, 2)
+#undef SGS_OCC_CASE
+    default:
+      return 0;
+  }
+}
+
 // Launch one instantiation: PDL always, plus a 2-CTA cluster for CG == 2.
 template <typename Kern, typename... Args>
 static cudaError_t launch_gemm(Kern kern, int cg, dim3 grid, size_t smem, cudaStream_t stream, Args... args) {
   static thread_local std::unordered_map<const void*, bool> attr;  // per instantiation
   bool& done = attr[reinterpret_cast<const void*>(kern)];
   if (!done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
     done = true;
   }
   if (cg == 1) return launch_pdl(kern, grid, dim3(256), smem, stream, args...);
@@ -525,12 +622,16 @@ static cudaError_t launch_gemm(Kern kern, int cg, dim3 grid, size_t smem, cudaSt
 }
 
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
-                      cudaStream_t stream, const ArgmaxArgs* am) {
+                      cudaStream_t stream, const ArgmaxArgs* am, const PreNorm* pn) {
   if (T <= 0) return cudaSuccess;
   if (N % GEMM_BM != 0 || K % GEMM_BK != 0) return cudaErrorInvalidValue;
   // SGS_GEMM_BN_CAP (experiments, tools/gemm_explore.py): largest token tile
   static const int bn_cap = std::getenv("SGS_GEMM_BN_CAP") ? std::atoi(std::getenv("SGS_GEMM_BN_CAP")) : 256;
-  const int BN = std::min(bn_cap, T >= 256 ? 256 : ((T + 15) / 16) * 16);
+  int BN = std::min(bn_cap, T >= 256 ? 256 : ((T + 15) / 16) * 16);
+  // small split-K projections (QKV, O: N*K <= 16.5M) at T >= 256: 128-token
+  // tiles (twice the units per split) measured 7-8% faster than 256-token ones
+  // (profiles/r02/gemm_explore_*.log: QKV 13.7 vs 14.6 us, O 12.6 vs 13.6 us)
+  if (mode == 1 && T >= 256 && (int64_t)N * K <= 4608LL * 3584 && bn_cap >= 256) BN = 128;
   // CTA pairs for compute-bound token tiles (BN >= 128) when the 256-row pair tiles N
   const int CG = (BN >= 128 && N % (2 * GEMM_BM) == 0) ? 2 : 1;
   const int kc = K / GEMM_BK;
@@ -538,6 +639,11 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (splits > 1 && mode != 1) return cudaErrorInvalidValue;
   if (mode == 4 && !am) return cudaErrorInvalidValue;
   const ArgmaxArgs amv = am ? *am : ArgmaxArgs{};
+  PreNorm pnv = pn ? *pn : PreNorm{};
+  if (pn) {
+    if (K % 4 != 0) return cudaErrorInvalidValue;
+    pnv.x = const_cast<void*>(X);
+  }
   // decode-sized tiles (BN <= 128) use half the shared memory and TMEM so two
   // CTAs fit on an SM: the next tile (or the next GEMM, via PDL) streams its
   // weights while the current one drains
@@ -562,11 +668,17 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   // needs one barrier per 16-token chunk); decode tiles keep the smem for stages
   const int xbufs = small ? 1 : 2;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + (size_t)xbufs * 4 * 32 * 17 * 4 +
-                      (mode == 4 ? 4 * 16 * 8 : 0);
+                      4 * 16 * 8 + 64;  // + mode-4 keys [4][16] + PreNorm reduction [4] (fp64)
   // persistent grid: one CTA (pair) per resident slot, at most one per unit
   const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
   const int units = num_mp * num_n * splits;
-  const int slots = sm_count() * (small ? 2 : 1) / CG;
+  int slots = sm_count() * (small ? 2 : 1) / CG;
+  {
+    // never more CTAs than are co-resident (a PreNorm grid barrier needs all of them)
+    const int occ = gemm_occupancy(CG, mode, kcs, smem);
+    if (occ > 0 && sm_count() * occ / CG < slots) slots = sm_count() * occ / CG;
+    if (occ <= 0) return cudaErrorInvalidConfiguration;
+  }
   const int pairs = units < slots ? units : slots;
   // double-buffer TMEM when a CTA runs several compute-bound units; decode-
   // sized units (BN <= 64) keep all accumulators for precision (their
@@ -588,7 +700,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
 #define SGS_GEMM_CASE(cg, md, kk)                                                                                     \
   case (cg - 1) * 10 + md * 2 + (kk - 1):                                                                           \
     return launch_gemm(gemm_bf16_tc_kernel<cg, md, kk>, cg, grid, smem, stream, tw, tx, C, T, ldc, BN, stages, kc, \
-                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs, amv);
+                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs, amv, pnv, K);
     SGS_GEMM_CASE(1, 0, 1) SGS_GEMM_CASE(1, 0, 2) SGS_GEMM_CASE(1, 1, 1) SGS_GEMM_CASE(1, 1, 2)
     SGS_GEMM_CASE(1, 2, 1) SGS_GEMM_CASE(1, 2, 2) SGS_GEMM_CASE(1, 3, 1) SGS_GEMM_CASE(1, 3, 2)
     SGS_GEMM_CASE(1, 4, 1) SGS_GEMM_CASE(1, 4, 2)

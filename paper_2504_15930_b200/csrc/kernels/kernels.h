@@ -25,8 +25,25 @@ struct ArgmaxArgs {
   int32_t* hist;
   int max_gen;
 };
+// RMSNorm fused in front of a GEMM (decode program): before the GEMM reads its
+// activation operand X, the CTAs of the (persistent, co-resident) grid compute
+// X = bf16(h / sqrt(mean(h^2) + eps) * w) row by row (rows blockIdx.x, +grid;
+// the arithmetic of the standalone rmsnorm kernel) and meet at a grid barrier;
+// the activation TMA loads start after it, the weight loads before it.  The
+// barrier counter bar[2 * site + parity] (zero-initialised) is armed by the
+// last arrival resetting the other parity's counter; `parity` must alternate
+// between consecutive launches of the same site.
+struct PreNorm {
+  const float* h;            // fp32 residual stream [T, K]
+  const void* w;             // bf16 norm weight [K]
+  void* x;                   // bf16 [T, K]: written here, the GEMM's X (set by gemm_bf16)
+  float eps;
+  unsigned int* bar;         // barrier counters
+  int site;
+  const int32_t* parity;     // device int: launch parity of this site (read after griddepcontrol.wait)
+};
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
-                      cudaStream_t stream, const ArgmaxArgs* am = nullptr);
+                      cudaStream_t stream, const ArgmaxArgs* am = nullptr, const PreNorm* pn = nullptr);
 int gemm_auto_splits(int N, int K, int T);
 
 // ---- decode attention (attention.cu)

@@ -264,6 +264,7 @@ class Instance:
         if getattr(self, "h", None):
             lib().sgs_destroy(self.h)
             self.h = None
+        self.arena = None  # the device arena goes back to PyTorch's allocator
 
     def __del__(self):
         try:

@@ -73,9 +73,9 @@ def main():
         policy, score = (spec.split("_max")[0], 1) if spec.endswith("_max") else (spec, 0)
         key = (policy, score)
         # one engine per (policy, score): the dispatch policy is an engine setting
+        inst = None
         for k in list(insts):
-            if k != key:
-                insts.pop(k).close()
+            insts.pop(k).close()
         torch.cuda.empty_cache()
         inst = sgs.Instance(shape, cfg.max_batch, max_ctx, device=local, n_instances=N, instance_rank=me,
                             weight_seed=cfg.seed, dispatch=policy, score=score, profile=prof, sample_seed=seed,

@@ -69,7 +69,7 @@ def main():
         # iterations start at each embed kernel
         starts = [i for i, k in enumerate(ks) if k[0] == "embed"]
         iters = []
-        stats = collections.defaultdict(lambda: [0, 0.0, 0.0])
+        stats = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
         for j in range(len(starts) - 1):
             seg = ks[starts[j]:starts[j + 1]]
             span = seg[-1][2] - seg[0][1]
@@ -80,6 +80,8 @@ def main():
                 st[0] += 1
                 st[1] += s1 - s0
                 st[2] += (s0 - seg[i - 1][2]) if i else 0.0
+                # critical-path increment: how far this kernel's end moves past every earlier end
+                st[3] += max(0.0, s1 - last_end) if i else s1 - s0
                 busy += max(0.0, s1 - max(s0, last_end))
                 last_end = max(last_end, s1)
             iters.append({"span_us": span, "busy_us": busy, "kernels": len(seg)})
@@ -89,7 +91,9 @@ def main():
                "busy_us_mean": round(float(np.mean([x["busy_us"] for x in iters])), 1) if iters else None,
                "kinds": {k: {"per_iter": round(v[0] / n_it, 1), "dur_us_mean": round(v[1] / v[0], 2),
                              "gap_before_us_mean": round(v[2] / v[0], 2),
-                             "dur_us_per_iter": round(v[1] / n_it, 1)} for k, v in sorted(stats.items())}}
+                             "dur_us_per_iter": round(v[1] / n_it, 1),
+                             "crit_us_mean": round(v[3] / v[0], 2), "crit_us_per_iter": round(v[3] / n_it, 1)}
+                         for k, v in sorted(stats.items())}}
         out["per_b"][str(b)] = rec
         print(json.dumps({"b": b, **{k: rec[k] for k in ("iterations", "span_us_mean", "busy_us_mean")}}),
               flush=True)
