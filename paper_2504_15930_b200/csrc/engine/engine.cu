@@ -269,7 +269,10 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   cksum_dev_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_cksum);
   amax_keys_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_amax);
   norm_bar_ = reinterpret_cast<unsigned int*>(arena_ + L_.off_nbar);
-  if (const char* nf = std::getenv("SGS_NO_FUSED_NORM")) fused_norm_ = std::atoi(nf) == 0;
+  // PreNorm is off by default: measured slower than the rmsnorm kernel + PDL
+  // (profiles/README.md r02: the norm and the grid barrier stay on the
+  // critical path, only the launch is saved); SGS_FUSED_NORM=1 turns it on
+  if (const char* nf = std::getenv("SGS_FUSED_NORM")) fused_norm_ = std::atoi(nf) != 0;
   tok_host_cap_ = (int64_t)e.max_batch * max_gen_;
   for (int k = 0; k < 2; ++k) {
     CK(cudaMallocHost(&meta_bufs_[k], L_.meta_bytes), "cudaMallocHost(meta)");

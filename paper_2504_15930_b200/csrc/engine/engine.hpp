@@ -183,7 +183,7 @@ class Engine {
   unsigned long long* cksum_dev_ = nullptr;
   unsigned long long* amax_keys_ = nullptr;  // fused greedy sampling (GEMM mode 4): [Bpad] keys + counter
   unsigned int* norm_bar_ = nullptr;          // PreNorm grid barriers: 2 per site (2 per layer + final)
-  bool fused_norm_ = true;                    // RMSNorm fused into the decode GEMMs (SGS_NO_FUSED_NORM=1: off)
+  bool fused_norm_ = false;                   // RMSNorm fused into the decode GEMMs (SGS_FUSED_NORM=1)
   int64_t dec_launch_ = 0;                    // decode-program launches (PreNorm barrier parity)
   int32_t* tok_host_ = nullptr;  // pinned, completed tokens (the current one of tok_bufs_)
   int64_t tok_host_cap_ = 0;

@@ -75,8 +75,15 @@ __global__ void __launch_bounds__(128, 2)
 
   const int npages = it.p1 - it.p0;
   const int n_my = npages > warp ? (npages - warp + ATTN_WARPS - 1) / ATTN_WARPS : 0;
-  auto issue = [&](int i) {
-    const int page = btr[it.p0 + warp + ATTN_WARPS * i];
+  // the warp's block-table entries, 32 at a time in lane registers (lane k
+  // holds the page of the warp's (32 j + k)-th page): the ring refill then
+  // needs a shuffle, not a dependent global load, before each bulk copy
+  auto bt_batch = [&](int j) {
+    const int i = 32 * j + lane;
+    return i < n_my ? btr[it.p0 + warp + ATTN_WARPS * i] : 0;
+  };
+  int my_pages = bt_batch(0);
+  auto issue = [&](int i, int page) {
     const __nv_bfloat16* src = kv + ((size_t)page * nkv + it.kvh) * (size_t)(2 * PAGE_T * HD);
     uint64_t* b = &bars[warp][i % ATTN_STAGES];
     mbar_expect_tx(b, STAGE);
@@ -85,11 +92,15 @@ __global__ void __launch_bounds__(128, 2)
   const int first = n_my < ATTN_STAGES ? n_my : ATTN_STAGES;
   int pre = 0;  // ring slots whose page is complete (pages ascend with i)
   while (pre < first && it.p0 + warp + ATTN_WARPS * pre < last_page) ++pre;
-  if (lane == 0)
-    for (int i = 0; i < pre; ++i) issue(i);
+  for (int i = 0; i < pre; ++i) {
+    const int pg = __shfl_sync(0xffffffffu, my_pages, i);
+    if (lane == 0) issue(i, pg);
+  }
   pdl_wait();
-  if (lane == 0)
-    for (int i = pre; i < first; ++i) issue(i);
+  for (int i = pre; i < first; ++i) {
+    const int pg = __shfl_sync(0xffffffffu, my_pages, i);
+    if (lane == 0) issue(i, pg);
+  }
 
   // Transposed formulation (tokens are the MMA's M dimension, the g <= 8
   // query heads its N): S^T = K Q^T and O^T += V^T P^T, so a 16-token page
@@ -169,9 +180,14 @@ __global__ void __launch_bounds__(128, 2)
       mma_bf16_16816(o[mt], a, bl0, bl1);
     }
     __syncwarp();
-    if (lane == 0 && i + ATTN_STAGES < n_my) {
-      fence_proxy_async_smem();
-      issue(i + ATTN_STAGES);
+    const int nx = i + ATTN_STAGES;
+    if (nx < n_my) {  // warp-uniform
+      if ((nx & 31) == 0) my_pages = bt_batch(nx >> 5);
+      const int pg = __shfl_sync(0xffffffffu, my_pages, nx & 31);
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        issue(nx, pg);
+      }
     }
   }
   // the row sums: reduce over the lanes holding the other tokens of each head
@@ -340,13 +356,39 @@ void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page
   static const int64_t kSlots = std::getenv("SGS_ATTN_SLOTS") ? std::atoll(std::getenv("SGS_ATTN_SLOTS")) : 2 * 148;
   static const int kMinPg = std::getenv("SGS_ATTN_MINPG") ? std::atoi(std::getenv("SGS_ATTN_MINPG")) : 2 * ATTN_WARPS;
   constexpr int ATTN_SPLIT_CAP = 32;
-  auto parts = [&](int np) {
-    int nch = (int)(kSlots * np / total);
+  auto cap = [&](int np, int nch) {
     const int by_pages = np / kMinPg;
     if (nch > by_pages) nch = by_pages;
     if (nch > ATTN_SPLIT_CAP) nch = ATTN_SPLIT_CAP;
     return nch < 1 ? 1 : nch;
   };
+  // parts per row: floor(slots * np / total), then the slots the floors leave
+  // empty go to the rows with the largest remainders (one part each), so a
+  // one-wave plan uses the whole wave
+  std::vector<int> nparts(b, 0);
+  {
+    std::vector<std::pair<int64_t, int>> rem;
+    int64_t used = 0;
+    for (int i = 0; i < b; ++i) {
+      const int np = (ctx[i] + page - 1) / page;
+      if (np == 0) continue;
+      const int64_t q = kSlots * np * nkv;  // this row's share of the slots, times total
+      nparts[i] = cap(np, (int)(q / total / nkv));
+      used += (int64_t)nparts[i] * nkv;
+      rem.push_back({(q / nkv) % total, i});
+    }
+    if (used < kSlots && split_pages <= 0) {
+      std::stable_sort(rem.begin(), rem.end(), [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& c) {
+        return a.first > c.first;
+      });
+      for (const auto& r : rem) {
+        const int i = r.second, np = (ctx[i] + page - 1) / page;
+        if (used + nkv > kSlots) break;
+        const int n2 = cap(np, nparts[i] + 1);
+        if (n2 > nparts[i]) used += (int64_t)(n2 - nparts[i]) * nkv, nparts[i] = n2;
+      }
+    }
+  }
   for (int i = 0; i < b; ++i) {
     const int np = (ctx[i] + page - 1) / page;
     if (np == 0) continue;
@@ -355,7 +397,7 @@ void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page
       nch = (np + split_pages - 1) / split_pages;
       if (nch > ATTN_MAX_PARTS) nch = ATTN_MAX_PARTS;
     } else {
-      nch = parts(np);
+      nch = nparts[i];
     }
     for (int h = 0; h < nkv; ++h) {
       if (nch == 1) {

@@ -673,11 +673,11 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
   const int units = num_mp * num_n * splits;
   int slots = sm_count() * (small ? 2 : 1) / CG;
-  {
-    // never more CTAs than are co-resident (a PreNorm grid barrier needs all of them)
+  if (pn) {
+    // a PreNorm grid barrier needs every CTA co-resident: never more CTAs than fit
     const int occ = gemm_occupancy(CG, mode, kcs, smem);
-    if (occ > 0 && sm_count() * occ / CG < slots) slots = sm_count() * occ / CG;
     if (occ <= 0) return cudaErrorInvalidConfiguration;
+    if (sm_count() * occ / CG < slots) slots = sm_count() * occ / CG;
   }
   const int pairs = units < slots ? units : slots;
   // double-buffer TMEM when a CTA runs several compute-bound units; decode-
