@@ -290,6 +290,22 @@ sgs_status sgs_io_bytes(const sgs_handle* h, int64_t* h2d, int64_t* d2h);
 /* Count of kernel launches (or graph launches' kernels) issued so far. */
 sgs_status sgs_kernel_launches(const sgs_handle* h, int64_t* n);
 
+/* NEXT-4, elastic DP scale-out (§4.2 "Dynamic adjustment"): the
+ * predicted generation time of this batch (n prompts, ranker hints as output
+ * lengths) on e->n_instances = N instances and on N + 1 -- Alg. 2 dispatch,
+ * then each instance's longest-first schedule timed with e->profile, makespan
+ * over instances (R25) -- in t_gen_ps[2]; delta' = t_gen_ps[0] -
+ * t_gen_ps[1]; *scale_out = delta' > 0 && delta_ps >= delta', delta_ps being
+ * the measured generation time minus the measured training time.  pool_pages
+ * is one instance's KV pool.  Pure host function. */
+sgs_status sgs_elastic_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* ids, const int32_t* prompt_len,
+                            const int32_t* hint, int64_t pool_pages, int64_t delta_ps, int64_t t_gen_ps[2],
+                            int64_t* delta_prime_ps, int32_t* scale_out);
+/* Change this handle's data-parallel layout (N instances, its rank) between
+ * RL batches -- the elastic scale-out of NEXT-4; SGS_E_STATE while samples
+ * are queued or in flight. */
+sgs_status sgs_set_instances(sgs_handle* h, int32_t n_instances, int32_t instance_rank);
+
 /* T(b) fit (C3): hinge least squares over n measured (b, T_ns)
  * points; out = {t0, k0, k1, t1, sse}, prof = rounded integer profile.
  * Returns SGS_E_INVAL when no breakpoint is identifiable. */
@@ -354,9 +370,11 @@ sgs_status sgs_rope_table(float* host_out, int32_t max_pos, int32_t hd, double t
 /* a4/K10: causal prefill attention.  q device bf16 [T, nq, hd]; k, v device
  * bf16 [T, nkv, hd] (contiguous, not paged); prompt p spans rows
  * [offs[p], offs[p+1]) (offs device int32 [n_prompts+1]); out bf16 [T, nq, hd].
- * workspace: device, >= sgs_prefill_workspace_bytes(T, n_prompts) bytes (the
- * 64-query block list); SGS_E_NOMEM when smaller.  Synchronises stream. */
-int64_t sgs_prefill_workspace_bytes(int32_t T, int32_t n_prompts);
+ * hd = 128 runs the tcgen05/TMEM kernel (P.V in fp16 on fp16(bf16 v), exact
+ * conversion); other hd the mma.sync kernel.  workspace: device, >=
+ * sgs_prefill_workspace_bytes(T, n_prompts, nkv, hd) bytes (query-block list
+ * and the fp16 v copy); SGS_E_NOMEM when smaller.  Synchronises stream. */
+int64_t sgs_prefill_workspace_bytes(int32_t T, int32_t n_prompts, int32_t nkv, int32_t hd);
 sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
                                     int32_t n_prompts, int32_t nq, int32_t nkv, int32_t hd, void* out,
                                     void* workspace, int64_t workspace_bytes, void* stream);

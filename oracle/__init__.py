@@ -10,6 +10,7 @@ Functions and the paper passages they follow (PAPER.md line numbers):
   dispatch         C5  Alg. 2 + Eq. 2
   tb_fit/T_ps      C3  piecewise-linear T(b), hinge fit
   min_merge_gain   C3  lemma T(x+y) < T(x)+T(y)
+  elastic_plan     NEXT-4 delta vs delta' (one more DP unit)
   brute_force      C4  LF vs all admission orders
   attention        C7  naive softmax attention, fp64
   decoder_layer/head  C6  one layer / final norm + LM head    (chained layer-local parity)
@@ -29,7 +30,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "src")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SOURCES = ["sched_sim.cpp", "dispatch.cpp", "tb.cpp", "model.cpp", "capi.cpp"]
+_SOURCES = ["sched_sim.cpp", "dispatch.cpp", "tb.cpp", "model.cpp", "elastic.cpp", "capi.cpp"]
 
 
 def build(force: bool = False) -> str:
@@ -75,6 +76,10 @@ def _declare(L):
     L.oracle_dispatch.argtypes = [ctypes.c_int32, P_i64, P_i32, P_i32, ctypes.c_int32, ctypes.c_int32,
                                   ctypes.c_int32, ctypes.c_int64, P_i64, ctypes.c_int32, ctypes.c_int32,
                                   ctypes.c_int32, P_i32, P_i64, P_i64]
+    L.oracle_elastic_plan.argtypes = [ctypes.c_int32, P_i64, P_i32, P_i32, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_int64, P_i64, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_int64, P_i64]
+    L.oracle_elastic_plan.restype = ctypes.c_int32
     L.oracle_nearest_rank.argtypes = [ctypes.c_int32, P_i64, ctypes.c_int32]
     L.oracle_nearest_rank.restype = ctypes.c_int64
     L.oracle_T_ps.argtypes = [P_i64, ctypes.c_int64, P_i64]
@@ -231,6 +236,21 @@ def dispatch(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profile, 
     nsc = int(info[6])
     return dict(instance=inst, n_l=int(info[0]), n_tail=int(info[1]), L_alpha=int(info[2]), L_r=int(info[3]),
                 score=_i128(info[4], info[5]), scores=[_i128(sc[2 * i], sc[2 * i + 1]) for i in range(nsc)])
+
+
+def elastic_plan(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profile, delta_ps: int, alpha_pct=20,
+                 score_max=0, tail_ceil=0):
+    """NEXT-4: predicted generation ps on N and N+1 instances, delta' and the decision."""
+    n = len(ids)
+    ids = np.ascontiguousarray(ids, np.int64)
+    P = np.ascontiguousarray(P, np.int32)
+    hint = np.ascontiguousarray(hint, np.int32)
+    out = np.zeros(6, np.int64)
+    dec = lib().oracle_elastic_plan(n, _p(ids, P_i64), _p(P, P_i32), _p(hint, P_i32), N, B, page, pool_pages,
+                                    _p(_prof(profile), P_i64), alpha_pct, score_max, tail_ceil, int(delta_ps),
+                                    _p(out, P_i64))
+    return dict(t_gen_ps=(_i128(out[0], out[1]), _i128(out[2], out[3])), delta_prime_ps=_i128(out[4], out[5]),
+                scale_out=bool(dec))
 
 
 def nearest_rank(v, q_pct):

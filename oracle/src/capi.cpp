@@ -76,6 +76,24 @@ int32_t oracle_dispatch(int32_t n, const int64_t* ids, const int32_t* P, const i
   return 0;
 }
 
+// NEXT-4: out128 = {t_gen(N) hi, lo, t_gen(N+1) hi, lo, delta' hi, lo}, returns the decision
+int32_t oracle_elastic_plan(int32_t n, const int64_t* ids, const int32_t* P, const int32_t* hint, int32_t N, int32_t B,
+                            int32_t page, int64_t pool_pages, const int64_t* profile4, int32_t alpha_pct,
+                            int32_t score_max, int32_t tail_ceil, int64_t delta_ps, int64_t* out128) {
+  DispatchIn in;
+  in.id.assign(ids, ids + n);
+  in.P.assign(P, P + n);
+  in.hint.assign(hint, hint + n);
+  in.N = N, in.B = B, in.page = page, in.pool_pages = pool_pages;
+  in.prof = Profile{profile4[0], profile4[1], profile4[2], profile4[3]};
+  in.alpha_pct = alpha_pct, in.score_max = score_max, in.tail_ceil = tail_ceil;
+  const ElasticOut o = elastic_plan(in, (__int128)delta_ps);
+  split128(o.t_gen_ps[0], out128);
+  split128(o.t_gen_ps[1], out128 + 2);
+  split128(o.delta_prime_ps, out128 + 4);
+  return o.scale_out;
+}
+
 int64_t oracle_nearest_rank(int32_t n, const int64_t* v, int32_t q_pct) {
   return nearest_rank(std::vector<int64_t>(v, v + n), q_pct);
 }

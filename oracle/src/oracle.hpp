@@ -63,6 +63,16 @@ struct DispatchOut {
   std::vector<__int128> scores;    // score per N_l = 1..N-1 (empty when degenerate)
 };
 DispatchOut dispatch(const DispatchIn& in);
+
+// NEXT-4: predicted generation time on N and N + 1 instances and
+// the scale-out decision delta >= delta' (elastic.cpp).
+struct ElasticOut {
+  __int128 t_gen_ps[2] = {0, 0};
+  __int128 delta_prime_ps = 0;
+  int scale_out = 0;
+};
+__int128 predicted_generation_ps(const DispatchIn& in);
+ElasticOut elastic_plan(const DispatchIn& in, __int128 delta_ps);
 int64_t nearest_rank(std::vector<int64_t> v, int q_pct);
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,7 @@ SOURCES = [
     "kernels/gemm.cu",
     "kernels/attention.cu",
     "kernels/prefill_attn.cu",
+    "kernels/prefill_attn_tc.cu",
     "kernels/elementwise.cu",
     "engine/engine.cu",
     "host/sched.cpp",

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -262,6 +263,31 @@ sgs_status sgs_dispatch_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t*
   return SGS_OK;
 }
 
+sgs_status sgs_elastic_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* ids, const int32_t* prompt_len,
+                            const int32_t* hint, int64_t pool_pages, int64_t delta_ps, int64_t t_gen_ps[2],
+                            int64_t* delta_prime_ps, int32_t* scale_out) {
+  if (!e || n < 0 || (n > 0 && (!ids || !prompt_len || !hint)) || e->n_instances < 1 || pool_pages < 1 ||
+      e->max_batch < 1 || e->page_size < 1)
+    return SGS_E_INVAL;
+  sgs::DispatchCfg dc{e->n_instances, e->max_batch, e->page_size, pool_pages, e->profile.t0_ns, e->profile.k0_ps,
+                      e->profile.b_star, e->profile.k1_ps, e->alpha_pct, e->score, e->tail_ceil, e->dispatch,
+                      e->sample_seed};
+  __int128 t[2];
+  t[0] = sgs::predicted_generation_ps(dc, n, ids, prompt_len, hint);
+  dc.N += 1;
+  t[1] = sgs::predicted_generation_ps(dc, n, ids, prompt_len, hint);
+  const __int128 dp = t[0] - t[1];
+  if (t_gen_ps) t_gen_ps[0] = (int64_t)t[0], t_gen_ps[1] = (int64_t)t[1];
+  if (delta_prime_ps) *delta_prime_ps = (int64_t)dp;
+  if (scale_out) *scale_out = dp > 0 && (__int128)delta_ps >= dp ? 1 : 0;
+  return SGS_OK;
+}
+
+sgs_status sgs_set_instances(sgs_handle* h, int32_t n_instances, int32_t instance_rank) {
+  if (!h || n_instances < 1 || instance_rank < 0 || instance_rank >= n_instances) return SGS_E_INVAL;
+  return h->eng.set_instances(n_instances, instance_rank);
+}
+
 // ------------------------------------------------------------------ kernel-level entry points
 static sgs_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SGS_OK : SGS_E_CUDA; }
 
@@ -394,9 +420,11 @@ sgs_status sgs_op_rope_append(const float* qkv, const void* bias, const int32_t*
                                       nullptr, nullptr, T, nq, nkv, hd, page, reinterpret_cast<cudaStream_t>(stream)));
 }
 
-int64_t sgs_prefill_workspace_bytes(int32_t T, int32_t n_prompts) {
-  // one (prompt, 64-query block) pair per block: sum ceil(len/64) <= T/64 + n_prompts
-  return 8 * ((int64_t)(T > 0 ? T : 0) / 64 + (n_prompts > 0 ? n_prompts : 0) + 1);
+int64_t sgs_prefill_workspace_bytes(int32_t T, int32_t n_prompts, int32_t nkv, int32_t hd) {
+  // (prompt, query block) pairs: sum ceil(len/64) <= T/64 + n_prompts; plus
+  // the fp16 copy of v for the tcgen05 kernel (hd 128)
+  const int64_t blocks = 8 * ((int64_t)(T > 0 ? T : 0) / 64 + (n_prompts > 0 ? n_prompts : 0) + 1);
+  return (blocks + 255) / 256 * 256 + (hd == 128 ? (int64_t)(T > 0 ? T : 0) * nkv * hd * 2 : 0);
 }
 
 sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v, const int32_t* offs,
@@ -409,15 +437,26 @@ sgs_status sgs_op_prefill_attention(const void* q, const void* k, const void* v,
   if (cudaMemcpyAsync(ho.data(), offs, ho.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return SGS_E_CUDA;
+  const int T = ho[n_prompts];
+  const bool tc = hd == 128 && !(std::getenv("SGS_PREFILL_LEGACY") && std::atoi(std::getenv("SGS_PREFILL_LEGACY")));
+  const int blk = tc ? 128 : 64;
   std::vector<int32_t> qb;
   for (int p = 0; p < n_prompts; ++p)
-    for (int b = 0; b < (ho[p + 1] - ho[p] + 63) / 64; ++b) qb.push_back(p), qb.push_back(b);
+    for (int b = 0; b < (ho[p + 1] - ho[p] + blk - 1) / blk; ++b) qb.push_back(p), qb.push_back(b);
   if (qb.empty()) return SGS_OK;
-  if (!workspace || (int64_t)qb.size() * 4 > workspace_bytes) return SGS_E_NOMEM;
+  if (!workspace || sgs_prefill_workspace_bytes(T, n_prompts, nkv, hd) > workspace_bytes) return SGS_E_NOMEM;
   int32_t* d_qb = reinterpret_cast<int32_t*>(workspace);
   cudaError_t e = cudaMemcpyAsync(d_qb, qb.data(), qb.size() * 4, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess)
+  if (e == cudaSuccess && tc) {
+    // the kernel's P.V operand: fp16(bf16 v) (exact), in the workspace
+    const int64_t blocks = 8 * ((int64_t)T / 64 + n_prompts + 1);
+    void* vh = reinterpret_cast<uint8_t*>(workspace) + (blocks + 255) / 256 * 256;
+    e = sgs::bf16_to_f16(v, vh, (int64_t)T * nkv * hd, st);
+    if (e == cudaSuccess)
+      e = sgs::attn_prefill_tc(q, k, vh, offs, d_qb, (int)qb.size() / 2, T, nq, nkv, out, st);
+  } else if (e == cudaSuccess) {
     e = sgs::attn_prefill(q, k, v, offs, d_qb, (int)qb.size() / 2, nq, nkv, hd, out, st);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host block list dies here
   return cuda_status(e);
 }

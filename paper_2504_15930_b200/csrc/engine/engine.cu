@@ -273,6 +273,11 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   // (profiles/README.md r02: the norm and the grid barrier stay on the
   // critical path, only the launch is saved); SGS_FUSED_NORM=1 turns it on
   if (const char* nf = std::getenv("SGS_FUSED_NORM")) fused_norm_ = std::atoi(nf) != 0;
+  // prefill attention: the tcgen05 kernel for hd 128 (128-query blocks), the
+  // mma.sync kernel otherwise or with SGS_PREFILL_LEGACY=1 (64-query blocks)
+  qblk_ = (m.head_dim == 128 && !(std::getenv("SGS_PREFILL_LEGACY") && std::atoi(std::getenv("SGS_PREFILL_LEGACY"))))
+              ? 128
+              : 64;
   tok_host_cap_ = (int64_t)e.max_batch * max_gen_;
   for (int k = 0; k < 2; ++k) {
     CK(cudaMallocHost(&meta_bufs_[k], L_.meta_bytes), "cudaMallocHost(meta)");
@@ -344,6 +349,16 @@ sgs_status Engine::load_weights(const sgs_weights* w, uint8_t* base, cudaStream_
     }
   }
   CK(cudaStreamSynchronize(st), "weight copy sync");  // the caller may free its buffers on return
+  return SGS_OK;
+}
+
+sgs_status Engine::set_instances(int32_t n_instances, int32_t instance_rank) {
+  if (!sched.idle() || !infl_.empty() || !ready_.empty()) {
+    err = "the DP layout changes only between RL batches (nothing queued, in flight or unreturned)";
+    return SGS_E_STATE;
+  }
+  e_.n_instances = n_instances;
+  e_.instance_rank = instance_rank;
   return SGS_OK;
 }
 
@@ -685,7 +700,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
       tok.insert(tok.end(), s.prompt.begin(), s.prompt.end());
       for (int j = 0; j < s.P; ++j) pos.push_back(j), slot.push_back(s.slot);
       offs.push_back(offs.back() + s.P);
-      for (int b = 0; b < (s.P + 63) / 64; ++b) qb.push_back((int32_t)k), qb.push_back(b);
+      for (int b = 0; b < (s.P + qblk_ - 1) / qblk_; ++b) qb.push_back((int32_t)k), qb.push_back(b);
       last.push_back(offs.back() - 1);
       pfs.push_back(s.slot);
       pft.push_back(0);
@@ -695,6 +710,14 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     c.o_pos = put(pos.data(), pos.size());
     c.o_slot = put(slot.data(), slot.size());
     c.o_offs = put(offs.data(), offs.size());
+    {
+      // query blocks with more KV tiles first (causal: block b reads b + 1 tiles)
+      std::vector<std::pair<int32_t, int32_t>> v;
+      for (size_t x = 0; x + 1 < qb.size(); x += 2) v.push_back({qb[x + 1], qb[x]});
+      std::stable_sort(v.begin(), v.end(), [](const std::pair<int32_t, int32_t>& a,
+                                              const std::pair<int32_t, int32_t>& c) { return a.first > c.first; });
+      for (size_t x = 0; x < v.size(); ++x) qb[2 * x] = v[x].second, qb[2 * x + 1] = v[x].first;
+    }
     c.o_qb = put(qb.data(), qb.size());
     c.nqb = (int)qb.size() / 2;
     c.o_last = put(last.data(), last.size());
@@ -1089,11 +1112,14 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     CK(rmsnorm(h_, Ly.n1, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm1");
     CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, T, false), "gemm qkv");
     CK(rope_append(qkv_, Ly.bqkv, d_pos, d_slot, bt_, L_.max_pages, rope_, q_, Ly.kv, kc_, vc_, T, nq, nkv, hd,
-                   e_.page_size, st_),
+                   e_.page_size, st_, qblk_ == 128),
        "rope_append");
     KRec kr;
     ktic(&kr, 2);
-    CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
+    if (qblk_ == 128)  // tcgen05/TMEM flash attention (hd 128)
+      CK(attn_prefill_tc(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, L_.tmax, nq, nkv, ao_, st_), "attn_prefill_tc");
+    else
+      CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
     // algorithmic bytes: q, k, v in and o out once per row (bf16); flops from the chunk's prompts
     ktoc(&kr, 0.0, 2.0 * hd * (2.0 * nq + 2.0 * nkv), cur_pf_attn_flops_ / std::max(T, 1), T);
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
@@ -1150,7 +1176,7 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, 
   const size_t o_offs = meta.size();
   meta.push_back(0), meta.push_back(T);
   const size_t o_qb = meta.size();
-  for (int b = 0; b < (T + 63) / 64; ++b) meta.push_back(0), meta.push_back(b);
+  for (int b = 0; b < (T + qblk_ - 1) / qblk_; ++b) meta.push_back(0), meta.push_back(b);
   const size_t o_last = meta.size();
   meta.push_back(T - 1), meta.push_back(0), meta.push_back(0);  // last row, pf slot, pf tok
   meta.push_back(0), meta.push_back(0);                         // sample id (lo, hi)
@@ -1160,7 +1186,7 @@ sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, 
   CK(apply_bt_deltas(bt_, L_.max_pages, MD, np, st_), "bt");
   std::vector<int32_t> idx(1, 0);
   cur_pf_attn_flops_ = 2.0 * m_.n_q_heads * m_.head_dim * (double)T * (T + 1);
-  sgs_status s = prefill_chunk(idx, 0, MD + o_tok, MD + o_pos, MD + o_slot, MD + o_offs, MD + o_qb, (T + 63) / 64,
+  sgs_status s = prefill_chunk(idx, 0, MD + o_tok, MD + o_pos, MD + o_slot, MD + o_offs, MD + o_qb, (T + qblk_ - 1) / qblk_,
                                MD + o_last, MD + o_last + 1, MD + o_last + 2, T, dump, layer, h_in);
   if (s != SGS_OK) return s;
   CK(cudaStreamSynchronize(st_), "debug sync");

@@ -53,6 +53,7 @@ class Engine {
                     int32_t* n_mine);
   sgs_status step(sgs_completion* out, int32_t cap, int32_t* n_out);
   sgs_status load_weights_seed(uint64_t seed);
+  sgs_status set_instances(int32_t n_instances, int32_t instance_rank);
   sgs_status checksum(int64_t tensor_id, uint64_t* out);
   sgs_status comm_init(const uint8_t id[128], int rank, int world);
   sgs_status update_weights(const sgs_weights* src, int root);
@@ -185,6 +186,7 @@ class Engine {
   unsigned int* norm_bar_ = nullptr;          // PreNorm grid barriers: 2 per site (2 per layer + final)
   bool fused_norm_ = false;                   // RMSNorm fused into the decode GEMMs (SGS_FUSED_NORM=1)
   int64_t dec_launch_ = 0;                    // decode-program launches (PreNorm barrier parity)
+  int qblk_ = 64;                             // prefill attention query block (128: tcgen05 kernel)
   int32_t* tok_host_ = nullptr;  // pinned, completed tokens (the current one of tok_bufs_)
   int64_t tok_host_cap_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

@@ -291,6 +291,32 @@ int dispatch_alg2(const DispatchCfg& c, int n, const uint64_t* ids, const int32_
   return n_l;
 }
 
+// ------------------------------------------------------------------ elastic DP (NEXT-4)
+__int128 predicted_generation_ps(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P,
+                                 const int32_t* hint) {
+  std::vector<int32_t> inst(n, 0);
+  dispatch_alg2(c, n, ids, P, hint, inst.data());
+  __int128 makespan = 0;
+  for (int k = 0; k < c.N; ++k) {
+    std::vector<Sample> mine;
+    for (int i = 0; i < n; ++i) {
+      if (inst[i] != k) continue;
+      Sample s;
+      s.id = ids[i], s.P = P[i], s.d = hint[i], s.hint = hint[i], s.batch = 0;  // the hint as the length
+      mine.push_back(std::move(s));
+    }
+    if (mine.empty()) continue;
+    Scheduler sch;
+    sch.init(c.B, c.page, c.pool_pages);
+    sch.submit(std::move(mine));
+    IterPlan plan;
+    __int128 t = 0;
+    while (sch.plan(&plan)) t += tb_ps(c, plan.b);  // b = samples that ran in the iteration
+    makespan = std::max(makespan, t);
+  }
+  return makespan;
+}
+
 // ------------------------------------------------------------------ T(b) fit
 // Least squares on the hinge basis [1, b, (b - b*)+] for every measured b* with
 // >= 2 distinct points at or below and >= 1 above; minimum SSE wins, ties ->

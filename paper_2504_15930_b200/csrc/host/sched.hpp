@@ -98,6 +98,14 @@ struct DispatchCfg {
 int dispatch_alg2(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P, const int32_t* hint,
                   int32_t* instance);
 
+// ------------------------------------------------------------------ elastic DP (NEXT-4)
+// Predicted generation time (ps) of a batch on c.N instances: Alg. 2, then
+// each instance's longest-first schedule on the hints as lengths (the same
+// Scheduler the engine runs), summing T(b_t) of the integer profile; the
+// makespan over instances (R25).
+__int128 predicted_generation_ps(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P,
+                                 const int32_t* hint);
+
 // ------------------------------------------------------------------ T(b) fit
 bool fit_tb(int n, const double* b, const double* T_ns, double out[5], int64_t* b_star, int64_t prof[4]);
 

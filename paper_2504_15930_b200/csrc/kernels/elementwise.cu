@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(ROPE_THREADS)
                        const int32_t* __restrict__ bt, int max_pages, const float* __restrict__ cs,
                        __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv,
                        __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out, int T, int nq, int nkv,
-                       int hd, int page, int per) {
+                       int hd, int page, int per, int v_f16) {
   pdl_trigger();
   const int half = hd >> 1;
   const int nh = nq + 2 * nkv;
@@ -167,8 +167,15 @@ __global__ void __launch_bounds__(ROPE_THREADS)
       }
       __nv_bfloat16* cont = isv ? v_out : k_out;
       if (cont) {
-        *reinterpret_cast<__nv_bfloat162*>(cont + ((size_t)t * nkv + kvh) * hd + i) = o1;
-        *reinterpret_cast<__nv_bfloat162*>(cont + ((size_t)t * nkv + kvh) * hd + i + half) = o2;
+        if (isv && v_f16) {  // fp16(bf16 v): exact, the tcgen05 prefill attention's P.V operand
+          const __half2 h1 = __floats2half2_rn(__low2float(o1), __high2float(o1));
+          const __half2 h2 = __floats2half2_rn(__low2float(o2), __high2float(o2));
+          *reinterpret_cast<__half2*>(cont + ((size_t)t * nkv + kvh) * hd + i) = h1;
+          *reinterpret_cast<__half2*>(cont + ((size_t)t * nkv + kvh) * hd + i + half) = h2;
+        } else {
+          *reinterpret_cast<__nv_bfloat162*>(cont + ((size_t)t * nkv + kvh) * hd + i) = o1;
+          *reinterpret_cast<__nv_bfloat162*>(cont + ((size_t)t * nkv + kvh) * hd + i + half) = o2;
+        }
       }
     }
   }
@@ -177,7 +184,8 @@ __global__ void __launch_bounds__(ROPE_THREADS)
 
 cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
                         const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
-                        void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream) {
+                        void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream,
+                        int v_f16) {
   if (T <= 0) return cudaSuccess;
   if (hd % 4) return cudaErrorInvalidValue;
   const int nduo = (nq + 2 * nkv) * (hd / 2) / 2;
@@ -192,7 +200,22 @@ cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, 
                     reinterpret_cast<const __nv_bfloat16*>(bias), pos, slot, block_table, max_pages, cos_sin,
                     reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(kv),
                     reinterpret_cast<__nv_bfloat16*>(k_out), reinterpret_cast<__nv_bfloat16*>(v_out), T, nq, nkv, hd,
-                    page, per);
+                    page, per, v_f16);
+}
+
+// ------------------------------------------------------------------ bf16 -> fp16 (exact for the normal fp16 range)
+__global__ void bf16_to_f16_kernel(const __nv_bfloat16* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2half_rn(__bfloat162float(src[i]));
+}
+
+cudaError_t bf16_to_f16(const void* src, void* dst, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  bf16_to_f16_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(src),
+                                                 reinterpret_cast<__half*>(dst), n);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ embedding gather

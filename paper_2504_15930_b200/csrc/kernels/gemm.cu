@@ -534,6 +534,11 @@ static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t
   return true;
 }
 
+// shared with the other tcgen05 kernels (prefill attention)
+bool tmap_bf16_rows(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc) {
+  return cached_tmap(out, ptr, rows, cols, box_rows, kc);
+}
+
 static int sm_count() {
   static int n[64] = {0};
   int dev = 0;

@@ -1,5 +1,6 @@
 // Host-side launchers of the sm_100a kernels (internal to libsgs).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -82,21 +83,33 @@ cudaError_t attn_decode(const void* q, const void* kv, const int32_t* block_tabl
                         int hd, int page, int max_pages, void* out, int out_fp32, float* part_o, float* part_ml,
                         int* arrive, cudaStream_t stream);
 
+// 2-byte-element row-major [rows, cols] matrix as a TMA map of (64 cols, box_rows,
+// kc 64-col chunks) boxes with the 128-byte swizzle (cached per pointer/shape).
+bool tmap_bf16_rows(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc);
+
 // ---- prefill attention (prefill_attn.cu): causal within each prompt.
 // q [T, nq, hd], k/v [T, nkv, hd] contiguous bf16; prompt p spans rows
 // [offs[p], offs[p+1]).  out bf16 [T, nq, hd].
 cudaError_t attn_prefill(const void* q, const void* k, const void* v, const int32_t* offs, const int32_t* qblocks,
                          int n_qblocks, int nq, int nkv, int hd, void* out, cudaStream_t stream);
+// tcgen05/TMEM/TMA flash attention for hd = 128 (prefill_attn_tc.cu): same
+// contract, except v is fp16 (= fp16(bf16 v), exact) and the work list holds
+// (prompt, 128-query block) pairs; T = rows of q/k/v (TMA bounds).
+cudaError_t attn_prefill_tc(const void* q, const void* k, const void* v_f16, const int32_t* offs,
+                            const int32_t* qblocks128, int n_qblocks128, int T, int nq, int nkv, void* out,
+                            cudaStream_t stream);
 
 // ---- elementwise (elementwise.cu)
 cudaError_t rmsnorm(const float* x, const void* w, void* y, const int32_t* rows, int T, int d, float eps,
                     cudaStream_t stream);
 cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, const int32_t* slot,
                         const int32_t* block_table, int max_pages, const float* cos_sin, void* q_out, void* kv,
-                        void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream);
+                        void* k_out, void* v_out, int T, int nq, int nkv, int hd, int page, cudaStream_t stream,
+                        int v_f16 = 0);  // v_f16: the contiguous v copy as fp16(bf16 v)
 cudaError_t embed(const void* E, const int32_t* tokens, const int32_t* slots, const int32_t* last_tok, float* h,
                   int T, int d, cudaStream_t stream);
 cudaError_t silu_mul(const float* gu, void* m, int T, int f, cudaStream_t stream);
+cudaError_t bf16_to_f16(const void* src, void* dst, int64_t n, cudaStream_t stream);
 cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, const int32_t* slot,
                         const int32_t* tok_idx, int32_t* last_tok, int32_t* out_hist, int max_gen,
                         cudaStream_t stream);

@@ -36,7 +36,7 @@ EXPORTS = [
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
     "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer", "sgs_op_sample_top_p",
     "sgs_weight_tensors", "sgs_stage_weights", "sgs_prefill_workspace_bytes", "sgs_host_state",
-    "sgs_op_decode_attention_timed",
+    "sgs_op_decode_attention_timed", "sgs_elastic_plan", "sgs_set_instances",
 ]
 
 
@@ -104,7 +104,9 @@ def _declare(L):
     L.sgs_weight_tensors.argtypes = [P(ModelCfg), P(i64), P(i64), P(i64), i32, P(i32)]
     L.sgs_stage_weights.argtypes = [vp, P(Weights)]
     L.sgs_host_state.argtypes = [vp, P(i64), P(i64), P(i64)]
-    L.sgs_prefill_workspace_bytes.argtypes = [i32, i32]
+    L.sgs_elastic_plan.argtypes = [P(EngineCfg), i32, P(u64), P(i32), P(i32), i64, i64, P(i64), P(i64), P(i32)]
+    L.sgs_set_instances.argtypes = [vp, i32, i32]
+    L.sgs_prefill_workspace_bytes.argtypes = [i32, i32, i32, i32]
     L.sgs_prefill_workspace_bytes.restype = i64
     L.sgs_destroy.argtypes = [vp]
     L.sgs_destroy.restype = None
@@ -311,6 +313,10 @@ class Instance:
         _check(lib().sgs_host_state(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), self.h)
         return a.value, b.value, c.value
 
+    def set_instances(self, n_instances: int, instance_rank: int):
+        """Elastic DP (NEXT-4): change the data-parallel layout between RL batches."""
+        _check(lib().sgs_set_instances(self.h, n_instances, instance_rank), self.h)
+
     def pending(self):
         q, a = ctypes.c_int64(), ctypes.c_int64()
         _check(lib().sgs_pending(self.h, ctypes.byref(q), ctypes.byref(a)), self.h)
@@ -500,6 +506,26 @@ def dispatch_plan(ids, prompt_len, hint, n_instances, max_batch, page, pool_page
     return inst, nl.value
 
 
+def elastic_plan(ids, prompt_len, hint, n_instances, max_batch, page, pool_pages, profile, delta_ps, alpha_pct=20,
+                 score=0, tail_ceil=0):
+    """NEXT-4: predicted generation ps on N and N+1 instances, delta' and the decision."""
+    e = EngineCfg()
+    e.n_instances, e.max_batch, e.page_size = n_instances, max_batch, page
+    e.profile = TbProfile(*profile)
+    e.alpha_pct, e.score, e.tail_ceil, e.dispatch = alpha_pct, score, tail_ceil, 0
+    n = len(ids)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    P = np.ascontiguousarray(prompt_len, np.int32)
+    h = np.ascontiguousarray(hint, np.int32)
+    t = np.zeros(2, np.int64)
+    dp = ctypes.c_int64()
+    so = ctypes.c_int32()
+    _check(lib().sgs_elastic_plan(ctypes.byref(e), n, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _i32p(P),
+                                  _i32p(h), pool_pages, int(delta_ps), t.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  ctypes.byref(dp), ctypes.byref(so)))
+    return dict(t_gen_ps=(int(t[0]), int(t[1])), delta_prime_ps=dp.value, scale_out=bool(so.value))
+
+
 def rope_table(max_pos: int, hd: int, theta: float) -> np.ndarray:
     out = np.zeros((max_pos, hd // 2, 2), np.float32)
     _check(lib().sgs_rope_table(out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), max_pos, hd, theta))
@@ -554,7 +580,7 @@ def op_prefill_attention(q, k, v, offs, out, workspace=None):
     import torch
     T, nq, hd = q.shape
     nkv = k.shape[1]
-    need = lib().sgs_prefill_workspace_bytes(T, offs.numel() - 1)
+    need = lib().sgs_prefill_workspace_bytes(T, offs.numel() - 1, nkv, hd)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     _check(lib().sgs_op_prefill_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(offs), offs.numel() - 1, nq, nkv, hd,

@@ -252,3 +252,45 @@ def test_host_state_bounded_without_trace_and_id_reuse():
         inst.submit_trace(workload.make_trace(50, 8, 20, 1.0, 120, shape.vocab, seed=k, id_base=1000 * k))
         inst.run()
     assert inst.host_state()[0] == 150
+
+
+def test_elastic_plan_matches_oracle():
+    # NEXT-4: the product's delta' (Alg. 2 + its own scheduler, timed
+    # with the integer T(b) profile) equals the oracle's bit for bit, and the
+    # decision flips exactly at delta = delta'
+    import json
+    import os
+    from paper_2504_15930_b200 import elastic_plan
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "elastic_delta_prime.json")))
+    for delta, dec in g["decisions"]:
+        r = elastic_plan(g["ids"], g["P"], g["hint"], g["N"], g["B"], g["page"], g["pool"], g["profile"], delta)
+        assert r["t_gen_ps"] == tuple(g["t_gen_ps"]) and r["scale_out"] == dec
+    rng = np.random.default_rng(3)
+    for _ in range(60):
+        n, N = int(rng.integers(1, 120)), int(rng.integers(1, 6))
+        ids, P, hint = rng.permutation(10_000)[:n], rng.integers(1, 600, n), rng.integers(1, 3000, n)
+        prof = (int(rng.integers(100, 5000)), int(rng.integers(1, 100)) * 1000, int(rng.integers(2, 300)),
+                int(rng.integers(100, 300)) * 1000)
+        B, pool = int(rng.integers(1, 64)), int(rng.integers(400, 20_000))
+        if ((P + hint - 1 + 15) // 16).max() > pool:
+            continue
+        o = oracle.elastic_plan(ids, P, hint, N, B, 16, pool, prof, 0)
+        r = elastic_plan(ids, P, hint, N, B, 16, pool, prof, o["delta_prime_ps"])
+        assert r["t_gen_ps"] == o["t_gen_ps"]
+        assert r["delta_prime_ps"] == o["delta_prime_ps"]
+        assert r["scale_out"] == (o["delta_prime_ps"] > 0)
+
+
+def test_set_instances_between_batches():
+    shape = workload.MODELS["tiny"]
+    tr = workload.make_trace(40, 8, 20, 1.0, 100, shape.vocab, seed=4)
+    inst = Instance(shape, 8, 400, device=None, n_pages=400, n_instances=1, instance_rank=0, profile=PROF)
+    assert inst.submit_trace(tr) == 40
+    with pytest.raises(SgsError) as e:
+        inst.set_instances(2, 0)
+    assert e.value.code == -3
+    inst.run()
+    inst.set_instances(2, 1)
+    tr2 = workload.make_trace(40, 8, 20, 1.0, 100, shape.vocab, seed=5, id_base=1000)
+    exp, _ = dispatch_plan(tr2.ids, tr2.prompt_len, tr2.hint, 2, 8, 16, 400, PROF)
+    assert inst.submit_trace(tr2) == int((exp == 1).sum())

@@ -373,3 +373,35 @@ def test_dispatch_eq2_argmin_n4_memory_cap_golden(mode, key):
     assert r["scores"] == e["scores"]
     assert r["n_l"] == e["n_l"]
     assert r["instance"].tolist() == e["instance"]
+
+
+def test_elastic_delta_prime_golden():
+    # tests/golden/elastic_delta_prime.json: NEXT-4's delta' for N = 1 -> 2 by hand (reading R25)
+    g = json.load(open(os.path.join(GOLD, "elastic_delta_prime.json")))
+    for delta, dec in g["decisions"]:
+        r = oracle.elastic_plan(g["ids"], g["P"], g["hint"], g["N"], g["B"], g["page"], g["pool"], g["profile"], delta)
+        assert r["t_gen_ps"] == tuple(g["t_gen_ps"])
+        assert r["delta_prime_ps"] == g["delta_prime_ps"]
+        assert r["scale_out"] == dec
+
+
+def test_elastic_delta_prime_is_simulated_makespan_difference():
+    # delta' composes C5 and C2: equals max over instances of sched_sim time on the dispatched subsets
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        n, N = int(rng.integers(2, 60)), int(rng.integers(1, 5))
+        ids, P, hint = np.arange(n), rng.integers(1, 40, n), rng.integers(1, 200, n)
+        prof = (int(rng.integers(100, 3000)), int(rng.integers(1, 50)) * 1000, int(rng.integers(2, 64)),
+                int(rng.integers(50, 200)) * 1000)
+        B, page, pool = int(rng.integers(1, 16)), 16, 100000
+        r = oracle.elastic_plan(ids, P, hint, N, B, page, pool, prof, 0)
+        for k, NN in enumerate((N, N + 1)):
+            inst = oracle.dispatch(ids, P, hint, NN, B, page, pool, prof)["instance"]
+            mk = 0
+            for i in range(NN):
+                sel = inst == i
+                if sel.any():
+                    mk = max(mk, oracle.sched_sim(ids[sel], P[sel], hint[sel], hint[sel], B, page, pool,
+                                                  profile=prof)["time_ps"])
+            assert r["t_gen_ps"][k] == mk
+        assert r["delta_prime_ps"] == r["t_gen_ps"][0] - r["t_gen_ps"][1]
