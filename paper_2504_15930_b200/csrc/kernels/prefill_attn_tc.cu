@@ -31,7 +31,7 @@ constexpr int PF_M = 128;                   // queries per CTA
 constexpr int PF_N = 128;                   // keys per KV tile
 constexpr int PF_CHUNK = 128 * 64 * 2;      // [128 rows][64 cols] 2-byte, 128-byte swizzle = 16 KB
 constexpr int PF_TILE = 2 * PF_CHUNK;       // 128 x 128 = 32 KB
-constexpr int PF_SMEM = 1024 + 6 * PF_TILE + 256;
+constexpr int PF_SMEM = 1024 + 6 * PF_TILE + 512;
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -62,10 +62,13 @@ constexpr uint32_t PF_IDESC_QK = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t
                                  ((uint32_t)(PF_M >> 4) << 24);
 constexpr uint32_t PF_IDESC_PV = (1u << 4) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(PF_M >> 4) << 24);
 
+// Persistent: one CTA per SM walks the work items (query block, head) with a
+// stride of gridDim.x; barrier phases run on global tile / item counters, so
+// the next item's Q, K and V loads overlap the current item's softmax.
 __global__ void __launch_bounds__(192, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ offs,
-                           const int32_t* __restrict__ qblocks, int nq, int nkv, float scale_log2,
+                           const int32_t* __restrict__ qblocks, int n_items, int nq, int nkv, float scale_log2,
                            __nv_bfloat16* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -75,25 +78,41 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sP = sV + 2 * PF_TILE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + PF_TILE);
   uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 3, *v_full = bars + 5, *v_empty = bars + 7,
-           *s_full = bars + 9, *s_empty = bars + 11, *p_full = bars + 13, *pv_done = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+           *s_full = bars + 9, *s_empty = bars + 11, *p_full = bars + 13, *pv_done = bars + 14, *q_empty = bars + 15,
+           *o_free = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.y, hk = h / (nq / nkv);
-  const int p = qblocks[2 * blockIdx.x], qb = qblocks[2 * blockIdx.x + 1];
-  const int off = offs[p], P = offs[p + 1] - off;
-  const int q0 = qb * PF_M;
-  const int qrows = min(PF_M, P - q0);
-  const int nt = (q0 + qrows - 1) / PF_N + 1;  // KV tiles up to the causal diagonal
+  const int g_sz = nq / nkv;
+  // work item -> (prompt, query block, head); consecutive items are the heads
+  // of one query block, so co-running CTAs share the K/V tiles in L2
+  struct Item {
+    int h, hk, off, P, q0, qrows, nt;
+  };
+  auto item = [&](int it) {
+    Item x;
+    const int e = it / nq;
+    x.h = it - e * nq;
+    x.hk = x.h / g_sz;
+    const int p = qblocks[2 * e], qb = qblocks[2 * e + 1];
+    x.off = offs[p];
+    x.P = offs[p + 1] - x.off;
+    x.q0 = qb * PF_M;
+    x.qrows = min(PF_M, x.P - x.q0);
+    x.nt = (x.q0 + x.qrows - 1) / PF_N + 1;  // KV tiles up to the causal diagonal
+    return x;
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1), mbar_init(&v_full[s], 1), mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 4);
     }
     mbar_init(p_full, 4);
     mbar_init(pv_done, 1);
+    mbar_init(o_free, 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -109,148 +128,163 @@ __global__ void __launch_bounds__(192, 1)
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
     pdl_wait();
-    mbar_expect_tx(q_full, PF_TILE);
-    tma_load_3d(sQ, &tmQ, off + q0, 2 * h, q_full);
-    for (int j = 0; j < nt; ++j) {
-      const int s = j & 1;
-      if (j >= 2) mbar_wait(&k_empty[s], ((j >> 1) - 1) & 1);
-      mbar_expect_tx(&k_full[s], PF_TILE);
-      tma_load_3d(sK + s * PF_TILE, &tmK, off + j * PF_N, 2 * hk, &k_full[s]);
-      if (j >= 2) mbar_wait(&v_empty[s], ((j >> 1) - 1) & 1);
-      mbar_expect_tx(&v_full[s], PF_TILE);
-      tma_load_3d(sV + s * PF_TILE, &tmV, off + j * PF_N, 2 * hk, &v_full[s]);
+    int gt = 0, ni = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ni) {
+      const Item x = item(it);
+      if (ni >= 1) mbar_wait(q_empty, (ni - 1) & 1);  // the previous item's S MMAs are done with Q
+      mbar_expect_tx(q_full, PF_TILE);
+      tma_load_3d(sQ, &tmQ, x.off + x.q0, 2 * x.h, q_full);
+      for (int j = 0; j < x.nt; ++j, ++gt) {
+        const int s = gt & 1;
+        if (gt >= 2) mbar_wait(&k_empty[s], ((gt >> 1) - 1) & 1);
+        mbar_expect_tx(&k_full[s], PF_TILE);
+        tma_load_3d(sK + s * PF_TILE, &tmK, x.off + j * PF_N, 2 * x.hk, &k_full[s]);
+        if (gt >= 2) mbar_wait(&v_empty[s], ((gt >> 1) - 1) & 1);
+        mbar_expect_tx(&v_full[s], PF_TILE);
+        tma_load_3d(sV + s * PF_TILE, &tmV, x.off + j * PF_N, 2 * x.hk, &v_full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer: S_j, then O += P_{j-1} V_{j-1}
-    mbar_wait(q_full, 0);
-    tc_fence_after();
     const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP);
-    for (int j = 0; j <= nt; ++j) {
-      if (j < nt) {
-        const int s = j & 1;
-        mbar_wait(&k_full[s], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&s_empty[s], ((j >> 1) - 1) & 1);  // the softmax has read S_{j-2}
-        tc_fence_after();
-        const uint32_t kb = smem_u32(sK + s * PF_TILE);
+    int gs = 0, gp = 0, ni = 0;  // global S tile, global PV tile, item
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ni) {
+      const Item x = item(it);
+      mbar_wait(q_full, ni & 1);
+      tc_fence_after();
+      for (int j = 0; j <= x.nt; ++j) {
+        if (j < x.nt) {
+          const int s = gs & 1;
+          mbar_wait(&k_full[s], (gs >> 1) & 1);
+          if (gs >= 2) mbar_wait(&s_empty[s], ((gs >> 1) - 1) & 1);  // the softmax has read S two tiles ago
+          tc_fence_after();
+          const uint32_t kb = smem_u32(sK + s * PF_TILE);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // head dims 16 kk .. 16 kk + 15
-          const uint64_t ad = umma_desc_sw128(qa + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
-          const uint64_t bd = umma_desc_sw128(kb + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
-          umma_bf16(tmem + (uint32_t)(s * PF_N), ad, bd, PF_IDESC_QK, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {  // head dims 16 kk .. 16 kk + 15
+            const uint64_t ad = umma_desc_sw128(qa + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
+            const uint64_t bd = umma_desc_sw128(kb + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
+            umma_bf16(tmem + (uint32_t)(s * PF_N), ad, bd, PF_IDESC_QK, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[s]);
+          umma_commit(&k_empty[s]);
+          if (j == x.nt - 1) umma_commit(q_empty);
+          ++gs;
         }
-        umma_commit(&s_full[s]);
-        umma_commit(&k_empty[s]);
-      }
-      if (j >= 1) {
-        const int jj = j - 1, s = jj & 1;
-        mbar_wait(p_full, jj & 1);  // P_jj written, O rescaled
-        mbar_wait(&v_full[s], (jj >> 1) & 1);
-        tc_fence_after();
-        const uint32_t vb = smem_u32(sV + s * PF_TILE);
+        if (j >= 1) {
+          const int s = gp & 1;
+          mbar_wait(p_full, gp & 1);  // P written, O rescaled
+          mbar_wait(&v_full[s], (gp >> 1) & 1);
+          if (j == 1 && ni >= 1) mbar_wait(o_free, (ni - 1) & 1);  // the previous item's O is read out
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sV + s * PF_TILE);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // keys 16 kk .. 16 kk + 15
-          const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
-          const uint64_t bd = umma_desc_sw128_mn(vb + kk * 2048, PF_CHUNK, 1024);
-          umma_bf16(tmem + 256u, ad, bd, PF_IDESC_PV, (jj > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {  // keys 16 kk .. 16 kk + 15
+            const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
+            const uint64_t bd = umma_desc_sw128_mn(vb + kk * 2048, PF_CHUNK, 1024);
+            umma_bf16(tmem + 256u, ad, bd, PF_IDESC_PV, (j > 1 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(pv_done);
+          umma_commit(&v_empty[s]);
+          ++gp;
         }
-        umma_commit(pv_done);
-        umma_commit(&v_empty[s]);
       }
     }
   } else if (warp >= 2) {
     // ---------------- softmax + epilogue: thread = query row = TMEM lane
     const int g = warp & 3;  // TMEM lane quarter this warp may access
     const int row = 32 * g + lane;
-    const int qi = q0 + row;  // query index within the prompt
     const uint32_t lane_off = (uint32_t)(32 * g) << 16;
     const uint32_t o_addr = tmem + 256u + lane_off;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nt; ++j) {
-      const int s = j & 1;
-      mbar_wait(&s_full[s], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t s_addr = tmem + (uint32_t)(s * PF_N) + lane_off;
-      const int kbase = j * PF_N;
-      const bool full_tile = kbase + PF_N - 1 <= q0 && kbase + PF_N <= P;  // no mask needed in this tile
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t r[16];
-        tmem_ld16(s_addr + 16 * c, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int key = kbase + 16 * c + i;
-          const bool ok = full_tile || (key <= qi && key < P);
-          mx = ok ? fmaxf(mx, __uint_as_float(r[i])) : mx;
-        }
-      }
-      const float m_new = fmaxf(m, mx * scale_log2);
-      if (j >= 1) {  // PV_{j-1} done: O is stable and the P buffer free
-        mbar_wait(pv_done, (j - 1) & 1);
+    int gt = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item x = item(it);
+      const int qi = x.q0 + row;  // query index within the prompt
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < x.nt; ++j, ++gt) {
+        const int s = gt & 1;
+        mbar_wait(&s_full[s], (gt >> 1) & 1);
         tc_fence_after();
-      }
-      const float alpha = exp2f(m - m_new);  // m = -inf at j = 0: alpha = 0, l = 0
-      if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
-          uint32_t r[16];
-          tmem_ld16(o_addr + 16 * c, r);
-          tmem_wait_ld();
+        const uint32_t s_addr = tmem + (uint32_t)(s * PF_N) + lane_off;
+        uint32_t r[8][16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st16(o_addr + 16 * c, r);
-        }
-        tmem_wait_st();
-      }
-      l *= alpha;
-      // P = 2^(s * scale - m_new) as fp16, row `row` of the K-major swizzled P tile
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t r[16];
-        tmem_ld16(s_addr + 16 * c, r);
+        for (int c = 0; c < 8; ++c) tmem_ld16(s_addr + 16 * c, r[c]);
         tmem_wait_ld();
-        uint32_t pk[8];
+        const int kbase = j * PF_N;
+        const bool full_tile = kbase + PF_N - 1 <= x.q0 && kbase + PF_N <= x.P;  // no mask in this tile
+        const int kmax = full_tile ? kbase + PF_N - 1 : min(qi, x.P - 1);       // last valid key of the row
+        float mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const int key = kbase + 16 * c + i;
-          const bool ok0 = full_tile || (key <= qi && key < P), ok1 = full_tile || (key + 1 <= qi && key + 1 < P);
-          const float p0 = ok0 ? exp2f(fmaf(__uint_as_float(r[i]), scale_log2, -m_new)) : 0.f;
-          const float p1 = ok1 ? exp2f(fmaf(__uint_as_float(r[i + 1]), scale_log2, -m_new)) : 0.f;
-          const __half2 hp = __floats2half2_rn(p0, p1);
-          l += __low2float(hp) + __high2float(hp);  // the denominator sums what the MMA multiplies
-          pk[i >> 1] = *reinterpret_cast<const uint32_t*>(&hp);
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            mx = (kbase + 16 * c + i <= kmax) ? fmaxf(mx, __uint_as_float(r[c][i])) : mx;
+        const float m_new = fmaxf(m, mx * scale_log2);
+        if (j >= 1) {  // PV of the previous tile done: O is stable and the P buffer free
+          mbar_wait(pv_done, (gt - 1) & 1);
+          tc_fence_after();
         }
-        uint8_t* chunk = sP + (c >> 2) * PF_CHUNK + row * 128;
-        const int u0 = 2 * (c & 3);  // 16-byte units (8 keys) within the 128-byte row
-        *reinterpret_cast<uint4*>(chunk + (((u0) ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(chunk + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-      m = m_new;
-      tc_fence_before();
-      fence_proxy_async_smem();  // P is read by the tensor core (async proxy)
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[s]);
-        mbar_arrive(p_full);
-      }
-    }
-    mbar_wait(pv_done, (nt - 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = out + ((size_t)(off + qi) * nq + h) * 128;
+        const float alpha = exp2f(m - m_new);  // m = -inf at j = 0: alpha = 0, l = 0
+        if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      uint32_t r[16];
-      tmem_ld16(o_addr + 16 * c, r);
-      tmem_wait_ld();
-      uint32_t w[8];
+          for (int c = 0; c < 8; ++c) {
+            uint32_t o[16];
+            tmem_ld16(o_addr + 16 * c, o);
+            tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        w[i] = pack_bf16x2(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
-      if (row < qrows) {
-        *reinterpret_cast<uint4*>(orow + 16 * c) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(orow + 16 * c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(o_addr + 16 * c, o);
+          }
+          tmem_wait_st();
+        }
+        l *= alpha;
+        // P = 2^(s * scale - m_new) as fp16, row `row` of the K-major swizzled P tile
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const int key = kbase + 16 * c + i;
+            const float p0 = key <= kmax ? exp2f(fmaf(__uint_as_float(r[c][i]), scale_log2, -m_new)) : 0.f;
+            const float p1 = key + 1 <= kmax ? exp2f(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, -m_new)) : 0.f;
+            const __half2 hp = __floats2half2_rn(p0, p1);
+            l += __low2float(hp) + __high2float(hp);  // the denominator sums what the MMA multiplies
+            pk[i >> 1] = *reinterpret_cast<const uint32_t*>(&hp);
+          }
+          uint8_t* chunk = sP + (c >> 2) * PF_CHUNK + row * 128;
+          const int u0 = 2 * (c & 3);  // 16-byte units (8 keys) within the 128-byte row
+          *reinterpret_cast<uint4*>(chunk + ((u0 ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(chunk + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        m = m_new;
+        tc_fence_before();
+        fence_proxy_async_smem();  // P is read by the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&s_empty[s]);
+          mbar_arrive(p_full);
+        }
+      }
+      mbar_wait(pv_done, (gt - 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* orow = out + ((size_t)(x.off + qi) * nq + x.h) * 128;
+      uint32_t o[8][16];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tmem_ld16(o_addr + 16 * c, o[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free);  // the next item's first PV may overwrite O
+      if (row < x.qrows) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = pack_bf16x2(__uint_as_float(o[c][2 * i]) * inv, __uint_as_float(o[c][2 * i + 1]) * inv);
+          *reinterpret_cast<uint4*>(orow + 16 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(orow + 16 * c + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
       }
     }
   }
@@ -278,8 +312,16 @@ cudaError_t attn_prefill_tc(const void* q, const void* k, const void* v_f16, con
     set = true;
   }
   const float sl2 = (float)(1.4426950408889634 / std::sqrt(128.0));
-  return launch_pdl(attn_prefill_tc_kernel, dim3(n_qblocks128, nq), dim3(192), (size_t)PF_SMEM, stream, tq, tk, tv,
-                    offs, qblocks128, nq, nkv, sl2, reinterpret_cast<__nv_bfloat16*>(out));
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int n_items = n_qblocks128 * nq;
+  return launch_pdl(attn_prefill_tc_kernel, dim3(n_items < sms ? n_items : sms), dim3(192), (size_t)PF_SMEM, stream,
+                    tq, tk, tv, offs, qblocks128, n_items, nq, nkv, sl2, reinterpret_cast<__nv_bfloat16*>(out));
 }
 
 }  // namespace sgs
