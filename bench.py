@@ -287,6 +287,77 @@ def kernel_roofline(inst, stats, peaks, n_iters, dev_s):
     return roof, kernels
 
 
+def timeline_shares(inst, sgs, tr, cfg, shape, width=32):
+    """Uninstrumented class shares (CUPTI kernel timestamps through torch.profiler:
+    no CUDA events between kernels) over two windows of `width` iterations of one
+    more RL batch -- at 5% of its iterations (the b = B phase) and at 75% (the
+    long tail) -- to set beside the event-sampled shares.  A kernel's share is its
+    critical-path increment (its end minus every earlier end), so the prefill
+    stream's kernels that overlap decode count only where they extend the
+    iteration.  The iteration count comes from the product's scheduler in
+    null-device mode (the same host code)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    dry = sgs.Instance(shape, cfg.max_batch, cfg.prompt_len + cfg.max_out, device=None, n_pages=inst.n_pages,
+                       trace=False)
+    dry.submit_trace(tr)
+    n_it = 0
+    while True:
+        q, a = dry.pending()
+        if q == 0 and a == 0:
+            break
+        dry.step()
+        n_it += 1
+    dry.close()
+    windows = [(int(0.05 * n_it), "b_large"), (int(0.75 * n_it), "tail")]
+    inst.submit_trace(tr)
+    it, out = 0, {}
+    while True:
+        q, a = inst.pending()
+        if q == 0 and a == 0:
+            break
+        w = next((w for w in windows if w[0] == it), None)
+        if not w:
+            inst.step()
+            it += 1
+            continue
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(width):
+                inst.step()
+                it += 1
+            torch.cuda.synchronize()
+        ev = []
+        for e in prof.profiler.kineto_results.events():
+            if e.device_type().name != "CUDA" or e.name().startswith(("Memcpy", "Memset")):
+                continue
+            ev.append((e.start_ns(), e.end_ns(), e.name(), e.device_resource_id()))
+        ev.sort()
+        streams = {}
+        for s0, s1, n, st in ev:
+            if "attn_decode" in n:
+                streams[st] = streams.get(st, 0) + 1
+        dec = max(streams, key=streams.get) if streams else None
+        inc = {}
+        frontier = ev[0][0] if ev else 0
+        for s0, s1, n, st in ev:
+            if "attn_decode" in n:
+                c = "decode_attention"
+            elif "attn_prefill" in n:
+                c = "prefill_attention"
+            elif "gemm_bf16" in n:
+                c = "decode_gemm" if st == dec else "prefill_gemm"
+            else:
+                c = "decode_other" if st == dec else "prefill_other"
+            inc[c] = inc.get(c, 0) + max(0, s1 - max(s0, frontier))
+            frontier = max(frontier, s1)
+        span = (frontier - ev[0][0]) if ev else 1
+        out[w[1]] = {"iterations": [w[0], w[0] + width], "span_ms": round(span / 1e6, 3),
+                     **{c: round(v / span, 4) for c, v in sorted(inc.items())}}
+    return {"what": "CUPTI critical-path shares of one more RL batch of this workload (uninstrumented)",
+            "iterations": n_it, **out}
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -306,6 +377,7 @@ def main():
     ap.add_argument("--strong", action="store_true", help="fixed global batch (cfg.n_prompts) instead of per GPU")
     ap.add_argument("--profile", default=None, help="T(b) profile t0_ns,k0_ps,b_star,k1_ps for Alg. 2")
     ap.add_argument("--hint-noise", type=float, default=None, help="ranker noise sigma (None: oracle hints)")
+    ap.add_argument("--no-timeline", action="store_true", help="skip the CUPTI timeline batch after the timed steps")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -458,6 +530,8 @@ def main():
         "kernels": kernels,
         "clocks": clk.summary(),
     }
+    if not args.no_timeline and world == 1 and kernels is not None:
+        kernels["_timeline"] = timeline_shares(inst, sgs, make_batch(args.warmup + args.steps), cfg, shape)
     if not args.no_cpu_baseline:
         cb = cpu_oracle_sample(shape, cfg)
         line["cpu_baseline"] = {"value": round(1.0 / cb["per_token_s"], 4), "unit": "tokens/s", "cores": cb["cores"],

@@ -69,8 +69,12 @@ enum {
                                 default: without it the host state is bounded by the samples in flight */
   SGS_F_DETERMINISTIC = 32,  /* no split-K in the GEMMs: bitwise run-to-run reproducible results
                                 (split-K's fp32 red.add order is the only variation, R21) */
-  SGS_F_SKIP_PREFILL = 64    /* T(b) profiling only (config 5): admitted prompts are not prefilled (stale
+  SGS_F_SKIP_PREFILL = 64,   /* T(b) profiling only (config 5): admitted prompts are not prefilled (stale
                                 KV, garbage tokens); decode iterations and their timing are unchanged */
+  SGS_F_PREFIX_SHARING = 128 /* NEXT-3 (R26): samples of one sgs_submit batch with
+                                identical prompts (GRPO groups) share the prompt's KV pages; the group's
+                                first admitted member runs the prefill, later members start with one decode
+                                row at position P-1 over the shared pages */
 };
 
 typedef struct {

@@ -69,7 +69,7 @@ def _declare(L):
     L.oracle_bf16_round.argtypes = [ctypes.c_float]
     L.oracle_bf16_round.restype = ctypes.c_float
     L.oracle_sched_sim.argtypes = [ctypes.c_int32, P_i64, P_i32, P_i32, P_i32, P_i32, P_i64, ctypes.c_int32,
-                                   ctypes.c_int32, ctypes.c_int64, P_i64, P_i64]
+                                   ctypes.c_int32, ctypes.c_int64, P_i64, P_i64, P_i64]
     L.oracle_sched_sim.restype = ctypes.c_int64
     L.oracle_sched_blob.argtypes = [ctypes.c_int32, P_i64]
     L.oracle_sched_blob.restype = ctypes.c_int64
@@ -166,8 +166,9 @@ def run_order(d, order, B: int, profile):
 
 # ------------------------------------------------------------------ C2
 def sched_sim(ids, P, d, hint, B: int, page: int, pool_pages: int, batch=None, arrival_after=None,
-              profile=None):
-    """Returns dict(iters=[...], samples={id: {...}}, n_iters, time_ps)."""
+              profile=None, group=None):
+    """Returns dict(iters=[...], samples={id: {...}}, n_iters, time_ps).  group: prefix-sharing group
+    per sample (-1: none; NEXT-3, reading R26)."""
     n = len(ids)
     ids = np.ascontiguousarray(ids, np.int64)
     P = np.ascontiguousarray(P, np.int32)
@@ -177,11 +178,12 @@ def sched_sim(ids, P, d, hint, B: int, page: int, pool_pages: int, batch=None, a
     ar = None if arrival_after is None else np.ascontiguousarray(arrival_after, np.int64)
     tp = np.zeros(2, np.int64)
     prof = None if profile is None else _prof(profile)
+    gr = None if group is None else np.ascontiguousarray(group, np.int64)
     L = lib()
     nit = L.oracle_sched_sim(n, _p(ids, P_i64), _p(P, P_i32), _p(d, P_i32), _p(hint, P_i32),
                              None if bt is None else _p(bt, P_i32), None if ar is None else _p(ar, P_i64),
                              int(B), int(page), int(pool_pages), None if prof is None else _p(prof, P_i64),
-                             _p(tp, P_i64))
+                             _p(tp, P_i64), None if gr is None else _p(gr, P_i64))
     if nit < 0:
         raise RuntimeError(L.oracle_last_error().decode())
     blobs = []

@@ -28,11 +28,13 @@ float oracle_bf16_round(float x) { return bf16_round(x); }
 // oracle_sched_blob.  time_ps128 receives {hi, lo} of sum_t T(b_t).
 int64_t oracle_sched_sim(int32_t n, const int64_t* ids, const int32_t* P, const int32_t* d,
                          const int32_t* hint, const int32_t* batch, const int64_t* arrival_after, int32_t B,
-                         int32_t page, int64_t pool_pages, const int64_t* profile4, int64_t* time_ps128) {
+                         int32_t page, int64_t pool_pages, const int64_t* profile4, int64_t* time_ps128,
+                         const int64_t* group) {
   try {
     std::vector<SimSample> s(n);
     for (int i = 0; i < n; ++i)
-      s[i] = SimSample{ids[i], P[i], d[i], hint[i], batch ? batch[i] : 0, arrival_after ? arrival_after[i] : 0};
+      s[i] = SimSample{ids[i], P[i], d[i], hint[i], batch ? batch[i] : 0, arrival_after ? arrival_after[i] : 0,
+                       group ? group[i] : -1};
     Profile prof{};
     if (profile4) prof = Profile{profile4[0], profile4[1], profile4[2], profile4[3]};
     SimResult r = sched_sim(s, B, page, pool_pages, profile4 ? &prof : nullptr);

@@ -32,6 +32,7 @@ struct SimSample {
   int32_t P, d, hint;
   int32_t batch;          // FIFO batch index (one sgs_submit call)
   int64_t arrival_after;  // queued after this many executed iterations
+  int64_t group = -1;     // NEXT-3 prefix sharing: samples of one group share their (identical) prompt
 };
 struct SimResult {
   std::vector<int64_t> iters;    // per iteration: t,b,sumctx,nadm,ncomp,nalloc,nfree, ids..., pages...

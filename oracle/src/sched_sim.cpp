@@ -14,7 +14,17 @@
 //    (R3); strict order, no backfill.
 //  * Paged KV: prompt pages at admission, one page on each
 //    boundary crossing, lowest free index first (R4).
+//  * Prefix sharing (NEXT-3; "prefix sharing to save key-value cache usage",
+//    P:1005-1007), reading R26: the samples of a group (one prompt, several
+//    samples -- GRPO) share the prompt's pages before the one holding its last
+//    token.  The group's ceil(P/page) prompt pages are allocated (and
+//    reserved) when its first member is admitted and freed (and released)
+//    when its last member completes; a member's block table is the group's
+//    floor((P-1)/page) leading pages followed by private pages: a copy of the
+//    page holding position P-1 and its generation pages, so it reserves
+//    ceil((P+d-1)/page) - floor((P-1)/page).
 #include <algorithm>
+#include <map>
 #include <set>
 #include <stdexcept>
 
@@ -47,6 +57,13 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
 
   std::set<int64_t> free_pages;
   for (int64_t p = 0; p < pool_pages; ++p) free_pages.insert(p);
+  // prefix groups: pages, members not yet completed
+  std::map<int64_t, std::vector<int64_t>> gpages;
+  std::map<int64_t, int> gremain;
+  for (int i = 0; i < n; ++i)
+    if (s[i].group >= 0) ++gremain[s[i].group];
+  auto shared_pages = [&](int i) { return s[i].group >= 0 ? (int64_t)(s[i].P - 1) / page : 0; };
+  auto own_reservation = [&](int i) { return ceil_div((int64_t)s[i].P + s[i].d - 1, page) - shared_pages(i); };
   std::vector<int> slot_of(B, -1);              // slot -> sample index
   std::vector<int> produced(n, 0), slot(n, -1);
   std::vector<int64_t> admit(n, -1), finish(n, -1);
@@ -79,7 +96,8 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
     while (active < B && qhead < (size_t)n) {
       int h = order[qhead];
       if (s[h].arrival_after > horizon) break;
-      int64_t R = ceil_div((int64_t)s[h].P + s[h].d - 1, page);
+      const bool first = s[h].group >= 0 && gpages[s[h].group].empty();
+      int64_t R = own_reservation(h) + (first ? ceil_div(s[h].P, page) : 0);
       if (reserved + R > pool_pages) break;
       int sl = 0;
       while (slot_of[sl] != -1) ++sl;
@@ -91,8 +109,22 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
       ++active;
       ++qhead;
       adm.push_back(s[h].id);
-      int64_t np = ceil_div(s[h].P, page);
-      for (int64_t k = 0; k < np; ++k) alloc_page(h, alloc_log);
+      if (s[h].group >= 0) {
+        auto& gp = gpages[s[h].group];
+        if (first) {  // the group's prompt pages
+          for (int64_t k = 0; k < ceil_div(s[h].P, page); ++k) {
+            if (free_pages.empty()) throw std::runtime_error("oracle: page pool exhausted");
+            gp.push_back(*free_pages.begin());
+            alloc_log.push_back(*free_pages.begin());
+            free_pages.erase(free_pages.begin());
+          }
+        }
+        for (int64_t k = 0; k < shared_pages(h); ++k) pages[h].push_back(gp[k]);  // shared leading pages
+        alloc_page(h, alloc_log);  // private copy of the page holding position P-1
+      } else {
+        int64_t np = ceil_div(s[h].P, page);
+        for (int64_t k = 0; k < np; ++k) alloc_page(h, alloc_log);
+      }
     }
     if (active == 0) throw std::runtime_error("oracle: head sample does not fit the pool");
     // (iii) running samples feed token j at pos P+j-1, ascending slot order
@@ -121,12 +153,20 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
     for (int i : fin) {
       comp.push_back(s[i].id);
       finish[i] = t;
-      for (int64_t p : pages[i]) {
-        free_pages.insert(p);
-        free_log.push_back(p);
+      for (size_t k = (size_t)shared_pages(i); k < pages[i].size(); ++k) {  // private pages
+        free_pages.insert(pages[i][k]);
+        free_log.push_back(pages[i][k]);
+      }
+      reserved -= own_reservation(i);
+      if (s[i].group >= 0 && --gremain[s[i].group] == 0) {  // the group's last member: its prompt pages
+        for (int64_t p : gpages[s[i].group]) {
+          free_pages.insert(p);
+          free_log.push_back(p);
+        }
+        reserved -= ceil_div(s[i].P, page);
+        gpages.erase(s[i].group);
       }
       slot_of[slot[i]] = -1;
-      reserved -= ceil_div((int64_t)s[i].P + s[i].d - 1, page);
       --active;
       ++done;
     }

@@ -446,6 +446,21 @@ sgs_status Engine::submit(const sgs_prompt* prompts, int32_t n, const int32_t* h
                  e_.sample_seed + (uint64_t)batch_counter_};
   dispatch_alg2(dc, n, ids.data(), P.data(), hint, inst.data());
   std::vector<Sample> mine;
+  // NEXT-3: identical prompts of this batch on this instance form a prefix group
+  std::map<std::vector<int32_t>, std::vector<int>> same_prompt;
+  if (e_.flags & SGS_F_PREFIX_SHARING)
+    for (int i = 0; i < n; ++i)
+      if (inst[i] == e_.instance_rank)
+        same_prompt[std::vector<int32_t>(prompts[i].tokens, prompts[i].tokens + P[i])].push_back(i);
+  std::vector<int64_t> group_of(n, -1);
+  {
+    int64_t gi = 0;
+    for (const auto& kv : same_prompt) {
+      if (kv.second.size() >= 2)
+        for (int i : kv.second) group_of[i] = ((int64_t)batch_counter_ << 32) | gi;
+      ++gi;
+    }
+  }
   for (int i = 0; i < n; ++i) {
     if (inst[i] != e_.instance_rank) continue;
     Sample s;
@@ -455,6 +470,7 @@ sgs_status Engine::submit(const sgs_prompt* prompts, int32_t n, const int32_t* h
     s.hint = hint[i];
     s.batch = batch_counter_;
     s.prompt.assign(prompts[i].tokens, prompts[i].tokens + P[i]);
+    s.group = group_of[i];
     live_ids_.insert(s.id);
     mine.push_back(std::move(s));
   }
@@ -627,7 +643,11 @@ cudaError_t Engine::gate_up(const void* W, int T, const PreNorm* pn) {
 sgs_status Engine::run_iteration(const IterPlan& plan) {
   auto& S = sched.samples();
   const int n_adm = (int)plan.admitted.size();
-  const int n_run = (int)plan.running.size();
+  // decode rows: the running samples (ascending slot), then the group members
+  // admitted without a prefill (their first token from position P-1)
+  std::vector<int32_t> drows(plan.running);
+  drows.insert(drows.end(), plan.admitted_decode.begin(), plan.admitted_decode.end());
+  const int n_run = (int)drows.size();
   // the prompt tokens are needed only to stage this iteration's prefill; a
   // completed sample's id may be submitted again (R22)
   struct Release {
@@ -683,6 +703,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   {
     Chunk cur;
     for (int32_t i : plan.admitted) {
+      if (S[i].group >= 0 && !S[i].group_first) continue;  // shared prefix: a decode row instead (R26)
       if (cur.T > 0 && cur.T + S[i].P > e_.max_prefill_tokens) {
         chunks.push_back(cur);
         cur = Chunk();
@@ -727,8 +748,13 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     c.row_base = row_base;
     row_base += (int)c.idx.size();
   }
-  const size_t o_bt = put(plan.bt_deltas.data(), plan.bt_deltas.size());
-  const int n_bt = (int)plan.bt_deltas.size() / 3;
+  std::vector<int32_t> deltas = plan.bt_deltas;
+  for (int32_t i : plan.admitted_decode)  // the member's first decode row re-feeds the prompt's last token
+    deltas.insert(deltas.end(), {S[i].slot, -1, S[i].prompt[S[i].P - 1]});
+  const size_t o_bt = put(deltas.data(), deltas.size());
+  const int n_bt = (int)deltas.size() / 3;
+  const size_t o_cpa = put(plan.copies_after_prefill.data(), plan.copies_after_prefill.size());
+  const size_t o_cpb = put(plan.copies_before_decode.data(), plan.copies_before_decode.size());
   // ---------------- decode rows (ascending slot) -> fixed region at the start of the metadata
   const int Bpad = (e_.max_batch + 15) / 16 * 16;
   const int Bk = (n_run + 15) / 16 * 16;  // CUDA-graph bucket; rows [n_run, Bk) are inert (slot -1)
@@ -737,9 +763,12 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   uint32_t* dsid = reinterpret_cast<uint32_t*>(dtok + Bpad);  // sample id (lo, hi) per row, top-p key
   for (int r = 0; r < Bk; ++r) {
     if (r < n_run) {
-      const Sample& s = S[plan.running[r]];
+      const Sample& s = S[drows[r]];
       const int j = s.produced - 1;  // tokens generated before this iteration (plan already counted this one)
-      dslot[r] = s.slot, dpos[r] = s.P + j - 1, dctx[r] = s.P + j, dtok[r] = j;
+      if (r >= (int)plan.running.size())  // shared-prefix member: position P-1 of its prompt, first token
+        dslot[r] = s.slot, dpos[r] = s.P - 1, dctx[r] = s.P, dtok[r] = 0;
+      else
+        dslot[r] = s.slot, dpos[r] = s.P + j - 1, dctx[r] = s.P + j, dtok[r] = j;
       dsid[2 * r] = (uint32_t)s.id, dsid[2 * r + 1] = (uint32_t)(s.id >> 32);
     } else {
       dslot[r] = -1, dpos[r] = 0, dctx[r] = 1, dtok[r] = 0;
@@ -782,12 +811,21 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
                        cudaMemcpyHostToDevice, st_),
        "meta H2D");
   h2d_bytes += (int64_t)meta.size() * 4 + (n_run > 0 ? (int64_t)dec_used : 0);
-  CK(apply_bt_deltas(bt_, L_.max_pages, MD + o_bt, n_bt, st_), "bt deltas");
+  CK(apply_bt_deltas(bt_, L_.max_pages, MD + o_bt, n_bt, st_, last_tok_), "bt deltas");
   ++launches;
+  const int64_t kv_layer_stride = n_pages_ * (L_.kv_page_bytes / m_.n_layers);
+  auto copy_pages = [&](size_t o, size_t n_pairs) {
+    ++launches;
+    return copy_kv_pages(arena_ + L_.off_kv, kv_layer_stride, L_.kv_page_bytes / m_.n_layers, m_.n_layers, MD + o,
+                         (int)n_pairs, st_);
+  };
 
   // ---------------- prefill: on its own stream and scratch, concurrent with the decode graph
   // (disjoint rows, slots and pages); sequential in timed / graph-less iterations
-  const bool concurrent = !chunks.empty() && n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && !timing_now_;
+  // (a group member decoding from a prefix prefilled in this same iteration
+  // needs that prefill first: no concurrency then)
+  const bool concurrent = !chunks.empty() && n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && !timing_now_ &&
+                          (plan.copies_after_prefill.empty() || plan.admitted_decode.empty());
   if (concurrent) {
     CK(cudaEventRecord(ev_meta_, st_), "event");
     CK(cudaStreamWaitEvent(st_pf_, ev_meta_, 0), "wait meta");
@@ -842,10 +880,14 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     CK(cudaGraphLaunch(g.exec, st_), "graph launch");
     launches += g.kernels;
   }
+  // a group's first member wrote the page holding position P-1 into its own
+  // copy: the group's page gets it (the source of later members' copies)
+  if (!plan.copies_after_prefill.empty()) CK(copy_pages(o_cpa, plan.copies_after_prefill.size() / 2), "kv copy");
   if (concurrent) {
     std::swap(st_, st_pf_);
     CK(cudaEventRecord(ev_pf_, st_pf_), "event");
   }
+  if (!plan.copies_before_decode.empty()) CK(copy_pages(o_cpb, plan.copies_before_decode.size() / 2), "kv copy");
   // ---------------- decode (graph replay per bucket)
   if (n_run > 0) {
     sgs_status s = run_decode(n_run);
@@ -885,7 +927,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     kept_tok_.clear();
     for (auto& c : chunks)
       for (int32_t i : c.idx) kept_ids_.push_back(S[i].id), kept_tok_.push_back(0);
-    for (int32_t i : plan.running) kept_ids_.push_back(S[i].id), kept_tok_.push_back(S[i].produced - 1);
+    for (int32_t i : drows) kept_ids_.push_back(S[i].id), kept_tok_.push_back(S[i].produced - 1);
   }
   CK(cudaEventRecord(ev1_, st_), "event");
   Inflight fl;

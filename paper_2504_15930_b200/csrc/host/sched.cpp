@@ -61,7 +61,12 @@ void Scheduler::init(int max_batch, int page, int64_t n_pages) {
   slot_of_.assign(max_batch, -1);
 }
 
-static inline int64_t reservation(const Sample& s, int page) { return ((int64_t)s.P + s.d - 1 + page - 1) / page; }
+// pages a sample owns: all of its block table, except the leading
+// floor((P-1)/page) prompt pages a prefix group shares (R26)
+static inline int64_t shared_pages(const Sample& s, int page) { return s.group >= 0 ? (int64_t)(s.P - 1) / page : 0; }
+static inline int64_t reservation(const Sample& s, int page) {
+  return ((int64_t)s.P + s.d - 1 + page - 1) / page - shared_pages(s, page);
+}
 
 void Scheduler::submit(std::vector<Sample>&& batch) {
   // drop the consumed queue prefix once it dominates the queue
@@ -72,6 +77,7 @@ void Scheduler::submit(std::vector<Sample>&& batch) {
   std::vector<int32_t> idx;
   idx.reserve(batch.size());
   for (auto& s : batch) {
+    if (s.group >= 0) ++groups_[s.group].remain;
     if (!tracing && !free_idx_.empty()) {
       idx.push_back(free_idx_.back());
       free_idx_.pop_back();
@@ -96,6 +102,9 @@ bool Scheduler::plan(IterPlan* p) {
   p->bt_deltas.clear();
   p->alloc_log.clear();
   p->free_log.clear();
+  p->admitted_decode.clear();
+  p->copies_after_prefill.clear();
+  p->copies_before_decode.clear();
   if (idle()) return false;
   // records of the samples completed by the previous plan are free from now on
   if (!tracing) {
@@ -110,7 +119,8 @@ bool Scheduler::plan(IterPlan* p) {
   while (active_ < B_ && qhead_ < queue_.size()) {
     const int32_t i = queue_[qhead_];
     Sample& s = samples_[i];
-    const int64_t R = reservation(s, page_);
+    const bool first = s.group >= 0 && groups_[s.group].pages.empty();
+    const int64_t R = reservation(s, page_) + (first ? ((int64_t)s.P + page_ - 1) / page_ : 0);
     if (reserved_ + R > pages_.capacity()) break;
     int slot = 0;
     while (slot_of_[slot] >= 0) ++slot;
@@ -121,13 +131,38 @@ bool Scheduler::plan(IterPlan* p) {
     ++active_;
     ++qhead_;
     p->admitted.push_back(i);
-    const int np = (s.P + page_ - 1) / page_;
-    for (int k = 0; k < np; ++k) {
+    auto alloc = [&]() {
       const int64_t pg = pages_.alloc();
       if (pg < 0) throw std::runtime_error("page pool exhausted (reservation invariant broken)");
-      s.pages.push_back((int32_t)pg);
       p->alloc_log.push_back((int32_t)pg);
-      p->bt_deltas.insert(p->bt_deltas.end(), {slot, k, (int32_t)pg});
+      return (int32_t)pg;
+    };
+    if (s.group >= 0) {
+      Group& g = groups_[s.group];
+      if (first)
+        for (int k = 0; k < (s.P + page_ - 1) / page_; ++k) g.pages.push_back(alloc());
+      const int n_sh = (int)shared_pages(s, page_);
+      for (int k = 0; k < n_sh; ++k) {
+        s.pages.push_back(g.pages[k]);
+        p->bt_deltas.insert(p->bt_deltas.end(), {slot, k, g.pages[k]});
+      }
+      const int32_t own = alloc();  // private copy of the page holding position P-1
+      s.pages.push_back(own);
+      p->bt_deltas.insert(p->bt_deltas.end(), {slot, n_sh, own});
+      s.group_first = first;
+      if (first) {
+        p->copies_after_prefill.insert(p->copies_after_prefill.end(), {own, g.pages[n_sh]});
+      } else {
+        p->copies_before_decode.insert(p->copies_before_decode.end(), {g.pages[n_sh], own});
+        p->admitted_decode.push_back(i);
+      }
+    } else {
+      const int np = (s.P + page_ - 1) / page_;
+      for (int k = 0; k < np; ++k) {
+        const int32_t pg = alloc();
+        s.pages.push_back(pg);
+        p->bt_deltas.insert(p->bt_deltas.end(), {slot, k, pg});
+      }
     }
   }
   if (active_ == 0) throw std::runtime_error("queue head can never fit the page pool");
@@ -160,12 +195,23 @@ bool Scheduler::plan(IterPlan* p) {
   for (int32_t i : p->completed) {
     Sample& s = samples_[i];
     s.finish_iter = t_;
-    for (int32_t pg : s.pages) {
-      pages_.free(pg);
-      p->free_log.push_back(pg);
+    for (size_t k = (size_t)shared_pages(s, page_); k < s.pages.size(); ++k) {  // its own pages
+      pages_.free(s.pages[k]);
+      p->free_log.push_back(s.pages[k]);
     }
     slot_of_[s.slot] = -1;
     reserved_ -= reservation(s, page_);
+    if (s.group >= 0) {
+      auto g = groups_.find(s.group);
+      if (--g->second.remain == 0) {  // the group's last member: its prompt pages go back
+        for (int32_t pg : g->second.pages) {
+          pages_.free(pg);
+          p->free_log.push_back(pg);
+        }
+        reserved_ -= ((int64_t)s.P + page_ - 1) / page_;
+        groups_.erase(g);
+      }
+    }
     --active_;
     if (!tracing) retire_.push_back(i);
   }

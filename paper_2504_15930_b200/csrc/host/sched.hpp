@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace sgs {
@@ -30,6 +31,8 @@ struct Sample {
   int32_t P, d, hint;
   int32_t batch;
   std::vector<int32_t> prompt;  // prompt tokens; released once the prefill metadata is staged
+  int64_t group = -1;           // NEXT-3 prefix-sharing group (identical prompts of one batch), -1: none
+  bool group_first = false;     // the group's first admitted member (runs the group's prefill)
   // runtime
   int32_t slot = -1;
   int32_t produced = 0;
@@ -44,6 +47,13 @@ struct IterPlan {
   std::vector<int32_t> completed;        // sample indices, ascending id
   std::vector<int32_t> bt_deltas;        // (slot, page_idx, page) triples in allocation order
   std::vector<int32_t> alloc_log, free_log;
+  // prefix sharing (R26): admitted non-first group members, which produce their
+  // first token as a decode row at position P-1 (their prompt KV is shared);
+  // page copies (src, dst): a first member's private copy of the page holding
+  // P-1 -> the group's page after the prefill, the group's page -> a later
+  // member's private copy before the decode program
+  std::vector<int32_t> admitted_decode;
+  std::vector<int32_t> copies_after_prefill, copies_before_decode;
   int64_t sumctx = 0;
   int32_t b = 0;
 };
@@ -81,6 +91,11 @@ class Scheduler {
   size_t qhead_ = 0;
   std::vector<int32_t> slot_of_;  // slot -> sample index or -1
   std::vector<int32_t> free_idx_, retire_;  // recyclable sample records (tracing off)
+  struct Group {
+    std::vector<int32_t> pages;  // the prompt's ceil(P/page) pages (allocated at the first admission)
+    int remain = 0;              // members not yet completed
+  };
+  std::unordered_map<int64_t, Group> groups_;
   int64_t reserved_ = 0;
   int32_t active_ = 0;
   int64_t t_ = 0;

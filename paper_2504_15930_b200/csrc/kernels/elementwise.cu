@@ -590,14 +590,40 @@ cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_de
 }
 
 // ------------------------------------------------------------------ block-table deltas
-__global__ void bt_delta_kernel(int32_t* bt, int max_pages, const int32_t* __restrict__ d, int n) {
+// (slot, index, value) triples: index >= 0 sets block-table entry bt[slot][index];
+// index -1 sets the slot's next input token (prefix sharing: a group member's
+// first decode row re-feeds the prompt's last token, R26)
+__global__ void bt_delta_kernel(int32_t* bt, int max_pages, const int32_t* __restrict__ d, int n,
+                                int32_t* last_tok) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) bt[(size_t)d[3 * i] * max_pages + d[3 * i + 1]] = d[3 * i + 2];
+  if (i >= n) return;
+  if (d[3 * i + 1] >= 0)
+    bt[(size_t)d[3 * i] * max_pages + d[3 * i + 1]] = d[3 * i + 2];
+  else if (last_tok)
+    last_tok[d[3 * i]] = d[3 * i + 2];
 }
 
-cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream) {
+cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream,
+                            int32_t* last_tok) {
   if (n <= 0) return cudaSuccess;
-  bt_delta_kernel<<<(n + 255) / 256, 256, 0, stream>>>(block_table, max_pages, deltas, n);
+  bt_delta_kernel<<<(n + 255) / 256, 256, 0, stream>>>(block_table, max_pages, deltas, n, last_tok);
+  return cudaGetLastError();
+}
+
+// KV page copies (src, dst) in every layer's pool (prefix sharing, R26)
+__global__ void copy_kv_pages_kernel(uint8_t* __restrict__ pool, int64_t layer_stride, int64_t page_bytes,
+                                     const int32_t* __restrict__ pairs) {
+  const int k = blockIdx.x, l = blockIdx.y;
+  const uint4* src = reinterpret_cast<const uint4*>(pool + l * layer_stride + (int64_t)pairs[2 * k] * page_bytes);
+  uint4* dst = reinterpret_cast<uint4*>(pool + l * layer_stride + (int64_t)pairs[2 * k + 1] * page_bytes);
+  for (int64_t i = threadIdx.x; i < page_bytes / 16; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t copy_kv_pages(void* pool, int64_t layer_stride, int64_t page_bytes, int n_layers, const int32_t* pairs,
+                          int n_pairs, cudaStream_t stream) {
+  if (n_pairs <= 0) return cudaSuccess;
+  copy_kv_pages_kernel<<<dim3(n_pairs, n_layers), 256, 0, stream>>>(reinterpret_cast<uint8_t*>(pool), layer_stride,
+                                                                    page_bytes, pairs);
   return cudaGetLastError();
 }
 

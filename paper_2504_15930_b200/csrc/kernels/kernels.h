@@ -122,6 +122,9 @@ cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, i
                       int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
 cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream,
                           int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
-cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream);
+cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream,
+                            int32_t* last_tok = nullptr);
+cudaError_t copy_kv_pages(void* pool, int64_t layer_stride, int64_t page_bytes, int n_layers, const int32_t* pairs,
+                          int n_pairs, cudaStream_t stream);
 
 }  // namespace sgs

@@ -23,6 +23,7 @@ F_SHADOW_WEIGHTS = 8
 F_TRACE = 16
 F_DETERMINISTIC = 32
 F_SKIP_PREFILL = 64
+F_PREFIX_SHARING = 128
 
 # every symbol include/sgs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [

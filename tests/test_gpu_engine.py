@@ -440,3 +440,31 @@ def test_c2_scale_pipelined_engine(sgs):
         inst.close()
         del inst
     assert runs[0] == runs[1]
+
+
+# ------------------------------------------------------------------ NEXT-3 prefix sharing
+@pytest.mark.parametrize("model,G,P", [("tiny", 4, 40), ("tiny", 3, 32), ("qwen2.5-7b", 4, 40)])
+def test_prefix_sharing_end_to_end(sgs, model, G, P):
+    # P:1005-1007 "prefix sharing to save key-value cache usage" (reading R26):
+    # GRPO groups of G samples per prompt; the schedule (with the group page
+    # rule) is bit-exact against the oracle, and every member's teacher-forced
+    # logits -- the first member's from the prefill, the others' first token from
+    # a decode row at position P-1 over the shared pages -- match the oracle
+    # decoder on its own prompt + tokens
+    shape = workload.MODELS[model]
+    n = 24 if model == "tiny" else 8
+    tr = workload.make_trace(n, P, 12, 0.8, 40 if model == "tiny" else 12, shape.vocab, seed=G * 100 + P,
+                             group_size=G)
+    B, pool = (6, 200) if model == "tiny" else (4, 64)
+    inst = sgs.Instance(shape, B, P + 64, device=0, n_pages=pool, weight_seed=31,
+                        flags=sgs.sgs.F_KEEP_LOGITS | sgs.sgs.F_PREFIX_SHARING)
+    comps, rows = _run_collect(inst, tr)
+    group = np.arange(n) // G
+    o = oracle.sched_sim(tr.ids, tr.prompt_len, tr.forced_len, tr.hint, B, 16, pool, group=group)
+    assert np.array_equal(inst.trace(0), o["iter_blob"])
+    assert np.array_equal(inst.trace(1), o["sample_blob"])
+    check = tr.ids.tolist() if model == "tiny" else tr.ids[:G].tolist()  # 7B: one whole group
+    tol = 2e-2 if model == "tiny" else TOL_7B_28L
+    worst = _check_teacher_forced(shape, 31, tr, comps, rows, check, tol=tol)
+    print(model, "prefix sharing worst teacher-forced max-abs", worst)
+    inst.close()

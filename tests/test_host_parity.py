@@ -294,3 +294,24 @@ def test_set_instances_between_batches():
     tr2 = workload.make_trace(40, 8, 20, 1.0, 100, shape.vocab, seed=5, id_base=1000)
     exp, _ = dispatch_plan(tr2.ids, tr2.prompt_len, tr2.hint, 2, 8, 16, 400, PROF)
     assert inst.submit_trace(tr2) == int((exp == 1).sum())
+
+
+@pytest.mark.parametrize("G,P,jitter", [(4, 40, 0), (8, 64, 0), (3, 20, 15), (2, 16, 0)])
+def test_prefix_sharing_schedule_matches_oracle(G, P, jitter):
+    # NEXT-3 (R26): with SGS_F_PREFIX_SHARING the product's schedule,
+    # page lists and page log equal the oracle's with the groups the workload
+    # implies (identical prompts of one batch); without the flag, the unshared one
+    from paper_2504_15930_b200 import sgs as binding
+    shape = workload.MODELS["tiny"]
+    tr = workload.make_trace(96, P, 30, 1.0, 200, shape.vocab, seed=G * 7 + P, group_size=G,
+                             prompt_len_jitter=jitter)
+    group = np.arange(len(tr)) // G
+    for B, pool in ((8, 4000), (16, 120)):
+        inst = Instance(shape, B, 40000, device=None, n_pages=pool, profile=PROF, flags=binding.F_PREFIX_SHARING)
+        inst.submit_trace(tr)
+        inst.run()
+        o = oracle.sched_sim(tr.ids, tr.prompt_len, tr.forced_len, tr.hint, B, 16, pool, group=group)
+        assert_same(inst, o)
+        if P >= 32:  # shared pages exist only before the page holding position P-1
+            u = oracle.sched_sim(tr.ids, tr.prompt_len, tr.forced_len, tr.hint, B, 16, pool)
+            assert sum(len(it["alloc"]) for it in o["iters"]) < sum(len(it["alloc"]) for it in u["iters"])

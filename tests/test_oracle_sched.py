@@ -405,3 +405,44 @@ def test_elastic_delta_prime_is_simulated_makespan_difference():
                                                   profile=prof)["time_ps"])
             assert r["t_gen_ps"][k] == mk
         assert r["delta_prime_ps"] == r["t_gen_ps"][0] - r["t_gen_ps"][1]
+
+
+@pytest.mark.parametrize("name", ["sched_prefix_sharing.json", "sched_prefix_sharing_full_page.json"])
+def test_sched_prefix_sharing_golden(name):
+    # tests/golden/sched_prefix_sharing*.json: NEXT-3 (reading R26) by hand
+    g = json.load(open(os.path.join(GOLD, name)))
+    s = np.array(g["samples"])
+    r = oracle.sched_sim(s[:, 0], s[:, 1], s[:, 2], s[:, 3], g["B"], g["page"], g["pool"], group=s[:, 4])
+    assert r["iters"] == g["iters"]
+    assert {str(k): v for k, v in r["samples"].items()} == g["per_sample"]
+
+
+def test_sched_prefix_sharing_invariants_and_savings():
+    # random GRPO-style batches: G samples per prompt; conservation, no page owned twice except
+    # the shared full prompt pages (held by every active member of a group), fewer page-iterations
+    # than without sharing
+    rng = np.random.default_rng(8)
+    for trial in range(40):
+        n_prompts, G = int(rng.integers(2, 12)), int(rng.integers(1, 6))
+        P = np.repeat(rng.integers(1, 70, n_prompts), G)
+        n = len(P)
+        d = rng.integers(1, 60, n)
+        ids = rng.permutation(10_000)[:n]
+        group = np.repeat(np.arange(n_prompts), G)
+        B, page, pool = int(rng.integers(1, 9)), 16, 400
+        r = oracle.sched_sim(ids, P, d, d, B, page, pool, group=group)
+        u = oracle.sched_sim(ids, P, d, d, B, page, pool)
+        held, alive = {}, set()
+        for it in r["iters"]:
+            for p in it["alloc"]:
+                assert p not in held and 0 <= p < pool
+                held[p] = True
+            for p in it["freed"]:
+                del held[p]
+        assert not held
+        for i, rec in r["samples"].items():
+            k = int(np.flatnonzero(ids == i)[0])
+            assert len(rec["pages"]) == -(-(int(P[k]) + int(d[k]) - 1) // page)
+            assert rec["finish"] - rec["admit"] + 1 == d[k]
+        # pages allocated in total never exceed the unshared run's
+        assert sum(len(it["alloc"]) for it in r["iters"]) <= sum(len(it["alloc"]) for it in u["iters"]) + n_prompts

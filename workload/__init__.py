@@ -170,17 +170,21 @@ class Trace:
 
 def make_trace(n: int, prompt_len: int, median_out: int, sigma: float, max_out: int, vocab: int,
                seed: int = 1234, hint_noise: float | None = None, id_base: int = 0,
-               prompt_len_jitter: int = 0) -> Trace:
+               prompt_len_jitter: int = 0, group_size: int = 1) -> Trace:
+    """group_size G > 1: GRPO-style groups -- samples i and j with i // G == j // G get the same
+    prompt (length and tokens), each with its own forced output length (NEXT-3 workloads)."""
     ids = np.arange(id_base, id_base + n, dtype=np.int64)
     forced = lognormal_lengths(n, median_out, sigma, max_out, seed)
+    n_p = (n + group_size - 1) // group_size
     if prompt_len_jitter:
         rng = np.random.Generator(np.random.PCG64(seed + 7))
-        plen = np.clip(prompt_len + rng.integers(-prompt_len_jitter, prompt_len_jitter + 1, size=n), 1, None)
+        plen = np.clip(prompt_len + rng.integers(-prompt_len_jitter, prompt_len_jitter + 1, size=n_p), 1, None)
     else:
-        plen = np.full(n, prompt_len, dtype=np.int64)
-    plen = plen.astype(np.int64)
+        plen = np.full(n_p, prompt_len, dtype=np.int64)
+    plen = np.repeat(plen.astype(np.int64), group_size)[:n]
     hint = forced.copy() if hint_noise is None else noisy_hints(forced, hint_noise, seed)
-    toks, offs = prompt_tokens(seed, ids, plen, vocab)
+    prompt_id = ids if group_size == 1 else id_base + np.arange(n, dtype=np.int64) // group_size
+    toks, offs = prompt_tokens(seed, prompt_id, plen, vocab)
     return Trace(ids, plen, forced, hint, toks, offs)
 
 
