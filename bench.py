@@ -378,6 +378,8 @@ def main():
     ap.add_argument("--profile", default=None, help="T(b) profile t0_ns,k0_ps,b_star,k1_ps for Alg. 2")
     ap.add_argument("--hint-noise", type=float, default=None, help="ranker noise sigma (None: oracle hints)")
     ap.add_argument("--no-timeline", action="store_true", help="skip the CUPTI timeline batch after the timed steps")
+    ap.add_argument("--group-size", type=int, default=1, help="GRPO-style groups: samples per prompt (NEXT-3)")
+    ap.add_argument("--prefix-sharing", action="store_true", help="SGS_F_PREFIX_SHARING (NEXT-3, reading R26)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -407,7 +409,8 @@ def main():
     inst = sgs.Instance(shape, cfg.max_batch, max_ctx, device=local, n_instances=world, instance_rank=rank,
                         weight_seed=cfg.seed,
                         flags=(0 if args.no_kernel_timing else sgs.sgs.F_KERNEL_TIMING) |
-                        (sgs.sgs.F_SHADOW_WEIGHTS if args.weight_sync == "async" else 0),
+                        (sgs.sgs.F_SHADOW_WEIGHTS if args.weight_sync == "async" else 0) |
+                        (sgs.sgs.F_PREFIX_SHARING if args.prefix_sharing else 0),
                         dispatch=args.dispatch, profile=prof, sample_seed=cfg.seed, trace=False)
     peaks0 = load_peaks()
     inst.set_roofline(peaks0["hbm_gbs"], peaks0["bf16_tflops_sustained"])
@@ -419,7 +422,8 @@ def main():
     def make_batch(step):
         # a fresh RL batch per step: same length distribution, new ids and prompts
         return workload.make_trace(n_total, cfg.prompt_len, cfg.median_out, cfg.sigma, cfg.max_out, shape.vocab,
-                                   seed=cfg.seed + 1000 * step, id_base=step * 1_000_000, hint_noise=args.hint_noise)
+                                   seed=cfg.seed + 1000 * step, id_base=step * 1_000_000, hint_noise=args.hint_noise,
+                                   group_size=args.group_size)
 
     stream = inst.stream
 
@@ -520,7 +524,8 @@ def main():
                    "dispatch": args.dispatch, "weight_sync": args.weight_sync,
                    "hints": "oracle (= forced)" if args.hint_noise is None else
                    f"noisy sigma {args.hint_noise}", "profile": list(prof) if prof else None,
-                   "l2": "inputs larger than L2 (weights 15 GB, KV pool > 100 GB)"},
+                   "l2": "inputs larger than L2 (weights 15 GB, KV pool > 100 GB)",
+                   "group_size": args.group_size, "prefix_sharing": args.prefix_sharing},
         "e2e": {"value": round(tokens / wall_s, 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(statistics.mean(r["h2d"] for r in results)),
                 "d2h_bytes_per_step": int(statistics.mean(r["d2h"] for r in results))},
