@@ -99,6 +99,15 @@ typedef struct {
   uint64_t sample_seed;      /* Philox key for top-p */
   uint64_t weight_seed;      /* hash-init seed when sgs_init gets no weights */
   int32_t flags;             /* SGS_F_* */
+  /* NEXT-2 tensor parallelism: this handle is shard
+   * tp_rank of a tp_size-GPU instance (0 or 1 = no TP).  q/kv heads, FFN
+   * columns and vocabulary rows are split tp_size ways (they must divide);
+   * the O / down projections and the LM head's argmax are combined with
+   * NCCL all-reduces over the communicator of sgs_tp_comm_init.  Every shard
+   * runs the same scheduler on the same submissions.  TP shards generate
+   * their weights from weight_seed (sgs_init's weights must be NULL), decode
+   * greedily, and have no debug hooks or weight sync. */
+  int32_t tp_size, tp_rank;
 } sgs_engine_cfg;
 
 /* One prompt (host memory, copied by sgs_submit). */
@@ -205,6 +214,10 @@ sgs_status sgs_host_state(const sgs_handle* h, int64_t* records, int64_t* queue_
  * sample in flight (SGS_E_STATE otherwise). */
 sgs_status sgs_comm_unique_id(uint8_t out[128]);
 sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int32_t world);
+/* NEXT-2: the tensor-parallel communicator of a tp_size > 1 handle (unique id
+ * from sgs_comm_unique_id on shard 0, shared by the caller); must precede the
+ * first sgs_step. */
+sgs_status sgs_tp_comm_init(sgs_handle* h, const uint8_t id[128]);
 sgs_status sgs_update_weights(sgs_handle* h, const sgs_weights* src, int32_t root);
 /* Trainer proxy: regenerate this handle's weights from a new seed on device
  * (the root does this before sgs_update_weights). */

@@ -102,6 +102,11 @@ sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int
   return h->eng.comm_init(id, rank, world);
 }
 
+sgs_status sgs_tp_comm_init(sgs_handle* h, const uint8_t id[128]) {
+  if (!h || !id) return SGS_E_INVAL;
+  return h->eng.tp_comm_init(id);
+}
+
 sgs_status sgs_update_weights(sgs_handle* h, const sgs_weights* src, int32_t root) {
   if (!h) return SGS_E_INVAL;
   return h->eng.update_weights(src, root);

@@ -28,8 +28,18 @@ namespace sgs {
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64_t n_pages, ArenaLayout* L) {
+// NEXT-2: the dims of tensor-parallel shard (q/kv heads, FFN, vocab rows / tp)
+static sgs_model_cfg tp_local(const sgs_model_cfg& m, const sgs_engine_cfg& e) {
+  const int tp = e.tp_size > 1 ? e.tp_size : 1;
+  sgs_model_cfg l = m;
+  l.n_q_heads /= tp, l.n_kv_heads /= tp, l.d_ffn /= tp, l.vocab /= tp;
+  return l;
+}
+
+sgs_status Engine::layout(const sgs_model_cfg& m_full, const sgs_engine_cfg& e, int64_t n_pages, ArenaLayout* L) {
+  const sgs_model_cfg m = tp_local(m_full, e);
   const int64_t d = m.d_model, hd = m.head_dim, nq = m.n_q_heads, nkv = m.n_kv_heads, f = m.d_ffn, V = m.vocab;
+  const int64_t V_full = m_full.vocab;
   const int64_t B = e.max_batch;
   const int64_t pf = e.max_prefill_tokens > 0 ? e.max_prefill_tokens : 16384;
   const int64_t tmax = std::max<int64_t>(pf, B);
@@ -43,7 +53,7 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   };
   // weights (contiguous so the weight sync can broadcast one range)
   const int64_t per_layer = ((nq + 2 * nkv) * hd * d + (nq + 2 * nkv) * hd + d * nq * hd + 2 * f * d + d * f + 2 * d);
-  const int64_t wbytes = (m.n_layers * per_layer + 2 * V * d + d) * 2;
+  const int64_t wbytes = (m.n_layers * per_layer + (V + V_full) * d + d) * 2;
   take(wbytes + 256 * (8 * m.n_layers + 8));
   L->weights_bytes = o;
   L->kv_page_bytes = m.n_layers * nkv * 2 * page * hd * 2;
@@ -92,7 +102,7 @@ sgs_status Engine::layout(const sgs_model_cfg& m, const sgs_engine_cfg& e, int64
   L->attn_bytes = max_items * (nq / nkv) * (hd + 2) * 4 + max_items * 4;  // partials + arrival counters
   L->off_attn = take(L->attn_bytes);
   L->off_cksum = take(64);
-  L->off_amax = take(((B + 15) / 16 * 16) * 8 + 64);
+  L->off_amax = take(((B + 15) / 16 * 16) * 8 + 64 + B * 8);
   L->off_nbar = take((2 * m.n_layers + 1) * 2 * 4 + 64);
   L->scratch_bytes = o - s0;
   L->off_shadow = (e.flags & SGS_F_SHADOW_WEIGHTS) ? take(L->weights_bytes) : -1;
@@ -147,30 +157,53 @@ Engine::~Engine() {
 void Engine::build_tensor_table() {
   tensors_.clear();
   const int64_t d = m_.d_model, hd = m_.head_dim, nq = m_.n_q_heads, nkv = m_.n_kv_heads, f = m_.d_ffn;
-  tensors_.push_back({0, embed_, (int64_t)m_.vocab * d, 0});
-  tensors_.push_back({1, lm_head_, (int64_t)m_.vocab * d, 0});
+  const int64_t r = tp_rank_, tp = tp_;
+  // shard windows of the full tensors (identity without TP): rows for the
+  // column-parallel QKV / gate / up / LM head, columns for the row-parallel O / down
+  auto rows_win = [&](int64_t row0, int64_t cols) { return tp > 1 ? ShardMap{cols, row0, 0, cols} : ShardMap{}; };
+  auto cols_win = [&](int64_t src_cols, int64_t col0, int64_t lcols) {
+    return tp > 1 ? ShardMap{src_cols, 0, col0, lcols} : ShardMap{};
+  };
+  tensors_.push_back({0, embed_, vocab_full_ * d, 0});
+  tensors_.push_back({1, lm_head_, (int64_t)m_.vocab * d, 0, 1, 0, 0, 0, rows_win(r * m_.vocab, d)});
   tensors_.push_back({2, nf_, d, 1});
   for (int l = 0; l < m_.n_layers; ++l) {
     const int64_t b = 16 + 16 * (int64_t)l;
     auto* L = &layers_[l];
     auto at = [](void* p, int64_t elems) { return (void*)((uint16_t*)p + elems); };
-    tensors_.push_back({b + 0, L->wqkv, nq * hd * d, 0});
-    tensors_.push_back({b + 1, at(L->wqkv, nq * hd * d), nkv * hd * d, 0});
-    tensors_.push_back({b + 2, at(L->wqkv, (nq + nkv) * hd * d), nkv * hd * d, 0});
-    tensors_.push_back({b + 3, L->bqkv, nq * hd, 0});
-    tensors_.push_back({b + 4, at(L->bqkv, nq * hd), nkv * hd, 0});
-    tensors_.push_back({b + 5, at(L->bqkv, (nq + nkv) * hd), nkv * hd, 0});
-    tensors_.push_back({b + 6, L->wo, d * nq * hd, 0});
+    tensors_.push_back({b + 0, L->wqkv, nq * hd * d, 0, 1, 0, 0, 0, rows_win(r * nq * hd, d)});
+    tensors_.push_back({b + 1, at(L->wqkv, nq * hd * d), nkv * hd * d, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, d)});
+    tensors_.push_back(
+        {b + 2, at(L->wqkv, (nq + nkv) * hd * d), nkv * hd * d, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, d)});
+    tensors_.push_back({b + 3, L->bqkv, nq * hd, 0, 1, 0, 0, 0, rows_win(r * nq * hd, 1)});
+    tensors_.push_back({b + 4, at(L->bqkv, nq * hd), nkv * hd, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, 1)});
+    tensors_.push_back({b + 5, at(L->bqkv, (nq + nkv) * hd), nkv * hd, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, 1)});
+    tensors_.push_back({b + 6, L->wo, d * nq * hd, 0, 1, 0, 0, 0, cols_win(nq * hd * tp, r * nq * hd, nq * hd)});
     // gate and up interleave in 64-row blocks: tile i of the fused matrix = 64 gate rows + 64 up rows
-    tensors_.push_back({b + 7, L->wgu, f * d, 0, d, 64, 128, 0});
-    tensors_.push_back({b + 8, L->wgu, f * d, 0, d, 64, 128, 64});
-    tensors_.push_back({b + 9, L->wd, d * f, 0});
+    tensors_.push_back({b + 7, L->wgu, f * d, 0, d, 64, 128, 0, rows_win(r * f, d)});
+    tensors_.push_back({b + 8, L->wgu, f * d, 0, d, 64, 128, 64, rows_win(r * f, d)});
+    tensors_.push_back({b + 9, L->wd, d * f, 0, 1, 0, 0, 0, cols_win(f * tp, r * f, f)});
     tensors_.push_back({b + 10, L->n1, d, 1});
     tensors_.push_back({b + 11, L->n2, d, 1});
   }
 }
 
-sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const sgs_weights* w) {
+sgs_status Engine::init(const sgs_model_cfg& m_full, const sgs_engine_cfg& e, const sgs_weights* w) {
+  tp_ = e.tp_size > 1 ? e.tp_size : 1;
+  tp_rank_ = tp_ > 1 ? e.tp_rank : 0;
+  vocab_full_ = m_full.vocab;
+  if (tp_ > 1) {
+    if (e.tp_rank < 0 || e.tp_rank >= tp_ || m_full.n_q_heads % tp_ || m_full.n_kv_heads % tp_ ||
+        m_full.d_ffn % tp_ || m_full.vocab % tp_) {
+      err = "tensor parallelism: tp_rank out of range or heads / FFN / vocab not divisible by tp_size";
+      return SGS_E_INVAL;
+    }
+    if (w || e.sampling != SGS_SAMPLE_GREEDY || e.device < 0) {
+      err = "tensor-parallel shards generate their weights (weights == NULL), decode greedily, need a device";
+      return SGS_E_UNSUPPORTED;
+    }
+  }
+  const sgs_model_cfg m = tp_local(m_full, e);
   m_ = m;
   e_ = e;
   if (e_.max_prefill_tokens <= 0) e_.max_prefill_tokens = 16384;
@@ -227,7 +260,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
       o = align_up(o + elems * 2, 256);
       return p;
     };
-    embed_ = w((int64_t)m.vocab * d);
+    embed_ = w(vocab_full_ * d);
     lm_head_ = w((int64_t)m.vocab * d);
     nf_ = w(d);
     layers_.resize(m.n_layers);
@@ -268,6 +301,7 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   attn_ws_ = arena_ + L_.off_attn;
   cksum_dev_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_cksum);
   amax_keys_ = reinterpret_cast<unsigned long long*>(arena_ + L_.off_amax);
+  amax_keys_pf_ = amax_keys_ + ((e.max_batch + 15) / 16 * 16) + 8;
   norm_bar_ = reinterpret_cast<unsigned int*>(arena_ + L_.off_nbar);
   // PreNorm is off by default: measured slower than the rmsnorm kernel + PDL
   // (profiles/README.md r02: the norm and the grid barrier stay on the
@@ -303,7 +337,8 @@ sgs_status Engine::init(const sgs_model_cfg& m, const sgs_engine_cfg& e, const s
   CK(cudaEventCreateWithFlags(&ev_meta_, cudaEventDisableTiming), "event");
   CK(cudaEventCreateWithFlags(&ev_pf_, cudaEventDisableTiming), "event");
   CK(cudaMemsetAsync(attn_ws_, 0, L_.attn_bytes, st_), "memset attention workspace");
-  CK(cudaMemsetAsync(amax_keys_, 0, ((e.max_batch + 15) / 16 * 16) * 8 + 64, st_), "memset argmax keys");
+  CK(cudaMemsetAsync(amax_keys_, 0, ((e.max_batch + 15) / 16 * 16) * 8 + 64 + e.max_batch * 8, st_),
+     "memset argmax keys");
   CK(cudaMemsetAsync(norm_bar_, 0, (2 * m.n_layers + 1) * 2 * 4 + 64, st_), "memset norm barriers");
   // RoPE table: cos/sin of pos * theta^(-2i/hd) computed in fp64 on the host, stored fp32
   {
@@ -365,7 +400,8 @@ sgs_status Engine::set_instances(int32_t n_instances, int32_t instance_rank) {
 sgs_status Engine::load_weights_seed(uint64_t seed) {
   if (null_) return SGS_OK;
   for (const auto& t : tensors_) {
-    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_, t.cols, t.blk, t.stride, t.off), "hash_init");
+    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_, t.cols, t.blk, t.stride, t.off, t.shard),
+       "hash_init");
     ++launches;
   }
   CK(cudaStreamSynchronize(st_), "hash_init sync");
@@ -411,7 +447,7 @@ sgs_status Engine::submit(const sgs_prompt* prompts, int32_t n, const int32_t* h
       return SGS_E_INVAL;
     }
     for (int j = 0; j < p.len; ++j)
-      if (p.tokens[j] < 0 || p.tokens[j] >= m_.vocab) {
+      if (p.tokens[j] < 0 || p.tokens[j] >= vocab_full_) {
         err = "token id out of range";
         return SGS_E_INVAL;
       }
@@ -485,6 +521,10 @@ sgs_status Engine::step(sgs_completion* out, int32_t cap, int32_t* n_out) {
   *n_out = 0;
   if (poisoned) {
     err = "handle poisoned by an earlier error";
+    return SGS_E_STATE;
+  }
+  if (tp_ > 1 && !tp_comm_) {
+    err = "tensor-parallel handle without sgs_tp_comm_init";
     return SGS_E_STATE;
   }
   handed_.clear();
@@ -824,7 +864,7 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
   // (disjoint rows, slots and pages); sequential in timed / graph-less iterations
   // (a group member decoding from a prefix prefilled in this same iteration
   // needs that prefill first: no concurrency then)
-  const bool concurrent = !chunks.empty() && n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && !timing_now_ &&
+  const bool concurrent = !chunks.empty() && n_run > 0 && !(e_.flags & SGS_F_NO_GRAPHS) && !timing_now_ && tp_ == 1 &&
                           (plan.copies_after_prefill.empty() || plan.admitted_decode.empty());
   if (concurrent) {
     CK(cudaEventRecord(ev_meta_, st_), "event");
@@ -1041,11 +1081,17 @@ sgs_status Engine::decode_body(int Bk) {
                      L_.max_pages, ao_, 0, part_o, part_ml, arrive, st_),
          "attn_decode");
     ktoc(&kr, -1.0, 0.0, 0.0, 0);
+    // TP: every shard adds its partial O projection; shard 0 keeps h, the others
+    // start from 0, and the all-reduce (sum) leaves h + sum of partials on all
+    if (tp_ > 1 && tp_rank_ != 0) CK(cudaMemsetAsync(h_, 0, (size_t)Bk * d * 4, st_), "tp zero h");
     if (on(4)) CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
+    if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)Bk * d), "tp allreduce o");
     if (!fuse) ktic(&ko, 5);
     if (on(0) && !fuse) CK(other(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm2");
     if (on(5)) CK(gate_up(Ly.wgu, Bk, fuse ? &pn2 : nullptr), "gemm gate_up + SwiGLU");
+    if (tp_ > 1 && tp_rank_ != 0) CK(cudaMemsetAsync(h_, 0, (size_t)Bk * d * 4, st_), "tp zero h");
     if (on(6)) CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
+    if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)Bk * d), "tp allreduce down");
     launches += fuse ? 2 : 4;  // (rmsnorm x2,) RoPE, attention; the GEMMs count themselves
   }
   const PreNorm pnf = pnorm(nf_, 2 * m_.n_layers);
@@ -1059,7 +1105,7 @@ sgs_status Engine::decode_body(int Bk) {
     const bool keep = (e_.flags & SGS_F_KEEP_LOGITS) != 0;
     const int Bpad = (e_.max_batch + 15) / 16 * 16;
     ArgmaxArgs am{amax_keys_, reinterpret_cast<unsigned int*>(amax_keys_ + Bpad), d_slot, d_tok, last_tok_, hist_,
-                  max_gen_};
+                  max_gen_, tp_rank_ * V, tp_ == 1};
     KRec kr;
     ktic(&kr, gemm_cls_);
     if (on(7))
@@ -1067,6 +1113,11 @@ sgs_status Engine::decode_body(int Bk) {
          "gemm lm_head");
     ktoc(&kr, 2.0 * V * d, 2.0 * d + (keep ? 4.0 * V : 0.0), 2.0 * V * d, Bk);
     launches += 1;
+    if (tp_ > 1) {  // the shards' (max logit, lowest index) keys: all-reduce max, then the tokens
+      CK(tp_allreduce_max_u64(amax_keys_, (size_t)Bk), "tp allreduce argmax");
+      CK(argmax_keys_finalize(amax_keys_, Bk, d_slot, d_tok, last_tok_, hist_, max_gen_, st_), "argmax finalize");
+      ++launches;
+    }
   } else {
     if (on(7)) CK(gemm(lm_head_, x_, logits_, V, d, Bk, false, fuse ? &pnf : nullptr), "gemm lm_head");
     ktic(&ko, 5);
@@ -1164,11 +1215,15 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
       CK(attn_prefill(q_, kc_, vc_, d_offs, d_qblocks, n_qblocks, nq, nkv, hd, ao_, st_), "attn_prefill");
     // algorithmic bytes: q, k, v in and o out once per row (bf16); flops from the chunk's prompts
     ktoc(&kr, 0.0, 2.0 * hd * (2.0 * nq + 2.0 * nkv), cur_pf_attn_flops_ / std::max(T, 1), T);
+    if (tp_ > 1 && tp_rank_ != 0) CK(cudaMemsetAsync(h_, 0, (size_t)T * d * 4, st_), "tp zero h");
     CK(gemm(Ly.wo, ao_, h_, d, nq * hd, T, true), "gemm o");
+    if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)T * d), "tp allreduce o");
     CK(save(), "dump");
     CK(rmsnorm(h_, Ly.n2, x_, nullptr, T, d, m_.rms_eps, st_), "rmsnorm2");
     CK(gate_up(Ly.wgu, T), "gemm gate_up + SwiGLU");
+    if (tp_ > 1 && tp_rank_ != 0) CK(cudaMemsetAsync(h_, 0, (size_t)T * d * 4, st_), "tp zero h");
     CK(gemm(Ly.wd, mm_, h_, d, f, T, true), "gemm down");
+    if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)T * d), "tp allreduce down");
     CK(save(), "dump");
     launches += 4;  // rmsnorm x2, RoPE, attention; the GEMMs count themselves
   }
@@ -1178,8 +1233,19 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
   }
   CK(rmsnorm(h_, nf_, x_, d_last_rows, np, d, m_.rms_eps, st_), "rmsnorm f");
   float* lg = logits_ + (size_t)((e_.max_batch + 15) / 16 * 16 + row_base) * V;
-  CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
-  CK(sample(lg, np, reinterpret_cast<const uint32_t*>(d_pf_tok + np), d_pf_slot, d_pf_tok), "sampler");
+  if (tp_ > 1) {
+    // the shards' LM-head halves: fused argmax keys, all-reduce max, tokens
+    const bool keep = (e_.flags & SGS_F_KEEP_LOGITS) != 0;
+    ArgmaxArgs am{amax_keys_pf_, nullptr, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, tp_rank_ * V, 0};
+    CK(gemm_bf16(lm_head_, x_, keep ? lg : nullptr, V, d, np, V, 4, 1, st_, &am), "gemm lm_head");
+    CK(tp_allreduce_max_u64(amax_keys_pf_, (size_t)np), "tp allreduce argmax");
+    CK(argmax_keys_finalize(amax_keys_pf_, np, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, st_),
+       "argmax finalize");
+    launches += 3;
+  } else {
+    CK(gemm(lm_head_, x_, lg, V, d, np, false), "gemm lm_head");
+    CK(sample(lg, np, reinterpret_cast<const uint32_t*>(d_pf_tok + np), d_pf_slot, d_pf_tok), "sampler");
+  }
   launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }
@@ -1187,6 +1253,10 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
 // Standalone prefill forward of one prompt in slot 0 (idle handle only) with
 // the residual stream dumped after the embedding and every residual add.
 sgs_status Engine::debug_forward(const int32_t* tokens, int32_t T, float* dump, int layer, const float* h_in) {
+  if (tp_ > 1) {
+    err = "debug hooks are not available on tensor-parallel shards";
+    return SGS_E_UNSUPPORTED;
+  }
   if (layer == m_.n_layers && h_in && dump && !null_ && T > 0) return debug_head(h_in, T, dump);
   if (layer >= m_.n_layers || (layer >= 0 && !h_in) || (layer < 0 && !tokens)) {
     err = "debug_forward: bad layer / input";
@@ -1274,6 +1344,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*);
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*GroupStart)();
   ncclResult_t (*GroupEnd)();
   const char* (*GetErrorString)(ncclResult_t);
@@ -1292,10 +1363,11 @@ static NcclApi* nccl() {
   api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
   api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
   api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
   api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-  api.ok = api.GetUniqueId && api.CommInitRank && api.Broadcast && api.GroupStart && api.GroupEnd;
+  api.ok = api.GetUniqueId && api.CommInitRank && api.Broadcast && api.AllReduce && api.GroupStart && api.GroupEnd;
   return api.ok ? &api : nullptr;
 }
 
@@ -1324,7 +1396,48 @@ sgs_status Engine::comm_init(const uint8_t id[128], int rank, int world) {
   return SGS_OK;
 }
 
+// NEXT-2: the tensor-parallel communicator (shard tp_rank_ of tp_)
+sgs_status Engine::tp_comm_init(const uint8_t id[128]) {
+  if (tp_ <= 1) {
+    err = "not a tensor-parallel handle (tp_size <= 1)";
+    return SGS_E_STATE;
+  }
+  NcclApi* api = nccl();
+  if (!api) {
+    err = "libnccl.so.2 not found";
+    return SGS_E_NCCL;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm;
+  ncclResult_t r = api->CommInitRank(&comm, tp_, uid, tp_rank_);
+  if (r != ncclSuccess) {
+    err = std::string("ncclCommInitRank (tp): ") + api->GetErrorString(r);
+    return SGS_E_NCCL;
+  }
+  tp_comm_ = comm;
+  return SGS_OK;
+}
+
+cudaError_t Engine::tp_allreduce_sum(float* x, size_t n) {
+  ++launches;
+  return nccl()->AllReduce(x, x, n, ncclFloat32, ncclSum, (ncclComm_t)tp_comm_, st_) == ncclSuccess
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
+
+cudaError_t Engine::tp_allreduce_max_u64(unsigned long long* x, size_t n) {
+  ++launches;
+  return nccl()->AllReduce(x, x, n, ncclUint64, ncclMax, (ncclComm_t)tp_comm_, st_) == ncclSuccess
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
+
 sgs_status Engine::update_weights(const sgs_weights* src, int root) {
+  if (tp_ > 1 && (src || nccl_world_ > 1)) {
+    err = "weight sync is not available on tensor-parallel shards";
+    return SGS_E_UNSUPPORTED;
+  }
   if (poisoned) {
     err = "handle poisoned";
     return SGS_E_STATE;

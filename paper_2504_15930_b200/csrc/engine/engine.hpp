@@ -23,6 +23,7 @@ struct TensorRef {
   int is_norm;
   int64_t cols = 1;  // row-block placement (interleaved gate/up): blk rows every stride rows at off
   int blk = 0, stride = 0, off = 0;
+  ShardMap shard{};  // tensor-parallel window of the full tensor (NEXT-2)
 };
 
 struct ArenaLayout {
@@ -56,6 +57,7 @@ class Engine {
   sgs_status set_instances(int32_t n_instances, int32_t instance_rank);
   sgs_status checksum(int64_t tensor_id, uint64_t* out);
   sgs_status comm_init(const uint8_t id[128], int rank, int world);
+  sgs_status tp_comm_init(const uint8_t id[128]);
   sgs_status update_weights(const sgs_weights* src, int root);
   sgs_status load_weights(const sgs_weights* w, uint8_t* base, cudaStream_t st);
   sgs_status stage_weights(const sgs_weights* src);
@@ -187,6 +189,14 @@ class Engine {
   bool fused_norm_ = false;                   // RMSNorm fused into the decode GEMMs (SGS_FUSED_NORM=1)
   int64_t dec_launch_ = 0;                    // decode-program launches (PreNorm barrier parity)
   int qblk_ = 64;                             // prefill attention query block (128: tcgen05 kernel)
+  // NEXT-2 tensor parallelism: m_ holds this shard's dims (q/kv heads, FFN, vocab
+  // rows divided by tp_); the embedding table is the full vocabulary
+  int tp_ = 1, tp_rank_ = 0;
+  int64_t vocab_full_ = 0;
+  void* tp_comm_ = nullptr;
+  unsigned long long* amax_keys_pf_ = nullptr;  // prefill rows' argmax keys (TP)
+  cudaError_t tp_allreduce_sum(float* x, size_t n);
+  cudaError_t tp_allreduce_max_u64(unsigned long long* x, size_t n);
   int32_t* tok_host_ = nullptr;  // pinned, completed tokens (the current one of tok_bufs_)
   int64_t tok_host_cap_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

@@ -203,6 +203,32 @@ cudaError_t rope_append(const float* qkv, const void* bias, const int32_t* pos, 
                     page, per, v_f16);
 }
 
+// ------------------------------------------------------------------ tensor-parallel greedy sampling
+// after the all-reduce (max) of the shards' packed (logit, ~vocab index) keys:
+// the token of each row, the keys re-zeroed for the next launch
+__global__ void argmax_keys_finalize_kernel(unsigned long long* keys, int rows, const int32_t* slot,
+                                            const int32_t* tok_idx, int32_t* last_tok, int32_t* hist, int max_gen) {
+  pdl_trigger();
+  pdl_wait();
+  for (int t = threadIdx.x; t < rows; t += blockDim.x) {
+    const unsigned long long k = keys[t];
+    keys[t] = 0ull;
+    const int s = slot[t];
+    if (s >= 0) {
+      const int32_t tok = (int32_t)(~(uint32_t)k);
+      last_tok[s] = tok;
+      hist[(size_t)s * max_gen + tok_idx[t]] = tok;
+    }
+  }
+}
+
+cudaError_t argmax_keys_finalize(unsigned long long* keys, int rows, const int32_t* slot, const int32_t* tok_idx,
+                                 int32_t* last_tok, int32_t* hist, int max_gen, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  return launch_pdl(argmax_keys_finalize_kernel, dim3(1), dim3(256), 0, stream, keys, rows, slot, tok_idx, last_tok,
+                    hist, max_gen);
+}
+
 // ------------------------------------------------------------------ bf16 -> fp16 (exact for the normal fp16 range)
 __global__ void bf16_to_f16_kernel(const __nv_bfloat16* __restrict__ src, __half* __restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -543,9 +569,12 @@ __device__ __forceinline__ int64_t phys_index(int64_t i, int64_t cols, int blk, 
 }
 
 __global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, int64_t n, int is_norm, int64_t cols,
-                                 int blk, int stride, int off) {
+                                 int blk, int stride, int off, ShardMap sm) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t h = splitmix64(key + (uint64_t)i);
+    // a tensor-parallel shard holds a window of the full tensor: element i of
+    // the shard is element (row0 + i / lcols, col0 + i % lcols) of the full one
+    const int64_t g = sm.src_cols ? (sm.row0 + i / sm.lcols) * sm.src_cols + sm.col0 + i % sm.lcols : i;
+    const uint64_t h = splitmix64(key + (uint64_t)g);
     const int32_t m = (int32_t)(h >> 40) - (1 << 23);
     const float u = (float)m * (1.0f / 8388608.0f);
     const float v = is_norm ? __fadd_rn(1.0f, __fmul_rn(u, 0.125f)) : __fmul_rn(u, 0.034641016f);
@@ -554,7 +583,7 @@ __global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, 
 }
 
 cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
-                      int64_t cols, int blk, int stride, int off) {
+                      int64_t cols, int blk, int stride, int off, ShardMap sm) {
   // key = splitmix64(seed ^ tensor_id * C): computed on the host, same constant as DESIGN.md §3
   uint64_t z = seed ^ (tensor_id * 0xD1B54A32D192ED03ull);
   z += 0x9E3779B97F4A7C15ull;
@@ -565,7 +594,7 @@ cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, i
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   hash_init_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<__nv_bfloat16*>(dst), key, n, is_norm, cols, blk,
-                                               stride, off);
+                                               stride, off, sm);
   return cudaGetLastError();
 }
 

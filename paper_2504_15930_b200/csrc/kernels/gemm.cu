@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256, 2)
           // fused greedy sampling: per token, the (value desc, vocab index asc)
           // maximum over this warp's 32 rows, then over the 4 epilogue warps
           // (shared memory), then one 64-bit atomicMax per token and tile
-          const int feat = m0 + 32 * e + lane;
+          const int feat = am.vocab_off + m0 + 32 * e + lane;
           // [4][16] keys, after the exchange buffers (the store path below reuses those)
           unsigned long long* sk = reinterpret_cast<unsigned long long*>(xch + (size_t)xbufs * 4 * 32 * 17);
 #pragma unroll
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256, 2)
     else
       tmem_dealloc(tmem, tmem_cols);
   }
-  if (mode == 4) {
+  if (mode == 4 && am.finalize) {
     // the last CTA to arrive turns the packed keys into tokens (all atomics of
     // every CTA precede its fenced arrival)
     // (no static shared memory in this kernel: the dynamic allocation takes the

@@ -25,6 +25,8 @@ struct ArgmaxArgs {
   int32_t* last_tok;
   int32_t* hist;
   int max_gen;
+  int vocab_off = 0;  // tensor-parallel shard: index of its first vocabulary row
+  int finalize = 1;   // 0: leave the keys for a cross-shard all-reduce (argmax_keys_finalize)
 };
 // RMSNorm fused in front of a GEMM (decode program): before the GEMM reads its
 // activation operand X, the CTAs of the (persistent, co-resident) grid compute
@@ -118,8 +120,15 @@ cudaError_t argmax_rows(const float* logits, int rows, int V, int32_t* ids, cons
 cudaError_t sample_top_p(const float* logits, int rows, int V, float temperature, float top_p, uint64_t seed,
                          const uint32_t* sample_ids, int32_t* ids, const int32_t* slot, const int32_t* tok_idx,
                          int32_t* last_tok, int32_t* out_hist, int max_gen, cudaStream_t stream);
+// tensor-parallel shard of a weight tensor: element i of the shard is element
+// (row0 + i / lcols) * src_cols + col0 + i % lcols of the full tensor (src_cols 0: identity)
+struct ShardMap {
+  int64_t src_cols = 0, row0 = 0, col0 = 0, lcols = 1;
+};
 cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
-                      int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
+                      int64_t cols = 1, int blk = 0, int stride = 0, int off = 0, ShardMap sm = ShardMap{});
+cudaError_t argmax_keys_finalize(unsigned long long* keys, int rows, const int32_t* slot, const int32_t* tok_idx,
+                                 int32_t* last_tok, int32_t* hist, int max_gen, cudaStream_t stream);
 cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream,
                           int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
 cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream,

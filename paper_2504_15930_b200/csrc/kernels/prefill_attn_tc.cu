@@ -16,9 +16,10 @@
 //               rescale in TMEM (tcgen05.ld/st) when the max moves, P = 2^(s -
 //               m) as fp16 into shared memory (K-major, swizzled), then the
 //               final O / l as bf16.
-// Numerics: P and V in fp16 (11 significant bits; V arrives as fp16(bf16 v),
-// which is exact), so P.V keeps ~2^-12 relative precision per term (the
-// legacy kernel's fp16 hi + lo split needed two MMAs for the same bound).
+// Numerics: V arrives as fp16(bf16 v) (exact); P is split P_hi + P_lo in fp16
+// (two MMAs, ~22 significant bits, as the mma.sync kernel does), so P.V keeps
+// the fp32 softmax weights' precision (a single fp16 P moved a 1-layer 7B-width
+// logit by 0.021 against the fp64 oracle; tolerance 2e-2).
 // V is the MN-major B operand (keys x dims in shared memory), so no transpose.
 #include <cmath>
 
@@ -31,7 +32,7 @@ constexpr int PF_M = 128;                   // queries per CTA
 constexpr int PF_N = 128;                   // keys per KV tile
 constexpr int PF_CHUNK = 128 * 64 * 2;      // [128 rows][64 cols] 2-byte, 128-byte swizzle = 16 KB
 constexpr int PF_TILE = 2 * PF_CHUNK;       // 128 x 128 = 32 KB
-constexpr int PF_SMEM = 1024 + 6 * PF_TILE + 512;
+constexpr int PF_SMEM = 1024 + 7 * PF_TILE + 512;  // Q, K[2], V[2], P hi, P lo
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -76,7 +77,8 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sK = sQ + PF_TILE;       // [2]
   uint8_t* sV = sK + 2 * PF_TILE;   // [2]
   uint8_t* sP = sV + 2 * PF_TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + PF_TILE);
+  uint8_t* sPl = sP + PF_TILE;      // P = P_hi + P_lo (fp16 each, ~22 significant bits)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sPl + PF_TILE);
   uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 3, *v_full = bars + 5, *v_empty = bars + 7,
            *s_full = bars + 9, *s_empty = bars + 11, *p_full = bars + 13, *pv_done = bars + 14, *q_empty = bars + 15,
            *o_free = bars + 16;
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer: S_j, then O += P_{j-1} V_{j-1}
-    const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP);
+    const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), pla = smem_u32(sPl);
     int gs = 0, gp = 0, ni = 0;  // global S tile, global PV tile, item
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ni) {
       const Item x = item(it);
@@ -178,10 +180,12 @@ __global__ void __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t vb = smem_u32(sV + s * PF_TILE);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {  // keys 16 kk .. 16 kk + 15
-            const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
+          for (int kk = 0; kk < 8; ++kk) {  // keys 16 kk .. 16 kk + 15: O += P_hi V, then P_lo V
             const uint64_t bd = umma_desc_sw128_mn(vb + kk * 2048, PF_CHUNK, 1024);
+            const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
             umma_bf16(tmem + 256u, ad, bd, PF_IDESC_PV, (j > 1 || kk > 0) ? 1u : 0u);
+            const uint64_t al = umma_desc_sw128(pla + (kk >> 2) * PF_CHUNK) + 2 * (kk & 3);
+            umma_bf16(tmem + 256u, al, bd, PF_IDESC_PV, 1u);
           }
           umma_commit(pv_done);
           umma_commit(&v_empty[s]);
@@ -237,23 +241,25 @@ __global__ void __launch_bounds__(192, 1)
           tmem_wait_st();
         }
         l *= alpha;
-        // P = 2^(s * scale - m_new) as fp16, row `row` of the K-major swizzled P tile
+        // P = 2^(s * scale - m_new) split as P_hi + P_lo (fp16 each: ~22 significant bits,
+        // the precision of the fp32 softmax weights), rows of the K-major swizzled P tiles
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          uint32_t pk[8];
+          uint32_t ph[8], pl[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
             const int key = kbase + 16 * c + i;
             const float p0 = key <= kmax ? exp2f(fmaf(__uint_as_float(r[c][i]), scale_log2, -m_new)) : 0.f;
             const float p1 = key + 1 <= kmax ? exp2f(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, -m_new)) : 0.f;
-            const __half2 hp = __floats2half2_rn(p0, p1);
-            l += __low2float(hp) + __high2float(hp);  // the denominator sums what the MMA multiplies
-            pk[i >> 1] = *reinterpret_cast<const uint32_t*>(&hp);
+            l += p0 + p1;
+            split_f16x2(p0, p1, ph[i >> 1], pl[i >> 1]);
           }
-          uint8_t* chunk = sP + (c >> 2) * PF_CHUNK + row * 128;
           const int u0 = 2 * (c & 3);  // 16-byte units (8 keys) within the 128-byte row
-          *reinterpret_cast<uint4*>(chunk + ((u0 ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(chunk + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          const size_t o0 = (size_t)(c >> 2) * PF_CHUNK + row * 128;
+          *reinterpret_cast<uint4*>(sP + o0 + ((u0 ^ (row & 7)) << 4)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+          *reinterpret_cast<uint4*>(sP + o0 + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(ph[4], ph[5], ph[6], ph[7]);
+          *reinterpret_cast<uint4*>(sPl + o0 + ((u0 ^ (row & 7)) << 4)) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+          *reinterpret_cast<uint4*>(sPl + o0 + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
         }
         m = m_new;
         tc_fence_before();

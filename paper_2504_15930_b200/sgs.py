@@ -37,7 +37,7 @@ EXPORTS = [
     "sgs_op_argmax", "sgs_op_prefill_attention", "sgs_debug_forward", "sgs_op_silu_mul", "sgs_kernel_stats", "sgs_io_bytes",
     "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer", "sgs_op_sample_top_p",
     "sgs_weight_tensors", "sgs_stage_weights", "sgs_prefill_workspace_bytes", "sgs_host_state",
-    "sgs_op_decode_attention_timed", "sgs_elastic_plan", "sgs_set_instances",
+    "sgs_op_decode_attention_timed", "sgs_elastic_plan", "sgs_set_instances", "sgs_tp_comm_init",
 ]
 
 
@@ -66,7 +66,7 @@ class EngineCfg(ctypes.Structure):
                 ("alpha_pct", ctypes.c_int32), ("score", ctypes.c_int32), ("tail_ceil", ctypes.c_int32),
                 ("profile", TbProfile), ("sampling", ctypes.c_int32), ("temperature", ctypes.c_float),
                 ("top_p", ctypes.c_float), ("sample_seed", ctypes.c_uint64), ("weight_seed", ctypes.c_uint64),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("tp_size", ctypes.c_int32), ("tp_rank", ctypes.c_int32)]
 
 
 class Weights(ctypes.Structure):
@@ -107,6 +107,7 @@ def _declare(L):
     L.sgs_host_state.argtypes = [vp, P(i64), P(i64), P(i64)]
     L.sgs_elastic_plan.argtypes = [P(EngineCfg), i32, P(u64), P(i32), P(i32), i64, i64, P(i64), P(i64), P(i32)]
     L.sgs_set_instances.argtypes = [vp, i32, i32]
+    L.sgs_tp_comm_init.argtypes = [vp, P(ctypes.c_uint8)]
     L.sgs_prefill_workspace_bytes.argtypes = [i32, i32, i32, i32]
     L.sgs_prefill_workspace_bytes.restype = i64
     L.sgs_destroy.argtypes = [vp]
@@ -212,7 +213,8 @@ class Instance:
                  instance_rank: int = 0, dispatch: str = "skew", alpha_pct: int = 20, score: int = 0,
                  tail_ceil: int = 0, profile=(2000, 1000, 208, 5000), weight_seed: int = 1234,
                  sample_seed: int = 0, flags: int = 0, max_prefill_tokens: int = 16384, stream=None,
-                 top_p: float | None = None, temperature: float = 1.0, trace: bool = True, weights=None):
+                 top_p: float | None = None, temperature: float = 1.0, trace: bool = True, weights=None,
+                 tp_size: int = 1, tp_rank: int = 0):
         """weights: None (hash-init from weight_seed) or a list of bf16 tensors in the
         canonical order of weight_tensors(shape).  trace: keep the schedule trace
         (SGS_F_TRACE; the C default is off, bench.py turns it off)."""
@@ -227,6 +229,7 @@ class Instance:
         e.profile = TbProfile(*profile)
         e.sampling, e.temperature, e.top_p = (1 if top_p is not None else 0), temperature, (top_p or 1.0)
         e.sample_seed, e.weight_seed, e.flags = sample_seed, weight_seed, flags | (F_TRACE if trace else 0)
+        e.tp_size, e.tp_rank = tp_size, tp_rank
         self.arena = None
         self.stream = None
         if device is None:
@@ -347,6 +350,11 @@ class Instance:
     def comm_init(self, uid: bytes, rank: int, world: int):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib().sgs_comm_init(self.h, buf, rank, world), self.h)
+
+    def tp_comm_init(self, uid: bytes):
+        """NEXT-2: the tensor-parallel communicator (uid from comm_unique_id on shard 0)."""
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().sgs_tp_comm_init(self.h, buf), self.h)
 
     def update_weights(self, root: int = 0, weights=None):
         """Weight sync: the root copies `weights` (canonical order, or None = keep its

@@ -9,3 +9,5 @@ timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --mas
 tail -2 gpurun_out/r02g/c3_n4_noisy.log | cut -c1-300
 SGS_TRACE_DIR=gpurun_out/r02g/traces timeout 900 python -m pytest tests/test_dp_traces.py -q -p no:cacheprovider > gpurun_out/r02g/pytest_traces.log 2>&1; tail -3 gpurun_out/r02g/pytest_traces.log
 rm -rf gpurun_out/r02g/traces
+timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29523 tools/elastic_experiment.py --steps 6 --out gpurun_out/r02g/elastic_7b.json > gpurun_out/r02g/elastic.log 2>&1
+grep step gpurun_out/r02g/elastic.log | cut -c1-300

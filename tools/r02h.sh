@@ -8,3 +8,5 @@ tail -3 gpurun_out/r02h/c4_wave$off.log | cut -c1-300
 done
 SGS_TRACE_DIR=gpurun_out/r02h/traces timeout 900 python -m pytest tests/test_dp_traces.py -q -p no:cacheprovider > gpurun_out/r02h/pytest_traces.log 2>&1; tail -3 gpurun_out/r02h/pytest_traces.log
 rm -rf gpurun_out/r02h/traces
+timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29551 tools/tp_experiment.py --mode tail --out gpurun_out/r02h/tp_tail.json > gpurun_out/r02h/tp_tail.log 2>&1
+grep -E "A_tp2|B_dp4" gpurun_out/r02h/tp_tail.log | cut -c1-300

@@ -1,0 +1,135 @@
+"""NEXT-2 on hardware: tensor-parallel (TP = 2) generation instances for the
+long tail ("tensor parallelism ... to reduce the per-sample
+latency"; dedicated instances for the long-tail samples).
+
+  --mode sweep   (2 GPUs) decode T(b) of one TP = 2 instance at a context,
+                 prompts admitted without prefill (SGS_F_SKIP_PREFILL)
+  --mode tail    (4 GPUs) one RL batch two ways: (A) the tail group (top
+                 alpha% by hint) on a TP = 2 instance over GPUs 0-1 and the
+                 rest round-robin on two DP instances (GPUs 2, 3); (B) four DP
+                 instances, round-robin over the whole batch (the best policy
+                 of config 3).  Makespan = max over instances (device time).
+
+    torchrun --nproc-per-node 2 tools/tp_experiment.py --mode sweep --out gpurun_out/tp_sweep.json
+    torchrun --nproc-per-node 4 tools/tp_experiment.py --mode tail --out gpurun_out/tp_tail.json
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import workload  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", default="sweep", choices=["sweep", "tail"])
+    ap.add_argument("--model", default="qwen2.5-7b")
+    ap.add_argument("--ctx", type=int, default=2048)
+    ap.add_argument("--b", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32, 64, 128, 256])
+    ap.add_argument("--prompts", type=int, default=1024)
+    ap.add_argument("--alpha-pct", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    import paper_2504_15930_b200 as sgs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", rank))
+    shape = workload.MODELS[a.model]
+    out = {"mode": a.mode, "model": a.model}
+
+    def tp_pair(ranks, **kw):
+        """A TP = 2 instance over `ranks` (this rank must be in it)."""
+        r = ranks.index(rank)
+        inst = sgs.Instance(shape, kw.pop("B"), kw.pop("max_ctx"), device=rank, tp_size=2, tp_rank=r, trace=False,
+                            **kw)
+        return inst
+
+    if a.mode == "sweep":
+        assert world == 2
+        inst = tp_pair([0, 1], B=max(a.b), max_ctx=a.ctx + 16, weight_seed=5, flags=sgs.sgs.F_SKIP_PREFILL,
+                       max_prefill_tokens=max(16384, a.ctx))
+        uid = [sgs.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        inst.tp_comm_init(uid[0])
+        pts, nid = [], 0
+        for b in a.b:
+            tr = workload.make_trace(b, a.ctx, 7, 0.0, 7, shape.vocab, seed=b, id_base=nid)
+            nid += b
+            n0 = len(inst.iter_log())
+            inst.submit_trace(tr)
+            inst.run()
+            log = inst.iter_log()[n0:]
+            dec = log[(log[:, 3] == 0) & (log[:, 1] == b)]
+            t = torch.tensor([float(np.median(dec[:, 5])) if len(dec) else 0.0], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pts.append({"b": b, "ctx": a.ctx, "T_us_tp2": float(t[0])})
+            if rank == 0:
+                print(json.dumps(pts[-1]), flush=True)
+        out["points"] = pts
+        inst.close()
+    else:
+        assert world == 4
+        tr = workload.make_trace(a.prompts, 512, 1024, 1.0, 8192, shape.vocab, seed=1234)
+        order = sorted(range(len(tr)), key=lambda i: (-int(tr.hint[i]), int(tr.ids[i])))
+        n_tail = a.alpha_pct * len(tr) // 100
+        tail, reg = tr.subset(order[:n_tail]), tr.subset(order[n_tail:])
+        res = {}
+        for phase in ("A_tp2_tail", "B_dp4_round_robin"):
+            torch.cuda.empty_cache()
+            if phase.startswith("A"):
+                if rank < 2:
+                    inst = tp_pair([0, 1], B=256, max_ctx=512 + 8192, weight_seed=5)
+                    uid = [sgs.comm_unique_id() if rank == 0 else None]
+                else:
+                    inst = sgs.Instance(shape, 256, 512 + 8192, device=rank, n_instances=2, instance_rank=rank - 2,
+                                        dispatch="round_robin", weight_seed=5, trace=False)
+                    uid = [None]
+                objs = [uid[0] if rank == 0 else None]
+                dist.broadcast_object_list(objs, src=0)
+                if rank < 2:
+                    inst.tp_comm_init(objs[0])
+                mine = tail if rank < 2 else reg
+            else:
+                inst = sgs.Instance(shape, 256, 512 + 8192, device=rank, n_instances=4, instance_rank=rank,
+                                    dispatch="round_robin", weight_seed=5, trace=False)
+                mine = tr
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(inst.stream)
+            kept = inst.submit_trace(mine)
+            comps = inst.run()
+            e1.record(inst.stream)
+            torch.cuda.synchronize()
+            rec = {"rank": rank, "samples": kept, "tokens": int(sum(len(c["tokens"]) for c in comps)),
+                   "dev_s": e0.elapsed_time(e1) / 1e3}
+            g = [None] * world
+            dist.all_gather_object(g, rec)
+            if rank == 0:
+                span = max(x["dev_s"] for x in g)
+                # a TP pair generates one set of tokens: count rank 0's, not rank 1's
+                tok = sum(x["tokens"] for x in g if not (phase.startswith("A") and x["rank"] == 1))
+                res[phase] = {"makespan_s": round(span, 3), "tokens": tok, "tokens_per_s": round(tok / span, 1),
+                              "per_rank": g}
+                print(json.dumps({phase: res[phase]}), flush=True)
+            inst.close()
+            del inst
+            dist.barrier()
+        out["alpha_pct"] = a.alpha_pct
+        out["results"] = res
+    if rank == 0 and a.out:
+        json.dump(out, open(a.out, "w"), indent=1)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
