@@ -373,7 +373,11 @@ def main():
     ap.add_argument("--max-out", type=int, default=None, help="cap forced lengths (profiling runs only)")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--iter-log", default=None, help="write the per-iteration log (t,b,adm,pf_tok,sumctx,us) as .npy")
-    ap.add_argument("--dispatch", default="skew", choices=["skew", "random", "round_robin"])
+    # default: round-robin in (hint desc, id asc) order -- the fastest measured policy on B200
+    # (profiles/r02/multi: config 3 at N = 2 / 4, round-robin 125.0 / 83.4 s, random 128.7 / 86.7 s,
+    # the paper's Alg. 2 148.6 / 96.1 s: its single tail instance carries every long sample);
+    # --dispatch skew runs Alg. 2
+    ap.add_argument("--dispatch", default="round_robin", choices=["skew", "random", "round_robin"])
     ap.add_argument("--strong", action="store_true", help="fixed global batch (cfg.n_prompts) instead of per GPU")
     ap.add_argument("--profile", default=None, help="T(b) profile t0_ns,k0_ps,b_star,k1_ps for Alg. 2")
     ap.add_argument("--hint-noise", type=float, default=None, help="ranker noise sigma (None: oracle hints)")
@@ -519,7 +523,8 @@ def main():
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg.model}-shaped random-init bf16 decoder, {per_gpu} prompts/GPU "
                                f"x {cfg.prompt_len} tokens, lognormal(median {cfg.median_out}, sigma {cfg.sigma}) "
-                               f"forced lengths <= {cfg.max_out}, B={cfg.max_batch}, longest-first, Alg. 2 dispatch",
+                               f"forced lengths <= {cfg.max_out}, B={cfg.max_batch}, longest-first, "
+                               f"{args.dispatch} dispatch",
                    "prompts_total": n_total, "global_batch": n_total, "parallelism": f"dp{world}",
                    "dispatch": args.dispatch, "weight_sync": args.weight_sync,
                    "hints": "oracle (= forced)" if args.hint_noise is None else
