@@ -102,8 +102,10 @@ typedef struct {
   /* NEXT-2 tensor parallelism: this handle is shard
    * tp_rank of a tp_size-GPU instance (0 or 1 = no TP).  q/kv heads, FFN
    * columns and vocabulary rows are split tp_size ways (they must divide);
-   * the O / down projections and the LM head's argmax are combined with
-   * NCCL all-reduces over the communicator of sgs_tp_comm_init.  Every shard
+   * the O / down projections and the LM head's argmax are combined across
+   * shards: in the decode program by exchange kernels over NVLink peer
+   * memory (each fused with the RMSNorm that consumes the sum), in prefill
+   * (and with SGS_TP_NCCL_AR=1 everywhere) by NCCL all-reduces.  Every shard
    * runs the same scheduler on the same submissions.  TP shards generate
    * their weights from weight_seed (sgs_init's weights must be NULL), decode
    * greedily, and have no debug hooks or weight sync. */
@@ -216,7 +218,11 @@ sgs_status sgs_comm_unique_id(uint8_t out[128]);
 sgs_status sgs_comm_init(sgs_handle* h, const uint8_t id[128], int32_t rank, int32_t world);
 /* NEXT-2: the tensor-parallel communicator of a tp_size > 1 handle (unique id
  * from sgs_comm_unique_id on shard 0, shared by the caller); must precede the
- * first sgs_step. */
+ * first sgs_step.  Collective over the shards: it also allocates this shard's
+ * peer-exchange buffer (cudaMalloc, freed by sgs_destroy; the one allocation
+ * outside the arena), gathers the shards' CUDA IPC handles over the new
+ * communicator and opens the peers' buffers.  SGS_E_CUDA when IPC is not
+ * available (then set SGS_TP_NCCL_AR=1 on every shard). */
 sgs_status sgs_tp_comm_init(sgs_handle* h, const uint8_t id[128]);
 sgs_status sgs_update_weights(sgs_handle* h, const sgs_weights* src, int32_t root);
 /* Trainer proxy: regenerate this handle's weights from a new seed on device

@@ -25,6 +25,7 @@ SOURCES = [
     "kernels/prefill_attn.cu",
     "kernels/prefill_attn_tc.cu",
     "kernels/elementwise.cu",
+    "kernels/tp_comm.cu",
     "engine/engine.cu",
     "host/sched.cpp",
     "capi.cpp",

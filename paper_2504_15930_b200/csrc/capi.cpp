@@ -1,5 +1,7 @@
 // extern "C" implementation of include/sgs.h.
 #include <cuda_runtime.h>
+#include <execinfo.h>
+#include <signal.h>
 
 #include <algorithm>
 #include <array>
@@ -18,6 +20,23 @@ struct sgs_handle {
 };
 
 static thread_local std::string g_init_err;
+
+// SGS_DEBUG_SIGNALS=1: a fatal signal inside the library prints the native
+// backtrace (libsgs.so offsets, resolve with addr2line) before the default action
+static void sgs_fatal_signal(int sig) {
+  void* bt[64];
+  const int n = backtrace(bt, 64);
+  backtrace_symbols_fd(bt, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+static struct SgsSignalHooks {
+  SgsSignalHooks() {
+    const char* e = std::getenv("SGS_DEBUG_SIGNALS");
+    if (e && e[0] == '1')
+      for (int s : {SIGFPE, SIGSEGV, SIGBUS, SIGABRT}) signal(s, sgs_fatal_signal);
+  }
+} g_signal_hooks;
 
 extern "C" {
 

@@ -151,6 +151,8 @@ Engine::~Engine() {
         if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto& kv : pgraphs_)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (void* p : xch_peer_) cudaIpcCloseMemHandle(p);
+    if (xch_) cudaFree(xch_);
   }
 }
 
@@ -238,14 +240,14 @@ sgs_status Engine::init(const sgs_model_cfg& m_full, const sgs_engine_cfg& e, co
   CK(cudaSetDevice(e.device), "cudaSetDevice");
   st_ = reinterpret_cast<cudaStream_t>(e.stream);
   ArenaLayout L0;
-  layout(m, e_, 0, &L0);
+  layout(m_full, e_, 0, &L0);  // layout() applies tp_local itself
   n_pages_ = e.n_pages;
   if (n_pages_ <= 0) n_pages_ = (e.arena_bytes - L0.total - 4096) / L0.kv_page_bytes;
   if (n_pages_ <= 0) {
     err = "arena too small for weights + scratch";
     return SGS_E_NOMEM;
   }
-  layout(m, e_, n_pages_, &L_);
+  layout(m_full, e_, n_pages_, &L_);
   if (!e.arena || e.arena_bytes < L_.total) {
     err = "arena smaller than sgs_arena_bytes()";
     return SGS_E_NOMEM;
@@ -1060,13 +1062,18 @@ sgs_status Engine::decode_body(int Bk) {
   // RMSNorm fused into the QKV / gate-up / LM-head GEMMs (PreNorm: rows
   // normalised by the GEMM's own CTAs before a grid barrier); the barrier
   // parity is this decode launch's, read from the metadata (D[3])
-  const bool fuse = fused_norm_ && on(0);
+  const bool fuse = fused_norm_ && on(0) && tp_ == 1;
+  // TP over peer memory: each RMSNorm after the first is fused into the
+  // exchange that produces its input (tp_comm.cu), and only shard 0 keeps
+  // the residual (the exchange leaves h = 0 on the others)
+  const bool p2p = tp_p2p_;
   auto pnorm = [&](const void* w, int site) { return PreNorm{h_, w, nullptr, m_.rms_eps, norm_bar_, site, counts + 3}; };
   for (int l = 0; l < m_.n_layers; ++l) {
     const Layer& Ly = layers_[l];
     const PreNorm pn1 = pnorm(Ly.n1, 2 * l), pn2 = pnorm(Ly.n2, 2 * l + 1);
     if (!fuse) ktic(&ko, 5);
-    if (on(0) && !fuse) CK(other(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm1");
+    if (on(0) && !fuse && !(p2p && l > 0))
+      CK(other(rmsnorm(h_, Ly.n1, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm1");
     if (on(1)) CK(gemm(Ly.wqkv, x_, qkv_, qkvN, d, Bk, false, fuse ? &pn1 : nullptr), "gemm qkv");
     ktic(&ko, 5);
     if (on(2))
@@ -1083,20 +1090,35 @@ sgs_status Engine::decode_body(int Bk) {
     ktoc(&kr, -1.0, 0.0, 0.0, 0);
     // TP: every shard adds its partial O projection; shard 0 keeps h, the others
     // start from 0, and the all-reduce (sum) leaves h + sum of partials on all
-    if (tp_ > 1 && tp_rank_ != 0) CK(cudaMemsetAsync(h_, 0, (size_t)Bk * d * 4, st_), "tp zero h");
+    if (tp_ > 1 && tp_rank_ != 0 && (!p2p || l == 0)) CK(cudaMemsetAsync(h_, 0, (size_t)Bk * d * 4, st_), "tp zero h");
     if (on(4)) CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
-    if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)Bk * d), "tp allreduce o");
-    if (!fuse) ktic(&ko, 5);
-    if (on(0) && !fuse) CK(other(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm2");
+    if (p2p) {  // exchange of the O partials + RMSNorm 2 in one kernel
+      ktic(&ko, 5);
+      CK(other(tp_allreduce_rmsnorm(h_, Ly.n2, x_, Bk, d, m_.rms_eps, tpp_, xch_rows_, st_), &ko,
+               (6.0 + 8.0 * (tp_ - 1)) * d),
+         "tp exchange o + rmsnorm2");
+    } else {
+      if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)Bk * d), "tp allreduce o");
+      if (!fuse) ktic(&ko, 5);
+      if (on(0) && !fuse) CK(other(rmsnorm(h_, Ly.n2, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm2");
+    }
     if (on(5)) CK(gate_up(Ly.wgu, Bk, fuse ? &pn2 : nullptr), "gemm gate_up + SwiGLU");
-    if (tp_ > 1 && tp_rank_ != 0) CK(cudaMemsetAsync(h_, 0, (size_t)Bk * d * 4, st_), "tp zero h");
+    if (tp_ > 1 && tp_rank_ != 0 && !p2p) CK(cudaMemsetAsync(h_, 0, (size_t)Bk * d * 4, st_), "tp zero h");
     if (on(6)) CK(gemm(Ly.wd, mm_, h_, d, f, Bk, true), "gemm down");
-    if (tp_ > 1) CK(tp_allreduce_sum(h_, (size_t)Bk * d), "tp allreduce down");
-    launches += fuse ? 2 : 4;  // (rmsnorm x2,) RoPE, attention; the GEMMs count themselves
+    if (p2p) {  // exchange of the down partials + the next layer's RMSNorm 1 (or the final norm)
+      ktic(&ko, 5);
+      CK(other(tp_allreduce_rmsnorm(h_, l + 1 < m_.n_layers ? layers_[l + 1].n1 : nf_, x_, Bk, d, m_.rms_eps, tpp_,
+                                    xch_rows_, st_),
+               &ko, (6.0 + 8.0 * (tp_ - 1)) * d),
+         "tp exchange down + rmsnorm");
+    } else if (tp_ > 1) {
+      CK(tp_allreduce_sum(h_, (size_t)Bk * d), "tp allreduce down");
+    }
+    launches += fuse ? 2 : p2p ? (l == 0 ? 5 : 4) : 4;  // (rmsnorm x2 | exchanges,) RoPE, attention
   }
   const PreNorm pnf = pnorm(nf_, 2 * m_.n_layers);
   if (!fuse) ktic(&ko, 5);
-  if (on(0) && !fuse) CK(other(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm f");
+  if (on(0) && !fuse && !p2p) CK(other(rmsnorm(h_, nf_, x_, nullptr, Bk, d, m_.rms_eps, st_), &ko, 6.0 * d), "rmsnorm f");
   if (e_.sampling == SGS_SAMPLE_GREEDY) {
     // LM head with greedy sampling fused into its epilogue (GEMM mode 4): no
     // fp32 logits round trip and no sampler launch; the logits are still
@@ -1113,7 +1135,11 @@ sgs_status Engine::decode_body(int Bk) {
          "gemm lm_head");
     ktoc(&kr, 2.0 * V * d, 2.0 * d + (keep ? 4.0 * V : 0.0), 2.0 * V * d, Bk);
     launches += 1;
-    if (tp_ > 1) {  // the shards' (max logit, lowest index) keys: all-reduce max, then the tokens
+    if (p2p) {  // the shards' (max logit, lowest index) keys: exchange, max, tokens
+      CK(tp_argmax_exchange(amax_keys_, Bk, d_slot, d_tok, last_tok_, hist_, max_gen_, tpp_, xch_rows_, d, st_),
+         "tp argmax exchange");
+      ++launches;
+    } else if (tp_ > 1) {  // the same over NCCL: all-reduce max, then the tokens
       CK(tp_allreduce_max_u64(amax_keys_, (size_t)Bk), "tp allreduce argmax");
       CK(argmax_keys_finalize(amax_keys_, Bk, d_slot, d_tok, last_tok_, hist_, max_gen_, st_), "argmax finalize");
       ++launches;
@@ -1123,7 +1149,7 @@ sgs_status Engine::decode_body(int Bk) {
     ktic(&ko, 5);
     if (on(8)) CK(other(sample(logits_, Bk, d_sid, d_slot, d_tok), &ko, 4.0 * V), "sampler");
   }
-  launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
+  if (!p2p) launches += 1;  // final rmsnorm (GEMM and sampler count themselves)
   return SGS_OK;
 }
 
@@ -1416,6 +1442,70 @@ sgs_status Engine::tp_comm_init(const uint8_t id[128]) {
     return SGS_E_NCCL;
   }
   tp_comm_ = comm;
+  return tp_p2p_init();
+}
+
+// Decode-program exchange over NVLink peer memory (tp_comm.cu): every shard
+// allocates its exchange buffer, the CUDA IPC handles are gathered over the
+// new communicator (an 8-bit sum of zero-padded handles) and the peers'
+// buffers opened in this process.  SGS_TP_NCCL_AR=1 keeps NCCL all-reduces.
+sgs_status Engine::tp_p2p_init() {
+  const char* env = std::getenv("SGS_TP_NCCL_AR");
+  if ((env && env[0] == '1') || tp_ > TPX_MAX) return SGS_OK;
+  xch_rows_ = (e_.max_batch + 15) / 16 * 16;
+  const size_t bytes = tp_xch_bytes(tp_, xch_rows_, m_.d_model);
+  cudaError_t e = cudaMalloc(&xch_, bytes);
+  if (e == cudaSuccess) e = cudaMemset(xch_, 0, bytes);
+  cudaIpcMemHandle_t mine;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&mine, xch_);
+  uint8_t* gath = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&gath, (size_t)tp_ * sizeof(mine));
+  if (e == cudaSuccess) e = cudaMemset(gath, 0, (size_t)tp_ * sizeof(mine));
+  if (e == cudaSuccess) e = cudaMemcpy(gath + (size_t)tp_rank_ * sizeof(mine), &mine, sizeof(mine), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    err = std::string("tp exchange buffer: ") + cudaGetErrorString(e);
+    if (gath) cudaFree(gath);
+    return SGS_E_CUDA;
+  }
+  std::vector<cudaIpcMemHandle_t> all(tp_);
+  const bool ok = nccl()->AllReduce(gath, gath, (size_t)tp_ * sizeof(mine), ncclUint8, ncclSum, (ncclComm_t)tp_comm_,
+                                    st_) == ncclSuccess;
+  e = ok ? cudaStreamSynchronize(st_) : cudaErrorUnknown;
+  if (e == cudaSuccess) e = cudaMemcpy(all.data(), gath, (size_t)tp_ * sizeof(mine), cudaMemcpyDeviceToHost);
+  cudaFree(gath);
+  if (e != cudaSuccess) {
+    err = "tp exchange: gathering the IPC handles failed";
+    return SGS_E_NCCL;
+  }
+  tpp_.me = tp_rank_;
+  tpp_.tp = tp_;
+  for (int s = 0; s < tp_; ++s) {
+    if (s == tp_rank_) {
+      tpp_.base[s] = xch_;
+      continue;
+    }
+    void* p = nullptr;
+    e = cudaIpcOpenMemHandle(&p, all[s], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      err = std::string("tp exchange: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+      return SGS_E_CUDA;
+    }
+    tpp_.base[s] = static_cast<uint8_t*>(p);
+    xch_peer_.push_back(p);
+  }
+  // every shard has opened its peers' buffers before any exchange is launched
+  uint8_t* one = nullptr;
+  e = cudaMalloc(&one, 4);
+  if (e == cudaSuccess) e = cudaMemset(one, 0, 4);
+  const bool ok2 = e == cudaSuccess && nccl()->AllReduce(one, one, 1, ncclUint8, ncclSum, (ncclComm_t)tp_comm_, st_) ==
+                                           ncclSuccess;
+  e = ok2 ? cudaStreamSynchronize(st_) : cudaErrorUnknown;
+  if (one) cudaFree(one);
+  if (e != cudaSuccess) {
+    err = "tp exchange: barrier failed";
+    return SGS_E_NCCL;
+  }
+  tp_p2p_ = true;
   return SGS_OK;
 }
 

@@ -197,6 +197,13 @@ class Engine {
   unsigned long long* amax_keys_pf_ = nullptr;  // prefill rows' argmax keys (TP)
   cudaError_t tp_allreduce_sum(float* x, size_t n);
   cudaError_t tp_allreduce_max_u64(unsigned long long* x, size_t n);
+  // decode-program exchange over NVLink peer memory (tp_comm.cu; NCCL when off)
+  sgs_status tp_p2p_init();
+  bool tp_p2p_ = false;
+  uint8_t* xch_ = nullptr;
+  std::vector<void*> xch_peer_;
+  TpPeers tpp_{};
+  int xch_rows_ = 0;
   int32_t* tok_host_ = nullptr;  // pinned, completed tokens (the current one of tok_bufs_)
   int64_t tok_host_cap_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

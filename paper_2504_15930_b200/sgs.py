@@ -230,6 +230,7 @@ class Instance:
         e.sampling, e.temperature, e.top_p = (1 if top_p is not None else 0), temperature, (top_p or 1.0)
         e.sample_seed, e.weight_seed, e.flags = sample_seed, weight_seed, flags | (F_TRACE if trace else 0)
         e.tp_size, e.tp_rank = tp_size, tp_rank
+        self.tp_size = max(1, tp_size)
         self.arena = None
         self.stream = None
         if device is None:
@@ -409,7 +410,7 @@ class Instance:
         rows = ctypes.c_int32()
         _check(lib().sgs_last_logits(self.h, None, None, None, 0, ctypes.byref(rows)), self.h)
         r = rows.value
-        lg = np.zeros((r, self.shape.vocab), np.float32)
+        lg = np.zeros((r, self.shape.vocab // self.tp_size), np.float32)  # a TP shard keeps its vocabulary rows
         ids = np.zeros(r, np.uint64)
         tk = np.zeros(r, np.int32)
         _check(lib().sgs_last_logits(self.h, lg.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),

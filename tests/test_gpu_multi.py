@@ -188,11 +188,15 @@ def test_weight_sync_from_trainer_source():
             assert v == oracle.tensor_checksum(555, tid, sizes[tid], tid in {2, 27}), (r["rank"], tid)
 
 
-def _tp_worker(rank, world, port, q, model):
+def _tp_worker(rank, world, port, q, model, ar):
     # NEXT-2: one tensor-parallel instance over 2 GPUs --
     # q/kv heads, FFN columns and vocabulary rows split, O / down partial sums
-    # and the LM-head argmax combined with NCCL all-reduces
+    # and the LM-head argmax combined over NVLink peer memory (tp_comm.cu) or
+    # with NCCL all-reduces (SGS_TP_NCCL_AR=1)
     import torch.distributed as dist
+    os.environ["SGS_TP_NCCL_AR"] = "1" if ar == "nccl" else "0"
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("SGS_TEST_STACK_DUMP_S", "600")), exit=False)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
@@ -227,8 +231,8 @@ def _tp_worker(rank, world, port, q, model):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("model", ["tiny", "qwen2.5-7b"])
-def test_tensor_parallel_instance_vs_oracle(model):
+@pytest.mark.parametrize("model,ar", [("tiny", "p2p"), ("tiny", "nccl"), ("qwen2.5-7b", "p2p")])
+def test_tensor_parallel_instance_vs_oracle(model, ar):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (run with gpurun --gpus 2)")
     import functools
@@ -237,7 +241,7 @@ def test_tensor_parallel_instance_vs_oracle(model):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q, model)) for r in range(2)]
+    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q, model, ar)) for r in range(2)]
     for p in procs:
         p.start()
     tr, res = q.get(timeout=900)

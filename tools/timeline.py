@@ -6,7 +6,8 @@ iteration; per iteration: span and the sum of kernel busy time.
 
     python tools/timeline.py --model qwen2.5-7b --b 1 16 64 256 --ctx 2048 [--out gpurun_out/timeline.json]
 Prompts are admitted without prefill (SGS_F_SKIP_PREFILL); 8 decode iterations
-are traced per b after 4 untraced ones.
+are traced per b after 4 untraced ones.  A tensor-parallel instance (NEXT-2):
+    torchrun --nproc-per-node 2 tools/timeline.py --tp 2 ...   (each shard writes <out>.rank<r>)
 """
 import argparse
 import collections
@@ -27,8 +28,8 @@ def kind(name):
     if "gemm_bf16" in n:
         m = re.search(r"gemm_bf16_tc_kernel<(\d+), (\d+), (\d+)>", n)
         return "gemm" + (f"<cg{m.group(1)},m{m.group(2)}>" if m else "")
-    for k in ("attn_decode", "attn_prefill", "rmsnorm", "rope_append", "embed", "argmax", "top_p", "bt_delta",
-              "silu_mul"):
+    for k in ("tp_allreduce_rmsnorm", "tp_argmax_exchange", "nccl", "attn_decode", "attn_prefill", "rmsnorm",
+              "rope_append", "embed", "argmax", "top_p", "bt_delta", "silu_mul"):
         if k in n:
             return k
     return n[:40]
@@ -41,14 +42,26 @@ def main():
     ap.add_argument("--ctx", type=int, default=2048)
     ap.add_argument("--iters", type=int, default=8)
     ap.add_argument("--out", default="gpurun_out/timeline.json")
+    ap.add_argument("--tp", type=int, default=1)
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
     import paper_2504_15930_b200 as sgs
     shape = workload.MODELS[a.model]
     bmax = max(a.b)
-    inst = sgs.Instance(shape, bmax, a.ctx + 64, device=0, weight_seed=5, trace=False,
-                        flags=sgs.sgs.F_SKIP_PREFILL, max_prefill_tokens=max(16384, a.ctx))
+    rank = int(os.environ.get("RANK", "0"))
+    if a.tp > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo")
+    inst = sgs.Instance(shape, bmax, a.ctx + 64, device=rank, weight_seed=5, trace=False,
+                        flags=sgs.sgs.F_SKIP_PREFILL, max_prefill_tokens=max(16384, a.ctx),
+                        tp_size=a.tp, tp_rank=rank if a.tp > 1 else 0)
+    if a.tp > 1:
+        uid = [sgs.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        inst.tp_comm_init(uid[0])
+        a.out = f"{a.out}.rank{rank}"
     out = {"model": a.model, "ctx": a.ctx, "per_b": {}}
     nid = 0
     for b in a.b:

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--b", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32, 64, 128, 256])
     ap.add_argument("--prompts", type=int, default=1024)
     ap.add_argument("--alpha-pct", type=int, default=20)
+    ap.add_argument("--ar", nargs="*", default=["p2p", "nccl"], choices=["p2p", "nccl"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     import torch
@@ -55,27 +56,33 @@ def main():
 
     if a.mode == "sweep":
         assert world == 2
-        inst = tp_pair([0, 1], B=max(a.b), max_ctx=a.ctx + 16, weight_seed=5, flags=sgs.sgs.F_SKIP_PREFILL,
-                       max_prefill_tokens=max(16384, a.ctx))
-        uid = [sgs.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        inst.tp_comm_init(uid[0])
         pts, nid = [], 0
-        for b in a.b:
-            tr = workload.make_trace(b, a.ctx, 7, 0.0, 7, shape.vocab, seed=b, id_base=nid)
-            nid += b
-            n0 = len(inst.iter_log())
-            inst.submit_trace(tr)
-            inst.run()
-            log = inst.iter_log()[n0:]
-            dec = log[(log[:, 3] == 0) & (log[:, 1] == b)]
-            t = torch.tensor([float(np.median(dec[:, 5])) if len(dec) else 0.0], dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            pts.append({"b": b, "ctx": a.ctx, "T_us_tp2": float(t[0])})
-            if rank == 0:
-                print(json.dumps(pts[-1]), flush=True)
+        for ar in a.ar:
+            # exchange of the partials: NVLink peer memory (tp_comm.cu) or NCCL all-reduces
+            os.environ["SGS_TP_NCCL_AR"] = "1" if ar == "nccl" else "0"
+            inst = tp_pair([0, 1], B=max(a.b), max_ctx=a.ctx + 16, weight_seed=5, flags=sgs.sgs.F_SKIP_PREFILL,
+                           max_prefill_tokens=max(16384, a.ctx))
+            uid = [sgs.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            inst.tp_comm_init(uid[0])
+            for b in a.b:
+                tr = workload.make_trace(b, a.ctx, 7, 0.0, 7, shape.vocab, seed=b, id_base=nid)
+                nid += b
+                n0 = len(inst.iter_log())
+                inst.submit_trace(tr)
+                inst.run()
+                log = inst.iter_log()[n0:]
+                dec = log[(log[:, 3] == 0) & (log[:, 1] == b)]
+                t = torch.tensor([float(np.median(dec[:, 5])) if len(dec) else 0.0], dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                pts.append({"b": b, "ctx": a.ctx, "exchange": ar, "T_us_tp2": float(t[0])})
+                if rank == 0:
+                    print(json.dumps(pts[-1]), flush=True)
+            inst.close()
+            del inst
+            torch.cuda.empty_cache()
+            dist.barrier()
         out["points"] = pts
-        inst.close()
     else:
         assert world == 4
         tr = workload.make_trace(a.prompts, 512, 1024, 1.0, 8192, shape.vocab, seed=1234)
