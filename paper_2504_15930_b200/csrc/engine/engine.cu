@@ -668,7 +668,11 @@ cudaError_t Engine::sample(const float* logits, int rows, const uint32_t* sid, c
 // 148 tiles), else the fp32 GEMM + the silu_mul kernel.
 cudaError_t Engine::gate_up(const void* W, int T, const PreNorm* pn) {
   const int d = m_.d_model, f = m_.d_ffn;
-  if (!(e_.flags & SGS_F_DETERMINISTIC) && gemm_auto_splits(2 * f, d, T) > 1) {
+  // split-K (fp32 partials + a SwiGLU kernel) only when the unsplit GEMM has
+  // fewer 128-row tiles than SMs; at >= 148 tiles (e.g. a TP = 2 shard of 7B)
+  // the fused SwiGLU epilogue saves the extra kernel boundary
+  const int tiles = (2 * f / 128) * ((T + 255) / 256);
+  if (!(e_.flags & SGS_F_DETERMINISTIC) && tiles < 148 && gemm_auto_splits(2 * f, d, T) > 1) {
     cudaError_t e = gemm(W, x_, gu_, 2 * f, d, T, false, pn);
     if (e != cudaSuccess) return e;
     ++launches;
@@ -825,7 +829,8 @@ sgs_status Engine::run_iteration(const IterPlan& plan) {
     return SGS_E_NOMEM;
   }
   D[0] = (int32_t)ap.items.size(), D[1] = (int32_t)ap.combs.size(), D[2] = n_run;
-  D[3] = n_run > 0 ? (int32_t)(dec_launch_++ & 1) : 0;  // PreNorm barrier parity of this decode launch
+  // decode launch counter: PreNorm barrier parity (bit 0) and the TP exchange epochs
+  D[3] = n_run > 0 ? (int32_t)(dec_launch_++ & 0x3fffffff) : 0;
   AttnComb* hcombs = reinterpret_cast<AttnComb*>(D + 4 + 6 * Bpad);
   AttnItem* hitems = reinterpret_cast<AttnItem*>(hcombs + L_.max_items);
   std::memcpy(hcombs, ap.combs.data(), ap.combs.size() * sizeof(AttnComb));
@@ -1067,6 +1072,7 @@ sgs_status Engine::decode_body(int Bk) {
   // exchange that produces its input (tp_comm.cu), and only shard 0 keeps
   // the residual (the exchange leaves h = 0 on the others)
   const bool p2p = tp_p2p_;
+  const int nx = 2 * m_.n_layers + 1;  // exchanges per decode launch (epoch numbering)
   auto pnorm = [&](const void* w, int site) { return PreNorm{h_, w, nullptr, m_.rms_eps, norm_bar_, site, counts + 3}; };
   for (int l = 0; l < m_.n_layers; ++l) {
     const Layer& Ly = layers_[l];
@@ -1094,7 +1100,7 @@ sgs_status Engine::decode_body(int Bk) {
     if (on(4)) CK(gemm(Ly.wo, ao_, h_, d, nq * hd, Bk, true), "gemm o");
     if (p2p) {  // exchange of the O partials + RMSNorm 2 in one kernel
       ktic(&ko, 5);
-      CK(other(tp_allreduce_rmsnorm(h_, Ly.n2, x_, Bk, d, m_.rms_eps, tpp_, xch_rows_, st_), &ko,
+      CK(other(tp_allreduce_rmsnorm(h_, Ly.n2, x_, Bk, d, m_.rms_eps, tpp_, xch_rows_, counts + 3, 2 * l, nx, st_), &ko,
                (6.0 + 8.0 * (tp_ - 1)) * d),
          "tp exchange o + rmsnorm2");
     } else {
@@ -1108,7 +1114,7 @@ sgs_status Engine::decode_body(int Bk) {
     if (p2p) {  // exchange of the down partials + the next layer's RMSNorm 1 (or the final norm)
       ktic(&ko, 5);
       CK(other(tp_allreduce_rmsnorm(h_, l + 1 < m_.n_layers ? layers_[l + 1].n1 : nf_, x_, Bk, d, m_.rms_eps, tpp_,
-                                    xch_rows_, st_),
+                                    xch_rows_, counts + 3, 2 * l + 1, nx, st_),
                &ko, (6.0 + 8.0 * (tp_ - 1)) * d),
          "tp exchange down + rmsnorm");
     } else if (tp_ > 1) {
@@ -1136,7 +1142,8 @@ sgs_status Engine::decode_body(int Bk) {
     ktoc(&kr, 2.0 * V * d, 2.0 * d + (keep ? 4.0 * V : 0.0), 2.0 * V * d, Bk);
     launches += 1;
     if (p2p) {  // the shards' (max logit, lowest index) keys: exchange, max, tokens
-      CK(tp_argmax_exchange(amax_keys_, Bk, d_slot, d_tok, last_tok_, hist_, max_gen_, tpp_, xch_rows_, d, st_),
+      CK(tp_argmax_exchange(amax_keys_, Bk, d_slot, d_tok, last_tok_, hist_, max_gen_, tpp_, xch_rows_, d, counts + 3,
+                            2 * m_.n_layers, nx, st_),
          "tp argmax exchange");
       ++launches;
     } else if (tp_ > 1) {  // the same over NCCL: all-reduce max, then the tokens

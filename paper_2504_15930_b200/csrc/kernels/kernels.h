@@ -131,17 +131,19 @@ cudaError_t argmax_keys_finalize(unsigned long long* keys, int rows, const int32
                                  int32_t* last_tok, int32_t* hist, int max_gen, cudaStream_t stream);
 // ---- NEXT-2 tensor-parallel exchange over NVLink peer memory (tp_comm.cu)
 constexpr int TPX_MAX = 8;     // shards
-constexpr int TPX_CTAS = 148;  // CTAs (= flag slots) of one exchange
+constexpr int TPX_CTAS = 296;  // CTAs of one exchange (two per SM, co-resident)
 struct TpPeers {
   uint8_t* base[TPX_MAX];  // every shard's exchange buffer, mapped in this process (own at [me])
   int me, tp;
 };
 size_t tp_xch_bytes(int tp, int rows, int d);
+// exchange epoch = *launch * per_launch + index + 1 (launch: device counter of
+// the decode launch, index: the exchange's position in it, < per_launch)
 cudaError_t tp_allreduce_rmsnorm(float* h, const void* w, void* y, int T, int d, float eps, const TpPeers& P,
-                                 int rows_cap, cudaStream_t stream);
+                                 int rows_cap, const int32_t* launch, int index, int per_launch, cudaStream_t stream);
 cudaError_t tp_argmax_exchange(unsigned long long* keys, int rows, const int32_t* slot, const int32_t* tok_idx,
                                int32_t* last_tok, int32_t* hist, int max_gen, const TpPeers& P, int rows_cap, int d,
-                               cudaStream_t stream);
+                               const int32_t* launch, int index, int per_launch, cudaStream_t stream);
 cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream,
                           int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
 cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream,
