@@ -282,8 +282,21 @@ def kernel_roofline(inst, stats, peaks, n_iters, dev_s):
             "peak": peak, "unit": unit, "frac": round(roof_ms / st["ms"], 4),
             "frac_definition": "sum over the class's sampled launches of max(algorithmic bytes/HBM, flops/bf16 "
                                "sustained) / their measured time (CUDA events on the engine stream)",
-            "traffic": None, "traffic_source": "ncu --set full per-launch DRAM bytes: profiles/README.md (r02)",
+            "traffic": None, "traffic_source": None,
             "peak_source": peaks["_source"], "share_of_step": round(st["ms"] / it["ms"], 4)}
+    # DRAM bytes per launch: ncu's dram__bytes_read + write over the 7B decode
+    # GEMM shapes (one cold launch each, tools/gemm_traffic.py) relative to
+    # their algorithmic bytes, applied to this class's algorithmic bytes per launch
+    traffic_file = os.path.join(ROOT, "profiles", "r02", "ncu_gemm_traffic.json")
+    if CLASSES[dom] == "decode_gemm" and os.path.exists(traffic_file) and st["launches"] > 0:
+        cases = json.load(open(traffic_file))["cases"]
+        ratio = sum(c["dram_bytes"] for c in cases) / sum(c["alg_bytes"] for c in cases)
+        roof["traffic"] = round(ratio * st["bytes"] / st["launches"])
+        roof["traffic_alg"] = round(st["bytes"] / st["launches"])
+        roof["traffic_over_alg"] = round(ratio, 3)
+        roof["traffic_source"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum / algorithmic bytes over the "
+                                  "decode GEMM shapes (profiles/r02/ncu_gemm_traffic.json) x this class's "
+                                  "algorithmic bytes per sampled launch")
     return roof, kernels
 
 
