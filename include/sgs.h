@@ -144,9 +144,12 @@ sgs_status sgs_arena_bytes(const sgs_model_cfg* m, const sgs_engine_cfg* e, int6
  * Every tensor is bf16, row-major in that logical shape (a PyTorch
  * Linear.weight is [out, in]).  ptrs[i] may be host or device memory (CUDA
  * unified addressing decides the copy direction); the library copies the
- * values into its own layout (gate/up interleaved in 64-row blocks) before
- * the call returns, so the caller keeps ownership.  sgs_weight_tensors lists
- * the order, logical ids and shapes. */
+ * values into its own layout (gate/up interleaved in 64-row blocks; with
+ * SGS_WEIGHT_LAYOUT=tiles every GEMM weight matrix stored as contiguous
+ * [128 rows x 64 cols] blocks) before the call returns, so the
+ * caller keeps ownership (pageable host memory is page-locked for the copy
+ * and released).  sgs_weight_tensors lists the order, logical ids and
+ * shapes. */
 typedef struct {
   const void* const* ptrs;   /* n pointers, canonical order */
   int32_t n;                 /* 3 + 12 * n_layers */
@@ -245,7 +248,8 @@ sgs_status sgs_load_weights_seed(sgs_handle* h, uint64_t seed);
  * previous commit's shadow -> active copy, so a stage or begin may follow a
  * commit immediately; a caller that writes the shadow buffer directly
  * (through sgs_shadow_weights) must first synchronise the handle's stream
- * after a commit. */
+ * after a commit, and writes the library's internal layout (the arena's
+ * weight region byte for byte); sgs_stage_weights takes canonical tensors. */
 sgs_status sgs_shadow_weights(sgs_handle* h, void** ptr, int64_t* bytes);
 sgs_status sgs_stage_weights_seed(sgs_handle* h, uint64_t seed);
 /* Trainer path of the asynchronous sync: copy src (canonical order, host or

@@ -167,24 +167,31 @@ void Engine::build_tensor_table() {
     return tp > 1 ? ShardMap{src_cols, 0, col0, lcols} : ShardMap{};
   };
   tensors_.push_back({0, embed_, vocab_full_ * d, 0});
-  tensors_.push_back({1, lm_head_, (int64_t)m_.vocab * d, 0, 1, 0, 0, 0, rows_win(r * m_.vocab, d)});
+  // GEMM weights: row-major, or (w_tiled_) the tiled layout of their fused
+  // matrix; a tensor at row R0 of a fused matrix is placed with blk = its
+  // rows, stride 0, off = R0 (kernels.h weight placement)
+  const int tl = w_tiled_;
+  auto gemm_w = [&](int64_t id, void* base, int64_t rows, int64_t k, int64_t r0, ShardMap sm) {
+    if (tl) return TensorRef{id, base, rows * k, 0, k, (int)rows, 0, (int)r0, sm, 1};
+    return TensorRef{id, (void*)((uint16_t*)base + r0 * k), rows * k, 0, 1, 0, 0, 0, sm, 0};
+  };
+  tensors_.push_back(gemm_w(1, lm_head_, m_.vocab, d, 0, rows_win(r * m_.vocab, d)));
   tensors_.push_back({2, nf_, d, 1});
   for (int l = 0; l < m_.n_layers; ++l) {
     const int64_t b = 16 + 16 * (int64_t)l;
     auto* L = &layers_[l];
     auto at = [](void* p, int64_t elems) { return (void*)((uint16_t*)p + elems); };
-    tensors_.push_back({b + 0, L->wqkv, nq * hd * d, 0, 1, 0, 0, 0, rows_win(r * nq * hd, d)});
-    tensors_.push_back({b + 1, at(L->wqkv, nq * hd * d), nkv * hd * d, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, d)});
-    tensors_.push_back(
-        {b + 2, at(L->wqkv, (nq + nkv) * hd * d), nkv * hd * d, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, d)});
+    tensors_.push_back(gemm_w(b + 0, L->wqkv, nq * hd, d, 0, rows_win(r * nq * hd, d)));
+    tensors_.push_back(gemm_w(b + 1, L->wqkv, nkv * hd, d, nq * hd, rows_win(r * nkv * hd, d)));
+    tensors_.push_back(gemm_w(b + 2, L->wqkv, nkv * hd, d, (nq + nkv) * hd, rows_win(r * nkv * hd, d)));
     tensors_.push_back({b + 3, L->bqkv, nq * hd, 0, 1, 0, 0, 0, rows_win(r * nq * hd, 1)});
     tensors_.push_back({b + 4, at(L->bqkv, nq * hd), nkv * hd, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, 1)});
     tensors_.push_back({b + 5, at(L->bqkv, (nq + nkv) * hd), nkv * hd, 0, 1, 0, 0, 0, rows_win(r * nkv * hd, 1)});
-    tensors_.push_back({b + 6, L->wo, d * nq * hd, 0, 1, 0, 0, 0, cols_win(nq * hd * tp, r * nq * hd, nq * hd)});
+    tensors_.push_back(gemm_w(b + 6, L->wo, d, nq * hd, 0, cols_win(nq * hd * tp, r * nq * hd, nq * hd)));
     // gate and up interleave in 64-row blocks: tile i of the fused matrix = 64 gate rows + 64 up rows
-    tensors_.push_back({b + 7, L->wgu, f * d, 0, d, 64, 128, 0, rows_win(r * f, d)});
-    tensors_.push_back({b + 8, L->wgu, f * d, 0, d, 64, 128, 64, rows_win(r * f, d)});
-    tensors_.push_back({b + 9, L->wd, d * f, 0, 1, 0, 0, 0, cols_win(f * tp, r * f, f)});
+    tensors_.push_back({b + 7, L->wgu, f * d, 0, d, 64, 128, 0, rows_win(r * f, d), tl});
+    tensors_.push_back({b + 8, L->wgu, f * d, 0, d, 64, 128, 64, rows_win(r * f, d), tl});
+    tensors_.push_back(gemm_w(b + 9, L->wd, d, f, 0, cols_win(f * tp, r * f, f)));
     tensors_.push_back({b + 10, L->n1, d, 1});
     tensors_.push_back({b + 11, L->n2, d, 1});
   }
@@ -349,6 +356,9 @@ sgs_status Engine::init(const sgs_model_cfg& m_full, const sgs_engine_cfg& e, co
     sgs_rope_table(tab.data(), e.max_ctx + 1, m.head_dim, m.rope_theta);
     CK(cudaMemcpy(rope_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice), "rope table");
   }
+  // GEMM weight layout: tiled 16 KB blocks (one contiguous TMA box each) or
+  // row-major (SGS_WEIGHT_LAYOUT=rows)
+  if (const char* wl = std::getenv("SGS_WEIGHT_LAYOUT")) w_tiled_ = std::string(wl) == "tiles" ? 1 : 0;
   build_tensor_table();
   sgs_status s = w ? load_weights(w, arena_, st_) : load_weights_seed(e.weight_seed);
   if (s != SGS_OK) return s;
@@ -375,7 +385,26 @@ sgs_status Engine::load_weights(const sgs_weights* w, uint8_t* base, cudaStream_
   for (size_t i = 0; i < tensors_.size(); ++i) {
     const TensorRef& t = tensors_[i];
     uint8_t* dst = base + (reinterpret_cast<uint8_t*>(t.ptr) - arena_);
-    if (t.blk == 0) {
+    if (t.tiled) {
+      // canonical row-major source -> tiled placement by a kernel that reads the
+      // source directly: device memory, or host memory page-locked for the copy
+      const void* src = w->ptrs[i];
+      const size_t bytes = (size_t)t.n * 2;
+      cudaPointerAttributes pa{};
+      bool reg = false;
+      if (cudaPointerGetAttributes(&pa, src) != cudaSuccess) cudaGetLastError();
+      if (pa.type == cudaMemoryTypeUnregistered) {
+        CK(cudaHostRegister(const_cast<void*>(src), bytes, cudaHostRegisterMapped), "cudaHostRegister(weights)");
+        reg = true;
+      }
+      void* dsrc = const_cast<void*>(src);
+      if (pa.type == cudaMemoryTypeHost || reg) CK(cudaHostGetDevicePointer(&dsrc, const_cast<void*>(src), 0), "host pointer");
+      CK(relayout_bf16(dsrc, dst, t.n, t.cols, t.blk, t.stride, t.off, 1, st), "weight relayout");
+      if (reg) {
+        CK(cudaStreamSynchronize(st), "weight relayout sync");
+        CK(cudaHostUnregister(const_cast<void*>(src)), "cudaHostUnregister(weights)");
+      }
+    } else if (t.blk == 0) {
       CK(cudaMemcpyAsync(dst, w->ptrs[i], (size_t)t.n * 2, cudaMemcpyDefault, st), "weight copy");
     } else {
       // rows of 64 gate (or up) rows land every 128 rows of the fused matrix
@@ -402,7 +431,7 @@ sgs_status Engine::set_instances(int32_t n_instances, int32_t instance_rank) {
 sgs_status Engine::load_weights_seed(uint64_t seed) {
   if (null_) return SGS_OK;
   for (const auto& t : tensors_) {
-    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_, t.cols, t.blk, t.stride, t.off, t.shard),
+    CK(hash_init(t.ptr, seed, (uint64_t)t.id, t.n, t.is_norm, st_, t.cols, t.blk, t.stride, t.off, t.shard, t.tiled),
        "hash_init");
     ++launches;
   }
@@ -418,7 +447,7 @@ sgs_status Engine::checksum(int64_t tensor_id, uint64_t* out) {
   for (const auto& t : tensors_)
     if (t.id == tensor_id) {
       CK(cudaMemsetAsync(cksum_dev_, 0, 8, st_), "memset");
-      CK(checksum_bf16(t.ptr, t.n, cksum_dev_, st_, t.cols, t.blk, t.stride, t.off), "checksum");
+      CK(checksum_bf16(t.ptr, t.n, cksum_dev_, st_, t.cols, t.blk, t.stride, t.off, t.tiled), "checksum");
       unsigned long long v = 0;
       CK(cudaMemcpyAsync(&v, cksum_dev_, 8, cudaMemcpyDeviceToHost, st_), "checksum d2h");
       CK(cudaStreamSynchronize(st_), "checksum sync");
@@ -642,9 +671,9 @@ cudaError_t Engine::gemm(const void* W, const void* X, float* C, int N, int K, i
       e = cudaMemsetAsync(C, 0, (size_t)T * N * 4, st_);
       if (e != cudaSuccess) return e;
     }
-    e = gemm_bf16(W, X, C, N, K, T, N, 1, splits, st_, nullptr, pn);
+    e = gemm_bf16(W, X, C, N, K, T, N, 1, splits, st_, nullptr, pn, w_tiled_);
   } else {
-    e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_, nullptr, pn);
+    e = gemm_bf16(W, X, C, N, K, T, N, accumulate ? 2 : 0, 1, st_, nullptr, pn, w_tiled_);
   }
   // algorithmic bytes: weights + per row activations in + fp32 out (read-modify-write when accumulating)
   ktoc(&kr, 2.0 * N * K, 2.0 * K + (accumulate ? 8.0 : 4.0) * N, 2.0 * N * K, T);
@@ -680,7 +709,7 @@ cudaError_t Engine::gate_up(const void* W, int T, const PreNorm* pn) {
   }
   KRec kr;
   ktic(&kr, gemm_cls_);
-  cudaError_t e = gemm_bf16(W, x_, reinterpret_cast<float*>(mm_), 2 * f, d, T, f, 3, 1, st_, nullptr, pn);
+  cudaError_t e = gemm_bf16(W, x_, reinterpret_cast<float*>(mm_), 2 * f, d, T, f, 3, 1, st_, nullptr, pn, w_tiled_);
   ktoc(&kr, 2.0 * 2 * f * d, 2.0 * d + 2.0 * f, 2.0 * 2 * f * d, T);
   ++launches;
   return e;
@@ -1137,7 +1166,8 @@ sgs_status Engine::decode_body(int Bk) {
     KRec kr;
     ktic(&kr, gemm_cls_);
     if (on(7))
-      CK(gemm_bf16(lm_head_, x_, keep ? logits_ : nullptr, V, d, Bk, V, 4, 1, st_, &am, fuse ? &pnf : nullptr),
+      CK(gemm_bf16(lm_head_, x_, keep ? logits_ : nullptr, V, d, Bk, V, 4, 1, st_, &am, fuse ? &pnf : nullptr,
+                   w_tiled_),
          "gemm lm_head");
     ktoc(&kr, 2.0 * V * d, 2.0 * d + (keep ? 4.0 * V : 0.0), 2.0 * V * d, Bk);
     launches += 1;
@@ -1270,7 +1300,7 @@ sgs_status Engine::prefill_chunk(const std::vector<int32_t>& idx, int row_base, 
     // the shards' LM-head halves: fused argmax keys, all-reduce max, tokens
     const bool keep = (e_.flags & SGS_F_KEEP_LOGITS) != 0;
     ArgmaxArgs am{amax_keys_pf_, nullptr, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, tp_rank_ * V, 0};
-    CK(gemm_bf16(lm_head_, x_, keep ? lg : nullptr, V, d, np, V, 4, 1, st_, &am), "gemm lm_head");
+    CK(gemm_bf16(lm_head_, x_, keep ? lg : nullptr, V, d, np, V, 4, 1, st_, &am, nullptr, w_tiled_), "gemm lm_head");
     CK(tp_allreduce_max_u64(amax_keys_pf_, (size_t)np), "tp allreduce argmax");
     CK(argmax_keys_finalize(amax_keys_pf_, np, d_pf_slot, d_pf_tok, last_tok_, hist_, max_gen_, st_),
        "argmax finalize");
@@ -1622,7 +1652,7 @@ sgs_status Engine::stage_weights_seed(uint64_t seed) {
   // the same tensors at the same offsets of the shadow buffer, on the side stream
   for (const auto& t : tensors_) {
     void* dst = shadow_ + (reinterpret_cast<uint8_t*>(t.ptr) - arena_);
-    CK(hash_init(dst, seed, (uint64_t)t.id, t.n, t.is_norm, st_side_, t.cols, t.blk, t.stride, t.off),
+    CK(hash_init(dst, seed, (uint64_t)t.id, t.n, t.is_norm, st_side_, t.cols, t.blk, t.stride, t.off, t.shard, t.tiled),
        "hash_init(shadow)");
   }
   return SGS_OK;

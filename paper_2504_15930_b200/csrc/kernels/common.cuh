@@ -220,6 +220,27 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const CUtensorMa
       : "memory");
 }
 
+// 4-D TMA load from tiled weights [rows/128][K/64][128][64] viewed as
+// (64, 128, K/64, rows/128): box (64, 128, kc, 1) at k-chunk `chunk` of
+// 128-row tile `tile` -- kc contiguous 16 KB blocks, landing exactly as the
+// row-major 2-D / 3-D boxes do.
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* map, int32_t chunk, int32_t tile,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(0), "r"(chunk), "r"(tile)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm(void* smem_dst, const CUtensorMap* map, int32_t chunk, int32_t tile,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(0), "r"(0), "r"(chunk), "r"(tile)
+      : "memory");
+}
+
 // Shared-memory matrix descriptor for a K-major operand tile stored with the
 // 128-byte swizzle (rows of 64 bf16 = 128 B, 8-row groups 1024 B apart).
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {

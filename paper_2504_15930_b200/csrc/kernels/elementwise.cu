@@ -562,14 +562,16 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
 // row blocks of `blk` rows every `stride` rows starting at `off` (blk 0:
 // contiguous).  The gate/up weights interleave 64-row blocks so
 // one 128-row GEMM tile holds the gate and up rows of the same 64 features.
-__device__ __forceinline__ int64_t phys_index(int64_t i, int64_t cols, int blk, int stride, int off) {
-  if (blk == 0) return i;
+__device__ __forceinline__ int64_t phys_index(int64_t i, int64_t cols, int blk, int stride, int off, int tiled) {
+  if (blk == 0 && !tiled) return i;
   const int64_t r = i / cols, c = i - r * cols;
-  return ((r / blk) * stride + off + r % blk) * cols + c;
+  const int64_t R = blk ? (r / blk) * stride + off + r % blk : r;
+  if (!tiled) return R * cols + c;
+  return (((R >> 7) * (cols >> 6) + (c >> 6)) << 13) + ((R & 127) << 6) + (c & 63);
 }
 
 __global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, int64_t n, int is_norm, int64_t cols,
-                                 int blk, int stride, int off, ShardMap sm) {
+                                 int blk, int stride, int off, ShardMap sm, int tiled) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     // a tensor-parallel shard holds a window of the full tensor: element i of
     // the shard is element (row0 + i / lcols, col0 + i % lcols) of the full one
@@ -578,12 +580,12 @@ __global__ void hash_init_kernel(__nv_bfloat16* __restrict__ dst, uint64_t key, 
     const int32_t m = (int32_t)(h >> 40) - (1 << 23);
     const float u = (float)m * (1.0f / 8388608.0f);
     const float v = is_norm ? __fadd_rn(1.0f, __fmul_rn(u, 0.125f)) : __fmul_rn(u, 0.034641016f);
-    dst[phys_index(i, cols, blk, stride, off)] = __float2bfloat16_rn(v);
+    dst[phys_index(i, cols, blk, stride, off, tiled)] = __float2bfloat16_rn(v);
   }
 }
 
 cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
-                      int64_t cols, int blk, int stride, int off, ShardMap sm) {
+                      int64_t cols, int blk, int stride, int off, ShardMap sm, int tiled) {
   // key = splitmix64(seed ^ tensor_id * C): computed on the host, same constant as DESIGN.md §3
   uint64_t z = seed ^ (tensor_id * 0xD1B54A32D192ED03ull);
   z += 0x9E3779B97F4A7C15ull;
@@ -594,27 +596,59 @@ cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, i
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   hash_init_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<__nv_bfloat16*>(dst), key, n, is_norm, cols, blk,
-                                               stride, off, sm);
+                                               stride, off, sm, tiled);
   return cudaGetLastError();
 }
 
 __global__ void checksum_kernel(const uint16_t* __restrict__ src, int64_t n, unsigned long long* out, int64_t cols,
-                                int blk, int stride, int off) {
+                                int blk, int stride, int off, int tiled) {
   unsigned long long acc = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    acc += (unsigned long long)src[phys_index(i, cols, blk, stride, off)] * (unsigned long long)(2 * i + 1);
+    acc += (unsigned long long)src[phys_index(i, cols, blk, stride, off, tiled)] * (unsigned long long)(2 * i + 1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
 cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream, int64_t cols,
-                          int blk, int stride, int off) {
+                          int blk, int stride, int off, int tiled) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   checksum_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint16_t*>(src), n, out_dev, cols, blk, stride,
-                                              off);
+                                              off, tiled);
+  return cudaGetLastError();
+}
+
+// canonical row-major tensor -> its placement (interleaved rows, tiled blocks);
+// reads are coalesced, writes land in 128-byte runs
+__global__ void relayout_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, int64_t n, int64_t cols,
+                                int blk, int stride, int off, int tiled) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[phys_index(i, cols, blk, stride, off, tiled)] = src[i];
+}
+// 8 elements (16 bytes) per thread: 8 consecutive columns stay consecutive in
+// every placement when cols % 8 == 0 (a 64-column block holds whole groups)
+__global__ void relayout8_kernel(const uint4* __restrict__ src, uint16_t* __restrict__ dst, int64_t n8, int64_t cols,
+                                 int blk, int stride, int off, int tiled) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n8; j += (int64_t)gridDim.x * blockDim.x)
+    *reinterpret_cast<uint4*>(dst + phys_index(8 * j, cols, blk, stride, off, tiled)) = src[j];
+}
+
+cudaError_t relayout_bf16(const void* src, void* dst, int64_t n, int64_t cols, int blk, int stride, int off, int tiled,
+                          cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const bool vec = n % 8 == 0 && cols % 8 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  const int64_t work = vec ? n / 8 : n;
+  int blocks = (int)((work + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (vec)
+    relayout8_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint16_t*>(dst),
+                                                 n / 8, cols, blk, stride, off, tiled);
+  else
+    relayout_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint16_t*>(src),
+                                                reinterpret_cast<uint16_t*>(dst), n, cols, blk, stride, off, tiled);
   return cudaGetLastError();
 }
 

@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(256, 2)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         float* __restrict__ C, int T, int ldc, int BN, int stages, int k_chunks_total,
                         int chunks_per_split, int tmem_cols, int n_acc, int acc_stride, int num_mp, int num_n,
-                        int units, int nbuf, int xbufs, const ArgmaxArgs am, const PreNorm pn, int K) {
+                        int units, int nbuf, int xbufs, const ArgmaxArgs am, const PreNorm pn, int K,
+                        int w_tiled) {
   constexpr int mode = MODE, kcs = KCS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -189,10 +190,16 @@ __global__ void __launch_bounds__(256, 2)
       int m0, n0, kc0, nk;
       coords(u, m0, n0, kc0, nk);
       auto load_a = [&](int s, int i) {
-        if (CG == 2)
+        if (w_tiled) {  // one contiguous 16 KB block of the tiled weights
+          if (CG == 2)
+            tma_load_4d_2sm(sA + (size_t)s * GEMM_A_BYTES, &tmW, kc0 + i, m0 / GEMM_BM, &full[s]);
+          else
+            tma_load_4d(sA + (size_t)s * GEMM_A_BYTES, &tmW, kc0 + i, m0 / GEMM_BM, &full[s]);
+        } else if (CG == 2) {
           tma_load_2d_2sm(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
-        else
+        } else {
           tma_load_2d(sA + (size_t)s * GEMM_A_BYTES, &tmW, (kc0 + i) * GEMM_BK, m0, &full[s]);
+        }
       };
       auto load_b = [&](int s, int i) {
         if (CG == 2)
@@ -246,10 +253,16 @@ __global__ void __launch_bounds__(256, 2)
         const int s = it % stages;
         if (it >= stages) mbar_wait(&empty[s], ((it / stages) - 1) & 1);
         if (leader) mbar_expect_tx(&full[s], tx);
-        if (CG == 2)
+        if (is_w && w_tiled) {
+          if (CG == 2)
+            tma_load_4d_2sm(base + (size_t)s * sbytes, tm, kc0 + i, row / GEMM_BM, &full[s]);
+          else
+            tma_load_4d(base + (size_t)s * sbytes, tm, kc0 + i, row / GEMM_BM, &full[s]);
+        } else if (CG == 2) {
           tma_load_3d_2sm(base + (size_t)s * sbytes, tm, row, (kc0 + i), &full[s]);
-        else
+        } else {
           tma_load_3d(base + (size_t)s * sbytes, tm, row, (kc0 + i), &full[s]);
+        }
       }
     }
   } else if (warp == 1 && lane == 0 && leader) {
@@ -481,9 +494,25 @@ static EncodeTiledFn get_encode_fn() {
 // Row-major bf16 [rows, cols] matrix viewed as (64, rows, cols/64) with
 // strides (2 cols, row pitch, 128 B): box (64, box_rows, kc) = kc consecutive
 // k-chunks of box_rows rows, 128-byte swizzle.
-static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc) {
+static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc,
+                      int tiled = 0) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
+  if (tiled) {
+    // tiled weights [rows/128][cols/64][128][64] (the engine's layout)
+    // viewed as (64, 128, cols/64, rows/128): box (64, 128, kc, 1) is kc
+    // consecutive 16 KB blocks of global memory, the same shared-memory image
+    // as the row-major box
+    if (box_rows != 128 || rows % 128 || cols % GEMM_BK) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)GEMM_BK, 128, (cuuint64_t)(cols / GEMM_BK), (cuuint64_t)(rows / 128)};
+    cuuint64_t strides[3] = {(cuuint64_t)GEMM_BK * 2, (cuuint64_t)128 * GEMM_BK * 2,
+                             (cuuint64_t)(cols / GEMM_BK) * 128 * GEMM_BK * 2};
+    cuuint32_t box[4] = {(cuuint32_t)GEMM_BK, 128, (cuuint32_t)kc, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   if (kc == 1) {  // 2-D [rows, cols], box [box_rows, 64]
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
@@ -506,29 +535,30 @@ static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
 struct TmapKey {
   const void* p;
   int64_t rows, cols;
-  int box, kc;
+  int box, kc, tiled;
   bool operator==(const TmapKey& o) const {
-    return p == o.p && rows == o.rows && cols == o.cols && box == o.box && kc == o.kc;
+    return p == o.p && rows == o.rows && cols == o.cols && box == o.box && kc == o.kc && tiled == o.tiled;
   }
 };
 struct TmapKeyHash {
   size_t operator()(const TmapKey& k) const {
     return std::hash<const void*>()(k.p) ^ (size_t)(k.rows * 1315423911u) ^ (size_t)(k.cols * 2654435761u) ^
-           (size_t)k.box ^ ((size_t)k.kc << 20);
+           (size_t)k.box ^ ((size_t)k.kc << 20) ^ ((size_t)k.tiled << 28);
   }
 };
 
-static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc) {
+static bool cached_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int box_rows, int kc,
+                        int tiled = 0) {
   static std::mutex mu;
   static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
-  TmapKey k{ptr, rows, cols, box_rows, kc};
+  TmapKey k{ptr, rows, cols, box_rows, kc, tiled};
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(k);
   if (it != cache.end()) {
     *out = it->second;
     return true;
   }
-  if (!make_tmap(out, ptr, rows, cols, box_rows, kc)) return false;
+  if (!make_tmap(out, ptr, rows, cols, box_rows, kc, tiled)) return false;
   if (cache.size() > 4096) cache.clear();
   cache.emplace(k, *out);
   return true;
@@ -627,7 +657,7 @@ static cudaError_t launch_gemm(Kern kern, int cg, dim3 grid, size_t smem, cudaSt
 }
 
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
-                      cudaStream_t stream, const ArgmaxArgs* am, const PreNorm* pn) {
+                      cudaStream_t stream, const ArgmaxArgs* am, const PreNorm* pn, int w_tiled) {
   if (T <= 0) return cudaSuccess;
   if (N % GEMM_BM != 0 || K % GEMM_BK != 0) return cudaErrorInvalidValue;
   // SGS_GEMM_BN_CAP (experiments, tools/gemm_explore.py): largest token tile
@@ -661,7 +691,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   per = (per + kcs - 1) / kcs * kcs;  // every split covers whole stages
   splits = (kc + per - 1) / per;      // every split has >= 1 chunk
   CUtensorMap tw, tx;
-  if (!cached_tmap(&tw, W, N, K, GEMM_BM, kcs)) return cudaErrorInvalidValue;
+  if (!cached_tmap(&tw, W, N, K, GEMM_BM, kcs, w_tiled)) return cudaErrorInvalidValue;
   if (!cached_tmap(&tx, X, T, K, BN / CG, kcs)) return cudaErrorInvalidValue;
   const int stage_bytes = kcs * (GEMM_A_BYTES + (BN / CG) * GEMM_BK * 2);
   int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
@@ -705,7 +735,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
 #define SGS_GEMM_CASE(cg, md, kk)                                                                                     \
   case (cg - 1) * 10 + md * 2 + (kk - 1):                                                                           \
     return launch_gemm(gemm_bf16_tc_kernel<cg, md, kk>, cg, grid, smem, stream, tw, tx, C, T, ldc, BN, stages, kc, \
-                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs, amv, pnv, K);
+                       per, tmem_cols, n_acc, acc_stride, num_mp, num_n, units, nbuf, xbufs, amv, pnv, K, w_tiled);
     SGS_GEMM_CASE(1, 0, 1) SGS_GEMM_CASE(1, 0, 2) SGS_GEMM_CASE(1, 1, 1) SGS_GEMM_CASE(1, 1, 2)
     SGS_GEMM_CASE(1, 2, 1) SGS_GEMM_CASE(1, 2, 2) SGS_GEMM_CASE(1, 3, 1) SGS_GEMM_CASE(1, 3, 2)
     SGS_GEMM_CASE(1, 4, 1) SGS_GEMM_CASE(1, 4, 2)

@@ -46,7 +46,8 @@ struct PreNorm {
   const int32_t* parity;     // device int: launch parity of this site (read after griddepcontrol.wait)
 };
 cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int T, int ldc, int mode, int splits,
-                      cudaStream_t stream, const ArgmaxArgs* am = nullptr, const PreNorm* pn = nullptr);
+                      cudaStream_t stream, const ArgmaxArgs* am = nullptr, const PreNorm* pn = nullptr,
+                      int w_tiled = 0);  // 1: W in the tiled layout [N/128][K/64][128][64] (weight_layout below)
 int gemm_auto_splits(int N, int K, int T);
 
 // ---- decode attention (attention.cu)
@@ -125,8 +126,16 @@ cudaError_t sample_top_p(const float* logits, int rows, int V, float temperature
 struct ShardMap {
   int64_t src_cols = 0, row0 = 0, col0 = 0, lcols = 1;
 };
+// Weight placement: element i = (r, c) of a row-major [n / cols, cols] tensor
+// lands at row R = (r / blk) * stride + off + r % blk of its fused matrix
+// (blk = 0: R = r; the interleaved gate/up rows), and, with tiled = 1, in the
+// GEMM weight layout [R/128][cols/64][128][64] (16 KB blocks, one TMA box each).
 cudaError_t hash_init(void* dst, uint64_t seed, uint64_t tensor_id, int64_t n, int is_norm, cudaStream_t stream,
-                      int64_t cols = 1, int blk = 0, int stride = 0, int off = 0, ShardMap sm = ShardMap{});
+                      int64_t cols = 1, int blk = 0, int stride = 0, int off = 0, ShardMap sm = ShardMap{},
+                      int tiled = 0);
+// dst[placement(i)] = src[i] for a canonical row-major bf16 tensor readable by the device
+cudaError_t relayout_bf16(const void* src, void* dst, int64_t n, int64_t cols, int blk, int stride, int off, int tiled,
+                          cudaStream_t stream);
 cudaError_t argmax_keys_finalize(unsigned long long* keys, int rows, const int32_t* slot, const int32_t* tok_idx,
                                  int32_t* last_tok, int32_t* hist, int max_gen, cudaStream_t stream);
 // ---- NEXT-2 tensor-parallel exchange over NVLink peer memory (tp_comm.cu)
@@ -145,7 +154,7 @@ cudaError_t tp_argmax_exchange(unsigned long long* keys, int rows, const int32_t
                                int32_t* last_tok, int32_t* hist, int max_gen, const TpPeers& P, int rows_cap, int d,
                                const int32_t* launch, int index, int per_launch, cudaStream_t stream);
 cudaError_t checksum_bf16(const void* src, int64_t n, unsigned long long* out_dev, cudaStream_t stream,
-                          int64_t cols = 1, int blk = 0, int stride = 0, int off = 0);
+                          int64_t cols = 1, int blk = 0, int stride = 0, int off = 0, int tiled = 0);
 cudaError_t apply_bt_deltas(int32_t* block_table, int max_pages, const int32_t* deltas, int n, cudaStream_t stream,
                             int32_t* last_tok = nullptr);
 cudaError_t copy_kv_pages(void* pool, int64_t layer_stride, int64_t page_bytes, int n_layers, const int32_t* pairs,
