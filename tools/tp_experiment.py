@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--b", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32, 64, 128, 256])
     ap.add_argument("--prompts", type=int, default=1024)
     ap.add_argument("--alpha-pct", type=int, default=20)
+    ap.add_argument("--phases", default="A_tp2_tail,B_dp4_round_robin")
     ap.add_argument("--ar", nargs="*", default=["p2p", "nccl"], choices=["p2p", "nccl"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -90,7 +91,7 @@ def main():
         n_tail = a.alpha_pct * len(tr) // 100
         tail, reg = tr.subset(order[:n_tail]), tr.subset(order[n_tail:])
         res = {}
-        for phase in ("A_tp2_tail", "B_dp4_round_robin"):
+        for phase in a.phases.split(","):
             torch.cuda.empty_cache()
             if phase.startswith("A"):
                 if rank < 2:
