@@ -358,7 +358,7 @@ sgs_status Engine::init(const sgs_model_cfg& m_full, const sgs_engine_cfg& e, co
   }
   // GEMM weight layout: tiled 16 KB blocks (one contiguous TMA box each) or
   // row-major (SGS_WEIGHT_LAYOUT=rows)
-  if (const char* wl = std::getenv("SGS_WEIGHT_LAYOUT")) w_tiled_ = std::string(wl) == "tiles" ? 1 : 0;
+  if (const char* wl = std::getenv("SGS_WEIGHT_LAYOUT")) w_tiled_ = std::string(wl) == "rows" ? 0 : 1;
   build_tensor_table();
   sgs_status s = w ? load_weights(w, arena_, st_) : load_weights_seed(e.weight_seed);
   if (s != SGS_OK) return s;

@@ -21,7 +21,7 @@ __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvt
 
 __global__ void __launch_bounds__(96) tma_stream(const __grid_constant__ CUtensorMap tm, int stages, int iters,
                                                  int box_rows, int mode, int rows_total, unsigned long long* sink,
-                                                 int kc, int producers) {
+                                                 int kc, int producers, const void* gbase) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int box_bytes = box_rows * 128 * kc;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(96) tma_stream(const __grid_constant__ CUtenso
       // mode 0: CTA-private row bands (distinct data, HBM); mode 1: 2 MB shared window (L2)
       const int kt = 64 / kc;  // boxes per row band (K = 4096 = 64 chunks)
       int x, y;
-      if (mode == 0 || mode == 2) {
+      if (mode == 0 || mode >= 2) {
         const int band = (blockIdx.x * 3 + i / kt) % row_tiles;
         x = (i % kt) * kc, y = band * box_rows;
       } else {
@@ -61,7 +61,15 @@ __global__ void __launch_bounds__(96) tma_stream(const __grid_constant__ CUtenso
         const int t = (blockIdx.x * 7 + i) % win;
         x = (t % kt) * kc, y = (t / kt) * box_rows;
       }
-      if (mode == 2)
+      if (mode == 3) {  // 1-D bulk copy of the same contiguous block (no tensor map, no swizzle)
+        const uint8_t* g = reinterpret_cast<const uint8_t*>(gbase) +
+                           ((size_t)(y / box_rows) * (4096 / 64) + x) * (size_t)(box_rows * 128);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                su32(smem + (size_t)s * box_bytes)),
+            "l"(g), "r"(box_bytes), "r"(su32(&full[s]))
+            : "memory");
+      } else if (mode == 2)
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
             "[%2];" ::"r"(su32(smem + (size_t)s * box_bytes)),
@@ -116,7 +124,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&b);
   struct Cfg { int mode, box_rows, kc, per_sm, stages, producers; };
   std::vector<Cfg> cfgs;
-  for (int mode : {0, 1, 2})
+  for (int mode : {0, 1, 2, 3})
     for (int box_rows : {128, 256})
       for (int kc : {1, 2, 4})
         for (int per_sm : {1, 2})
@@ -129,7 +137,7 @@ int main(int argc, char** argv) {
     if (tiled_only && c.mode == 1) continue;
     CUtensorMap tm;
     CUresult er;
-    if (c.mode == 2) {  // [rows / R][K / 64][R][64]: one contiguous block per box
+    if (c.mode >= 2) {  // [rows / R][K / 64][R][64]: one contiguous block per box
       const cuuint64_t R = (cuuint64_t)c.box_rows;
       cuuint64_t dims[4] = {64, R, (cuuint64_t)(K / 64), (cuuint64_t)rows / R};
       cuuint64_t strides[3] = {128, R * 128, (cuuint64_t)(K / 64) * R * 128};
@@ -154,7 +162,7 @@ int main(int argc, char** argv) {
     float best = 1e30f;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
-      tma_stream<<<grid, 96, smem>>>(tm, c.stages, iters, c.box_rows, c.mode, rows, sink, c.kc, c.producers);
+      tma_stream<<<grid, 96, smem>>>(tm, c.stages, iters, c.box_rows, c.mode, rows, sink, c.kc, c.producers, buf);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms = 0;
@@ -164,7 +172,7 @@ int main(int argc, char** argv) {
     const double bytes = (double)grid * iters * box_bytes;
     printf("{\"mode\": \"%s\", \"box_KB\": %d, \"box_rows\": %d, \"kc\": %d, \"ctas_per_sm\": %d, \"producers\": %d, "
            "\"stages\": %d, \"GBs\": %.1f, \"GBs_per_sm\": %.1f}\n",
-           c.mode == 0 ? "hbm" : c.mode == 1 ? "l2" : "hbm_tiled", box_bytes / 1024, c.box_rows, c.kc, c.per_sm, c.producers, c.stages,
+           c.mode == 0 ? "hbm" : c.mode == 1 ? "l2" : c.mode == 2 ? "hbm_tiled" : "hbm_bulk1d", box_bytes / 1024, c.box_rows, c.kc, c.per_sm, c.producers, c.stages,
            bytes / best / 1e6, bytes / best / 1e6 / sms);
     fflush(stdout);
   }
