@@ -11,6 +11,7 @@ Functions and the paper passages they follow (PAPER.md line numbers):
   tb_fit/T_ps      C3  piecewise-linear T(b), hinge fit
   min_merge_gain   C3  lemma T(x+y) < T(x)+T(y)
   elastic_plan     NEXT-4 delta vs delta' (one more DP unit)
+  tp_tail_plan     NEXT-2 long tail on a TP instance (R27)
   brute_force      C4  LF vs all admission orders
   attention        C7  naive softmax attention, fp64
   decoder_layer/head  C6  one layer / final norm + LM head    (chained layer-local parity)
@@ -80,6 +81,11 @@ def _declare(L):
                                       ctypes.c_int32, ctypes.c_int64, P_i64, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, ctypes.c_int64, P_i64]
     L.oracle_elastic_plan.restype = ctypes.c_int32
+    L.oracle_tp_tail_plan.argtypes = [ctypes.c_int32, P_i64, P_i32, P_i32, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_int64, P_i64, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                      P_i64, P_i64]
+    L.oracle_tp_tail_plan.restype = ctypes.c_int32
     L.oracle_nearest_rank.argtypes = [ctypes.c_int32, P_i64, ctypes.c_int32]
     L.oracle_nearest_rank.restype = ctypes.c_int64
     L.oracle_T_ps.argtypes = [P_i64, ctypes.c_int64, P_i64]
@@ -253,6 +259,22 @@ def elastic_plan(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profi
                                     _p(out, P_i64))
     return dict(t_gen_ps=(_i128(out[0], out[1]), _i128(out[2], out[3])), delta_prime_ps=_i128(out[4], out[5]),
                 scale_out=bool(dec))
+
+
+def tp_tail_plan(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profile, tp_size: int, tp_B: int,
+                 tp_pool_pages: int, tp_profile, policy="round_robin", alpha_pct=20, score_max=0, tail_ceil=0):
+    """NEXT-2 two-dimensional dispatch (reading R27): k longest to one TP instance, predicted times."""
+    n = len(ids)
+    ids = np.ascontiguousarray(ids, np.int64)
+    P = np.ascontiguousarray(P, np.int32)
+    hint = np.ascontiguousarray(hint, np.int32)
+    out = np.zeros(6, np.int64)
+    k = lib().oracle_tp_tail_plan(n, _p(ids, P_i64), _p(P, P_i32), _p(hint, P_i32), N, B, page, pool_pages,
+                                  _p(_prof(profile), P_i64), alpha_pct, score_max, tail_ceil,
+                                  {"skew": 0, "round_robin": 1}[policy], tp_size, tp_B, tp_pool_pages,
+                                  _p(_prof(tp_profile), P_i64), _p(out, P_i64))
+    return dict(n_tail=int(k), t_tp_ps=_i128(out[0], out[1]), t_dp_ps=_i128(out[2], out[3]),
+                t_all_ps=_i128(out[4], out[5]))
 
 
 def nearest_rank(v, q_pct):

@@ -74,6 +74,13 @@ struct ElasticOut {
 };
 __int128 predicted_generation_ps(const DispatchIn& in);
 ElasticOut elastic_plan(const DispatchIn& in, __int128 delta_ps);
+// NEXT-2 two-dimensional dispatch (R27); policy of the DP side: 0 Alg. 2, 1 round robin
+struct TailPlanOut {
+  int n_tail = 0;
+  __int128 t_tp = 0, t_dp = 0, t_all = 0;
+};
+TailPlanOut tp_tail_plan(const DispatchIn& dp, int dp_policy, int tp_size, int tp_B, int64_t tp_pool_pages,
+                         const Profile& tp_prof);
 int64_t nearest_rank(std::vector<int64_t> v, int q_pct);
 
 // ---------------------------------------------------------------------------

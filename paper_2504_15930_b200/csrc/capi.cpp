@@ -307,6 +307,24 @@ sgs_status sgs_elastic_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* 
   return SGS_OK;
 }
 
+sgs_status sgs_tp_tail_plan(const sgs_engine_cfg* e, int64_t pool_pages, int32_t tp_size, int32_t tp_max_batch,
+                            int64_t tp_pool_pages, const sgs_tb_profile* tp_profile, int32_t n, const uint64_t* ids,
+                            const int32_t* prompt_len, const int32_t* hint, int32_t* n_tail, int64_t t_ps[3]) {
+  if (!e || !tp_profile || n < 0 || (n > 0 && (!ids || !prompt_len || !hint)) || e->n_instances < 1 ||
+      pool_pages < 1 || e->max_batch < 1 || e->page_size < 1 || tp_size < 1 || tp_max_batch < 1 || tp_pool_pages < 1)
+    return SGS_E_INVAL;
+  sgs::DispatchCfg dp{e->n_instances, e->max_batch, e->page_size, pool_pages, e->profile.t0_ns, e->profile.k0_ps,
+                      e->profile.b_star, e->profile.k1_ps, e->alpha_pct, e->score, e->tail_ceil, e->dispatch,
+                      e->sample_seed};
+  sgs::DispatchCfg tp{1, tp_max_batch, e->page_size, tp_pool_pages, tp_profile->t0_ns, tp_profile->k0_ps,
+                      tp_profile->b_star, tp_profile->k1_ps, e->alpha_pct, e->score, e->tail_ceil, e->dispatch,
+                      e->sample_seed};
+  const sgs::TailPlan p = sgs::tp_tail_plan(dp, tp, tp_size, n, ids, prompt_len, hint);
+  if (n_tail) *n_tail = p.n_tail;
+  if (t_ps) t_ps[0] = (int64_t)p.t_tp, t_ps[1] = (int64_t)p.t_dp, t_ps[2] = (int64_t)p.t_all;
+  return SGS_OK;
+}
+
 sgs_status sgs_set_instances(sgs_handle* h, int32_t n_instances, int32_t instance_rank) {
   if (!h || n_instances < 1 || instance_rank < 0 || instance_rank >= n_instances) return SGS_E_INVAL;
   return h->eng.set_instances(n_instances, instance_rank);

@@ -363,6 +363,50 @@ __int128 predicted_generation_ps(const DispatchCfg& c, int n, const uint64_t* id
   return makespan;
 }
 
+// ------------------------------------------------------------------ NEXT-2 two-dimensional dispatch
+TailPlan tp_tail_plan(const DispatchCfg& c_dp, const DispatchCfg& c_tp, int tp_size, int n, const uint64_t* ids,
+                      const int32_t* P, const int32_t* hint) {
+  std::vector<int32_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    if (hint[a] != hint[b]) return hint[a] > hint[b];
+    return ids[a] < ids[b];
+  });
+  std::vector<uint64_t> sid(n);
+  std::vector<int32_t> sP(n), sh(n);
+  for (int j = 0; j < n; ++j) sid[j] = ids[order[j]], sP[j] = P[order[j]], sh[j] = hint[order[j]];
+  DispatchCfg tp1 = c_tp;
+  tp1.N = 1;
+  // predicted times of the split at k (the sorted prefix [0, k) to the TP instance)
+  auto times = [&](int k, __int128* t_tp, __int128* t_dp) {
+    *t_tp = k > 0 ? predicted_generation_ps(tp1, k, sid.data(), sP.data(), sh.data()) : 0;
+    *t_dp = k < n ? predicted_generation_ps(c_dp, n - k, sid.data() + k, sP.data() + k, sh.data() + k) : 0;
+  };
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) / 2;
+    __int128 a, b;
+    times(mid, &a, &b);
+    if (a >= b)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  TailPlan out;
+  __int128 a, b;
+  times(lo, &a, &b);
+  out.n_tail = lo, out.t_tp = a, out.t_dp = b;
+  if (lo > 0) {
+    __int128 a2, b2;
+    times(lo - 1, &a2, &b2);
+    if (std::max(a2, b2) <= std::max(a, b)) out.n_tail = lo - 1, out.t_tp = a2, out.t_dp = b2;
+  }
+  DispatchCfg all = c_dp;
+  all.N = c_dp.N + tp_size;
+  out.t_all = n > 0 ? predicted_generation_ps(all, n, ids, P, hint) : 0;
+  return out;
+}
+
 // ------------------------------------------------------------------ T(b) fit
 // Least squares on the hinge basis [1, b, (b - b*)+] for every measured b* with
 // >= 2 distinct points at or below and >= 1 above; minimum SSE wins, ties ->

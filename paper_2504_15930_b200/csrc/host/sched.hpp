@@ -121,6 +121,21 @@ int dispatch_alg2(const DispatchCfg& c, int n, const uint64_t* ids, const int32_
 __int128 predicted_generation_ps(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P,
                                  const int32_t* hint);
 
+// ------------------------------------------------------------------ NEXT-2 two-dimensional dispatch
+// The longest k samples (hint descending, id ascending -- the long tail the
+// ranker identifies) go to one tensor-parallel instance, the rest to the DP
+// instances with c_dp's policy (R27):
+//   T_tp(k) = predicted_generation_ps(c_tp [N = 1], top k),  T_dp(k) = that of c_dp, the rest,
+// k = the smallest k with T_tp(k) >= T_dp(k) (binary search over [0, n]) or
+// k - 1, whichever has the smaller max(T_tp, T_dp) (ties: the smaller k);
+// t_all = all samples on c_dp.N + tp_size DP instances.  Returns k.
+struct TailPlan {
+  int n_tail = 0;
+  __int128 t_tp = 0, t_dp = 0, t_all = 0;
+};
+TailPlan tp_tail_plan(const DispatchCfg& c_dp, const DispatchCfg& c_tp, int tp_size, int n, const uint64_t* ids,
+                      const int32_t* P, const int32_t* hint);
+
 // ------------------------------------------------------------------ T(b) fit
 bool fit_tb(int n, const double* b, const double* T_ns, double out[5], int64_t* b_star, int64_t prof[4]);
 

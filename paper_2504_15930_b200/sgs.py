@@ -38,6 +38,7 @@ EXPORTS = [
     "sgs_set_roofline", "sgs_kernel_roofline_ms", "sgs_iter_log", "sgs_debug_layer", "sgs_op_sample_top_p",
     "sgs_weight_tensors", "sgs_stage_weights", "sgs_prefill_workspace_bytes", "sgs_host_state",
     "sgs_op_decode_attention_timed", "sgs_elastic_plan", "sgs_set_instances", "sgs_tp_comm_init",
+    "sgs_tp_tail_plan",
 ]
 
 
@@ -107,6 +108,8 @@ def _declare(L):
     L.sgs_host_state.argtypes = [vp, P(i64), P(i64), P(i64)]
     L.sgs_elastic_plan.argtypes = [P(EngineCfg), i32, P(u64), P(i32), P(i32), i64, i64, P(i64), P(i64), P(i32)]
     L.sgs_set_instances.argtypes = [vp, i32, i32]
+    L.sgs_tp_tail_plan.argtypes = [P(EngineCfg), i64, i32, i32, i64, P(TbProfile), i32, P(u64), P(i32), P(i32), P(i32),
+                                   P(i64)]
     L.sgs_tp_comm_init.argtypes = [vp, P(ctypes.c_uint8)]
     L.sgs_prefill_workspace_bytes.argtypes = [i32, i32, i32, i32]
     L.sgs_prefill_workspace_bytes.restype = i64
@@ -534,6 +537,28 @@ def elastic_plan(ids, prompt_len, hint, n_instances, max_batch, page, pool_pages
                                   _i32p(h), pool_pages, int(delta_ps), t.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                   ctypes.byref(dp), ctypes.byref(so)))
     return dict(t_gen_ps=(int(t[0]), int(t[1])), delta_prime_ps=dp.value, scale_out=bool(so.value))
+
+
+def tp_tail_plan(ids, prompt_len, hint, n_dp, max_batch, page, pool_pages, profile, tp_size, tp_max_batch,
+                 tp_pool_pages, tp_profile, dispatch="round_robin", alpha_pct=20, score=0, tail_ceil=0):
+    """NEXT-2 two-dimensional dispatch (R27): how many of the longest samples go to one
+    tensor-parallel instance; predicted ps of the TP instance, of the DP instances, and of DP only."""
+    e = EngineCfg()
+    e.n_instances, e.max_batch, e.page_size = n_dp, max_batch, page
+    e.profile = TbProfile(*profile)
+    e.alpha_pct, e.score, e.tail_ceil, e.dispatch = alpha_pct, score, tail_ceil, DISPATCH[dispatch]
+    tpp = TbProfile(*tp_profile)
+    n = len(ids)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    P = np.ascontiguousarray(prompt_len, np.int32)
+    h = np.ascontiguousarray(hint, np.int32)
+    t = np.zeros(3, np.int64)
+    k = ctypes.c_int32()
+    _check(lib().sgs_tp_tail_plan(ctypes.byref(e), pool_pages, tp_size, tp_max_batch, tp_pool_pages, ctypes.byref(tpp),
+                                  n, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _i32p(P), _i32p(h),
+                                  ctypes.byref(k), t.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+    return dict(n_tail=k.value, t_tp_ps=int(t[0]), t_dp_ps=int(t[1]), t_all_ps=int(t[2]),
+                use_tp=bool(max(t[0], t[1]) < t[2]))
 
 
 def rope_table(max_pos: int, hd: int, theta: float) -> np.ndarray:

@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--ctx", type=int, default=2048)
     ap.add_argument("--b", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32, 64, 128, 256])
     ap.add_argument("--prompts", type=int, default=1024)
-    ap.add_argument("--alpha-pct", type=int, default=20)
+    ap.add_argument("--alpha-pct", type=int, default=20, help="< 0: sgs_tp_tail_plan chooses the split")
     ap.add_argument("--phases", default="A_tp2_tail,B_dp4_round_robin")
     ap.add_argument("--ar", nargs="*", default=["p2p", "nccl"], choices=["p2p", "nccl"])
     ap.add_argument("--out", default=None)
@@ -88,7 +88,24 @@ def main():
         assert world == 4
         tr = workload.make_trace(a.prompts, 512, 1024, 1.0, 8192, shape.vocab, seed=1234)
         order = sorted(range(len(tr)), key=lambda i: (-int(tr.hint[i]), int(tr.ids[i])))
-        n_tail = a.alpha_pct * len(tr) // 100
+        if a.alpha_pct >= 0:
+            n_tail = a.alpha_pct * len(tr) // 100
+        else:
+            # two-dimensional dispatch (sgs_tp_tail_plan, R27) with T(b) fits of the committed ctx-2048
+            # sweeps: one GPU (tiled weights) for the DP side, the TP = 2 pair (peer-memory exchange)
+            def fit(path, keep=lambda p: True):
+                pts = [p for p in json.load(open(os.path.join(ROOT, path)))["points"] if keep(p)]
+                return tuple(sgs.fit_profile(np.array([p["b"] for p in pts], float),
+                                             np.array([p.get("T_us", p.get("T_us_tp2")) * 1e3 for p in pts],
+                                                      float))["profile"])
+            dp_prof = fit("profiles/r02/tb_layout_tiles.json")
+            tp_prof = fit("profiles/r02/tp/tp2_sweep_ll_ctx2048.json", lambda p: p.get("exchange") == "p2p")
+            plan = sgs.tp_tail_plan(tr.ids, tr.prompt_len, tr.hint, 2, 256, 16, 150000, dp_prof, 2, 256, 300000,
+                                    tp_prof, dispatch="round_robin")
+            n_tail = plan["n_tail"]
+            out["plan"] = {**plan, "dp_profile": dp_prof, "tp_profile": tp_prof}
+            if rank == 0:
+                print(json.dumps({"plan": out["plan"]}), flush=True)
         tail, reg = tr.subset(order[:n_tail]), tr.subset(order[n_tail:])
         res = {}
         for phase in a.phases.split(","):
@@ -133,6 +150,7 @@ def main():
             del inst
             dist.barrier()
         out["alpha_pct"] = a.alpha_pct
+        out["n_tail"] = n_tail
         out["results"] = res
     if rank == 0 and a.out:
         json.dump(out, open(a.out, "w"), indent=1)
