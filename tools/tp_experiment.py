@@ -49,19 +49,19 @@ def main():
     out = {"mode": a.mode, "model": a.model}
 
     def tp_pair(ranks, **kw):
-        """A TP = 2 instance over `ranks` (this rank must be in it)."""
+        """A TP = len(ranks) instance over `ranks` (this rank must be in it)."""
         r = ranks.index(rank)
-        inst = sgs.Instance(shape, kw.pop("B"), kw.pop("max_ctx"), device=rank, tp_size=2, tp_rank=r, trace=False,
-                            **kw)
+        inst = sgs.Instance(shape, kw.pop("B"), kw.pop("max_ctx"), device=rank, tp_size=len(ranks), tp_rank=r,
+                            trace=False, **kw)
         return inst
 
     if a.mode == "sweep":
-        assert world == 2
+        assert world in (2, 4)
         pts, nid = [], 0
         for ar in a.ar:
             # exchange of the partials: NVLink peer memory (tp_comm.cu) or NCCL all-reduces
             os.environ["SGS_TP_NCCL_AR"] = "1" if ar == "nccl" else "0"
-            inst = tp_pair([0, 1], B=max(a.b), max_ctx=a.ctx + 16, weight_seed=5, flags=sgs.sgs.F_SKIP_PREFILL,
+            inst = tp_pair(list(range(world)), B=max(a.b), max_ctx=a.ctx + 16, weight_seed=5, flags=sgs.sgs.F_SKIP_PREFILL,
                            max_prefill_tokens=max(16384, a.ctx))
             uid = [sgs.comm_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
@@ -76,7 +76,7 @@ def main():
                 dec = log[(log[:, 3] == 0) & (log[:, 1] == b)]
                 t = torch.tensor([float(np.median(dec[:, 5])) if len(dec) else 0.0], dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                pts.append({"b": b, "ctx": a.ctx, "exchange": ar, "T_us_tp2": float(t[0])})
+                pts.append({"b": b, "ctx": a.ctx, "exchange": ar, "tp": world, "T_us_tp2": float(t[0])})
                 if rank == 0:
                     print(json.dumps(pts[-1]), flush=True)
             inst.close()
