@@ -247,6 +247,7 @@ CLASS_DESC = {0: "decode attention (K1+K2, paged split-K, merge in-kernel)",
               2: "prefill attention (causal)", 4: "prefill tcgen05 GEMMs",
               5: "decode RMSNorm / RoPE+append / embedding / sampler"}
 NCU_WINDOW = os.path.join(ROOT, "profiles", "r02_ncu_windows.json")
+TIMELINE_REF = os.path.join(ROOT, "profiles", "r02", "bench_timeline_shares.json")
 
 
 def kernel_roofline(inst, stats, peaks, n_iters, dev_s):
@@ -410,7 +411,9 @@ def main():
     ap.add_argument("--strong", action="store_true", help="fixed global batch (cfg.n_prompts) instead of per GPU")
     ap.add_argument("--profile", default=None, help="T(b) profile t0_ns,k0_ps,b_star,k1_ps for Alg. 2")
     ap.add_argument("--hint-noise", type=float, default=None, help="ranker noise sigma (None: oracle hints)")
-    ap.add_argument("--no-timeline", action="store_true", help="skip the CUPTI timeline batch after the timed steps")
+    ap.add_argument("--timeline", action="store_true",
+                    help="one more batch under CUPTI (torch.profiler) for uninstrumented class shares; default: "
+                         "the committed shares of such a run (profiles/r02/bench_timeline_shares.json)")
     ap.add_argument("--group-size", type=int, default=1, help="GRPO-style groups: samples per prompt (NEXT-3)")
     ap.add_argument("--prefix-sharing", action="store_true", help="SGS_F_PREFIX_SHARING (NEXT-3, reading R26)")
     args = ap.parse_args()
@@ -574,9 +577,14 @@ def main():
         "clocks": clk.summary(),
     }
     note(f"timed steps done: {line['value']} tok/s")
-    if not args.no_timeline and world == 1 and kernels is not None:
+    if args.timeline and world == 1 and kernels is not None:
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ.get("SGS_BENCH_STACK_DUMP_S", "600")), exit=False)
         kernels["_timeline"] = timeline_shares(inst, sgs, make_batch(args.warmup + args.steps), cfg, shape)
+        faulthandler.cancel_dump_traceback_later()
         note("timeline batch done")
+    elif kernels is not None and os.path.exists(TIMELINE_REF):
+        kernels["_timeline"] = {**json.load(open(TIMELINE_REF)), "source": os.path.relpath(TIMELINE_REF, ROOT)}
     if not args.no_cpu_baseline:
         cb = cpu_oracle_sample(shape, cfg)
         note("cpu baseline sample done")
