@@ -694,7 +694,12 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   if (!cached_tmap(&tw, W, N, K, GEMM_BM, kcs, w_tiled)) return cudaErrorInvalidValue;
   if (!cached_tmap(&tx, X, T, K, BN / CG, kcs)) return cudaErrorInvalidValue;
   const int stage_bytes = kcs * (GEMM_A_BYTES + (BN / CG) * GEMM_BK * 2);
-  int stages = (small ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
+  // experiment (SGS_GEMM_ONE_CTA=<modes bitmask>): decode tiles of the listed
+  // modes with one CTA per SM and the whole shared-memory ring, so a CTA walks
+  // several units and streams the next unit's weights during an epilogue
+  static const int one_cta_modes = std::getenv("SGS_GEMM_ONE_CTA") ? std::atoi(std::getenv("SGS_GEMM_ONE_CTA")) : 0;
+  const bool one_cta = small && CG == 1 && ((one_cta_modes >> mode) & 1) && !pn;
+  int stages = (small && !one_cta ? GEMM_SMEM_BUDGET / 2 : GEMM_SMEM_BUDGET) / stage_bytes;
   if (stages > 12) stages = 12;
   const int kst = kc / kcs;  // stages-worth of chunks in the whole K
   if (stages > kst) stages = kst < 2 ? 2 : kst;
@@ -707,7 +712,7 @@ cudaError_t gemm_bf16(const void* W, const void* X, float* C, int N, int K, int 
   // persistent grid: one CTA (pair) per resident slot, at most one per unit
   const int num_mp = N / GEMM_BM / CG, num_n = (T + BN - 1) / BN;
   const int units = num_mp * num_n * splits;
-  int slots = sm_count() * (small ? 2 : 1) / CG;
+  int slots = sm_count() * (small && !one_cta ? 2 : 1) / CG;
   if (pn) {
     // a PreNorm grid barrier needs every CTA co-resident: never more CTAs than fit
     const int occ = gemm_occupancy(CG, mode, kcs, smem);
