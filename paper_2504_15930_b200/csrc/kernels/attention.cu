@@ -350,11 +350,12 @@ void attn_plan(const int32_t* ctx, const int32_t* slot, int b, int nkv, int page
   for (int i = 0; i < b; ++i) total += (int64_t)((ctx[i] + page - 1) / page) * nkv;
   // One wave of 2 CTAs per SM (296 slots): a (row, kv head) with np pages
   // gets floor(296 np / total) parts, so the items never spill into a second,
-  // nearly empty wave; parts keep >= 2 pages per warp and there are at most
+  // nearly empty wave; parts keep >= 4 pages per warp (measured: 8 pages per part ->
+  // 16 saves ~1% of T(b) at b <= 16, profiles/r02/attn_planner) and there are at most
   // ATTN_SPLIT_CAP of them (the last-arriving CTA merges them serially).
   // SGS_ATTN_SLOTS / SGS_ATTN_MINPG: planner experiments (tools/attn_sweep.py)
   static const int64_t kSlots = std::getenv("SGS_ATTN_SLOTS") ? std::atoll(std::getenv("SGS_ATTN_SLOTS")) : 2 * 148;
-  static const int kMinPg = std::getenv("SGS_ATTN_MINPG") ? std::atoi(std::getenv("SGS_ATTN_MINPG")) : 2 * ATTN_WARPS;
+  static const int kMinPg = std::getenv("SGS_ATTN_MINPG") ? std::atoi(std::getenv("SGS_ATTN_MINPG")) : 4 * ATTN_WARPS;
   constexpr int ATTN_SPLIT_CAP = 32;
   auto cap = [&](int np, int nch) {
     const int by_pages = np / kMinPg;
