@@ -190,7 +190,7 @@ class Engine {
   bool fused_norm_ = false;                   // RMSNorm fused into the decode GEMMs (SGS_FUSED_NORM=1)
   int64_t dec_launch_ = 0;                    // decode-program launches (PreNorm barrier parity)
   int qblk_ = 64;                             // prefill attention query block (128: tcgen05 kernel)
-  int w_tiled_ = 1;                           // GEMM weights tiled [N/128][K/64][128][64] (SGS_WEIGHT_LAYOUT)
+  int w_tiled_ = 0;                           // GEMM weights tiled [N/128][K/64][128][64] (SGS_WEIGHT_LAYOUT)
   // NEXT-2 tensor parallelism: m_ holds this shard's dims (q/kv heads, FFN, vocab
   // rows divided by tp_); the embedding table is the full vocabulary
   int tp_ = 1, tp_rank_ = 0;
