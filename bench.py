@@ -577,7 +577,9 @@ def main():
         "clocks": clk.summary(),
     }
     note(f"timed steps done: {line['value']} tok/s")
-    if args.timeline and world == 1 and kernels is not None:
+    if args.timeline and world == 1:
+        kernels = kernels if kernels is not None else {}
+        line["kernels"] = kernels
         import faulthandler
         faulthandler.dump_traceback_later(float(os.environ.get("SGS_BENCH_STACK_DUMP_S", "600")), exit=False)
         kernels["_timeline"] = timeline_shares(inst, sgs, make_batch(args.warmup + args.steps), cfg, shape)
