@@ -321,6 +321,38 @@ def test_deterministic_paths_bitwise_equal(sgs):
         assert recs == runs["keep"][2], name
 
 
+@pytest.mark.parametrize("model", ["tiny", "qwen2.5-7b"])
+def test_tiled_weight_layout_bitwise_equal(sgs, model, monkeypatch):
+    # SGS_WEIGHT_LAYOUT=tiles changes only where the GEMM weights
+    # live and how TMA fetches them, not the arithmetic: with split-K off
+    # (SGS_F_DETERMINISTIC) the kept logits, tokens and schedules equal the
+    # row-major run bit for bit; the weight checksums (canonical order) agree
+    shape = workload.MODELS[model]
+    n, P, med, cap = (24, 16, 12, 40) if model == "tiny" else (4, 24, 6, 8)
+    tr = workload.make_trace(n, P, med, 1.0, cap, shape.vocab, seed=43)
+    runs = {}
+    for lay in ("rows", "tiles"):
+        monkeypatch.setenv("SGS_WEIGHT_LAYOUT", lay)
+        inst = sgs.Instance(shape, 4, P + cap + 8, device=0, n_pages=64, weight_seed=17,
+                            flags=sgs.sgs.F_KEEP_LOGITS | sgs.sgs.F_DETERMINISTIC)
+        sums = [inst.checksum(t) for t in (1, 16, 17, 22, 23, 24, 25)]
+        inst.submit_trace(tr)
+        rows, comps = [], []
+        while True:
+            q, a = inst.pending()
+            if q == 0 and a == 0:
+                break
+            comps += inst.step()
+            lg, ids, tk = inst.last_logits()
+            rows.append(lg.copy())
+        runs[lay] = (sums, inst.trace(0), sorted((c["id"], tuple(c["tokens"])) for c in comps), rows)
+        inst.close()
+    (s0, t0, c0, r0), (s1, t1, c1, r1) = runs["rows"], runs["tiles"]
+    assert s0 == s1
+    assert np.array_equal(t0, t1) and c0 == c1
+    assert len(r0) == len(r1) and all(np.array_equal(a, b) for a, b in zip(r0, r1))
+
+
 # ------------------------------------------------------------------ chained layer-local parity, every layer
 @pytest.mark.parametrize("model", ["qwen2.5-7b", "qwen2.5-14b", "qwen2.5-32b"])
 def test_chained_layer_parity_every_layer(sgs, model):
