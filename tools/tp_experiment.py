@@ -34,6 +34,10 @@ def main():
     ap.add_argument("--prompts", type=int, default=1024)
     ap.add_argument("--alpha-pct", type=int, default=20, help="< 0: sgs_tp_tail_plan chooses the split")
     ap.add_argument("--phases", default="A_tp2_tail,B_dp4_round_robin")
+    ap.add_argument("--dp-profile-file", default="profiles/r02/tb_layout_tiles.json",
+                    help="T(b) points of one GPU (ctx 2048 used) for the planner's DP side")
+    ap.add_argument("--tp-profile-file", default="profiles/r02/tp/tp2_sweep_ll_ctx2048.json",
+                    help="T(b) points of the TP pair (ctx 2048, p2p exchange) for the planner's TP side")
     ap.add_argument("--ar", nargs="*", default=["p2p", "nccl"], choices=["p2p", "nccl"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -98,8 +102,8 @@ def main():
                 return tuple(sgs.fit_profile(np.array([p["b"] for p in pts], float),
                                              np.array([p.get("T_us", p.get("T_us_tp2")) * 1e3 for p in pts],
                                                       float))["profile"])
-            dp_prof = fit("profiles/r02/tb_layout_tiles.json")
-            tp_prof = fit("profiles/r02/tp/tp2_sweep_ll_ctx2048.json", lambda p: p.get("exchange") == "p2p")
+            dp_prof = fit(a.dp_profile_file, lambda p: p.get("ctx", 2048) == 2048)
+            tp_prof = fit(a.tp_profile_file, lambda p: p.get("exchange") == "p2p" and p.get("ctx", 2048) == 2048)
             plan = sgs.tp_tail_plan(tr.ids, tr.prompt_len, tr.hint, 2, 256, 16, 150000, dp_prof, 2, 256, 300000,
                                     tp_prof, dispatch="round_robin")
             n_tail = plan["n_tail"]
