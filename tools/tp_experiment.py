@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--prompts", type=int, default=1024)
     ap.add_argument("--alpha-pct", type=int, default=20, help="< 0: sgs_tp_tail_plan chooses the split")
     ap.add_argument("--phases", default="A_tp2_tail,B_dp4_round_robin")
+    ap.add_argument("--dp-pool", type=int, default=150000, help="KV pages of one DP instance (planner)")
+    ap.add_argument("--tp-pool", type=int, default=300000, help="KV pages of one TP shard (planner)")
     ap.add_argument("--dp-profile-file", default="profiles/r02/tb_layout_tiles.json",
                     help="T(b) points of one GPU (ctx 2048 used) for the planner's DP side")
     ap.add_argument("--tp-profile-file", default="profiles/r02/tp/tp2_sweep_ll_ctx2048.json",
@@ -104,7 +106,7 @@ def main():
                                                       float))["profile"])
             dp_prof = fit(a.dp_profile_file, lambda p: p.get("ctx", 2048) == 2048)
             tp_prof = fit(a.tp_profile_file, lambda p: p.get("exchange") == "p2p" and p.get("ctx", 2048) == 2048)
-            plan = sgs.tp_tail_plan(tr.ids, tr.prompt_len, tr.hint, 2, 256, 16, 150000, dp_prof, 2, 256, 300000,
+            plan = sgs.tp_tail_plan(tr.ids, tr.prompt_len, tr.hint, 2, 256, 16, a.dp_pool, dp_prof, 2, 256, a.tp_pool,
                                     tp_prof, dispatch="round_robin")
             n_tail = plan["n_tail"]
             out["plan"] = {**plan, "dp_profile": dp_prof, "tp_profile": tp_prof}
