@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--prompts", type=int, default=1024)
     ap.add_argument("--alpha-pct", type=int, default=20, help="< 0: sgs_tp_tail_plan chooses the split")
     ap.add_argument("--phases", default="A_tp2_tail,B_dp4_round_robin")
+    ap.add_argument("--dp-ctx", type=int, default=2048, help="context of the DP side's T(b) points (planner)")
+    ap.add_argument("--tp-ctx", type=int, default=2048, help="context of the TP side's T(b) points (planner)")
     ap.add_argument("--dp-pool", type=int, default=150000, help="KV pages of one DP instance (planner)")
     ap.add_argument("--tp-pool", type=int, default=300000, help="KV pages of one TP shard (planner)")
     ap.add_argument("--dp-profile-file", default="profiles/r02/tb_layout_tiles.json",
@@ -104,12 +106,13 @@ def main():
                 return tuple(sgs.fit_profile(np.array([p["b"] for p in pts], float),
                                              np.array([p.get("T_us", p.get("T_us_tp2")) * 1e3 for p in pts],
                                                       float))["profile"])
-            dp_prof = fit(a.dp_profile_file, lambda p: p.get("ctx", 2048) == 2048)
-            tp_prof = fit(a.tp_profile_file, lambda p: p.get("exchange") == "p2p" and p.get("ctx", 2048) == 2048)
+            dp_prof = fit(a.dp_profile_file, lambda p: p.get("ctx", 2048) == a.dp_ctx)
+            tp_prof = fit(a.tp_profile_file, lambda p: p.get("exchange") == "p2p" and p.get("ctx", 2048) == a.tp_ctx)
             plan = sgs.tp_tail_plan(tr.ids, tr.prompt_len, tr.hint, 2, 256, 16, a.dp_pool, dp_prof, 2, 256, a.tp_pool,
                                     tp_prof, dispatch="round_robin")
             n_tail = plan["n_tail"]
-            out["plan"] = {**plan, "dp_profile": dp_prof, "tp_profile": tp_prof}
+            out["plan"] = {**plan, "dp_profile": dp_prof, "tp_profile": tp_prof, "dp_ctx": a.dp_ctx, "tp_ctx": a.tp_ctx,
+                           "dp_pool": a.dp_pool, "tp_pool": a.tp_pool}
             if rank == 0:
                 print(json.dumps({"plan": out["plan"]}), flush=True)
         tail, reg = tr.subset(order[:n_tail]), tr.subset(order[n_tail:])
