@@ -68,4 +68,5 @@ def dynamic(t_done, tokens, c: float, s_sat: float) -> dict:
         first = start if first is None else first
         free = start + _train(cum[j] - cum[i], c, s_sat)
         i, nmb = j, nmb + 1
-    return dict(policy="dynamic", end=float(free), minibatches=nmb, trainer_idle=float(idle), first_start=float(first))
+    return dict(policy="dynamic", end=float(free), minibatches=nmb, trainer_idle=float(idle),
+                first_start=None if first is None else float(first))
