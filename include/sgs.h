@@ -334,14 +334,18 @@ sgs_status sgs_elastic_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* 
  * tensor-parallel instance (max batch tp_max_batch, KV pool tp_pool_pages,
  * T(b) tp_profile), the other n - k to the e->n_instances DP instances
  * (e->dispatch policy, e->max_batch, e->profile, pool_pages each).  Both sides
- * are predicted like sgs_elastic_plan (longest-first schedule on the hints).
+ * are predicted like sgs_elastic_plan (longest-first schedule on the hints),
+ * each iteration priced at T(b) + kv_ps (tp_kv_ps for the TP instance) times
+ * the cached context tokens of its samples + pf_ps (tp_pf_ps) times the prompt
+ * tokens it prefills (0, 0 = T(b) alone).
  * k is the smallest k in [0, n] with T_tp(k) >= T_dp(k) (binary search), or
  * k - 1 when that has the smaller max(T_tp, T_dp) (ties: k - 1).  Out:
  * *n_tail = k; t_ps = {T_tp(k), T_dp(k), T_all} with T_all the prediction for
  * all n samples on n_instances + tp_size DP instances (use TP iff
  * max(T_tp, T_dp) < T_all).  Pure host function. */
 sgs_status sgs_tp_tail_plan(const sgs_engine_cfg* e, int64_t pool_pages, int32_t tp_size, int32_t tp_max_batch,
-                            int64_t tp_pool_pages, const sgs_tb_profile* tp_profile, int32_t n, const uint64_t* ids,
+                            int64_t tp_pool_pages, const sgs_tb_profile* tp_profile, int64_t kv_ps, int64_t tp_kv_ps,
+                            int64_t pf_ps, int64_t tp_pf_ps, int32_t n, const uint64_t* ids,
                             const int32_t* prompt_len, const int32_t* hint, int32_t* n_tail, int64_t t_ps[3]);
 /* Change this handle's data-parallel layout (N instances, its rank) between
  * RL batches -- the elastic scale-out of NEXT-4; SGS_E_STATE while samples

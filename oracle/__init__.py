@@ -84,7 +84,7 @@ def _declare(L):
     L.oracle_tp_tail_plan.argtypes = [ctypes.c_int32, P_i64, P_i32, P_i32, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, ctypes.c_int64, P_i64, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
-                                      P_i64, P_i64]
+                                      P_i64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, P_i64]
     L.oracle_tp_tail_plan.restype = ctypes.c_int32
     L.oracle_nearest_rank.argtypes = [ctypes.c_int32, P_i64, ctypes.c_int32]
     L.oracle_nearest_rank.restype = ctypes.c_int64
@@ -262,7 +262,8 @@ def elastic_plan(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profi
 
 
 def tp_tail_plan(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profile, tp_size: int, tp_B: int,
-                 tp_pool_pages: int, tp_profile, policy="round_robin", alpha_pct=20, score_max=0, tail_ceil=0):
+                 tp_pool_pages: int, tp_profile, policy="round_robin", alpha_pct=20, score_max=0, tail_ceil=0,
+                 kv_ps=0, tp_kv_ps=0, pf_ps=0, tp_pf_ps=0):
     """NEXT-2 two-dimensional dispatch (reading R27): k longest to one TP instance, predicted times."""
     n = len(ids)
     ids = np.ascontiguousarray(ids, np.int64)
@@ -272,7 +273,8 @@ def tp_tail_plan(ids, P, hint, N: int, B: int, page: int, pool_pages: int, profi
     k = lib().oracle_tp_tail_plan(n, _p(ids, P_i64), _p(P, P_i32), _p(hint, P_i32), N, B, page, pool_pages,
                                   _p(_prof(profile), P_i64), alpha_pct, score_max, tail_ceil,
                                   {"skew": 0, "round_robin": 1}[policy], tp_size, tp_B, tp_pool_pages,
-                                  _p(_prof(tp_profile), P_i64), _p(out, P_i64))
+                                  _p(_prof(tp_profile), P_i64), int(kv_ps), int(tp_kv_ps), int(pf_ps), int(tp_pf_ps),
+                                  _p(out, P_i64))
     return dict(n_tail=int(k), t_tp_ps=_i128(out[0], out[1]), t_dp_ps=_i128(out[2], out[3]),
                 t_all_ps=_i128(out[4], out[5]))
 

@@ -100,16 +100,18 @@ int32_t oracle_elastic_plan(int32_t n, const int64_t* ids, const int32_t* P, con
 int32_t oracle_tp_tail_plan(int32_t n, const int64_t* ids, const int32_t* P, const int32_t* hint, int32_t N, int32_t B,
                             int32_t page, int64_t pool_pages, const int64_t* profile4, int32_t alpha_pct,
                             int32_t score_max, int32_t tail_ceil, int32_t policy, int32_t tp_size, int32_t tp_B,
-                            int64_t tp_pool_pages, const int64_t* tp_profile4, int64_t* out128) {
+                            int64_t tp_pool_pages, const int64_t* tp_profile4, int64_t kv_ps, int64_t tp_kv_ps,
+                            int64_t pf_ps, int64_t tp_pf_ps, int64_t* out128) {
   DispatchIn in;
   in.id.assign(ids, ids + n);
   in.P.assign(P, P + n);
   in.hint.assign(hint, hint + n);
   in.N = N, in.B = B, in.page = page, in.pool_pages = pool_pages;
-  in.prof = Profile{profile4[0], profile4[1], profile4[2], profile4[3]};
+  in.prof = Profile{profile4[0], profile4[1], profile4[2], profile4[3], kv_ps, pf_ps};
   in.alpha_pct = alpha_pct, in.score_max = score_max, in.tail_ceil = tail_ceil;
   const TailPlanOut o = tp_tail_plan(in, policy, tp_size, tp_B, tp_pool_pages,
-                                     Profile{tp_profile4[0], tp_profile4[1], tp_profile4[2], tp_profile4[3]});
+                                     Profile{tp_profile4[0], tp_profile4[1], tp_profile4[2], tp_profile4[3], tp_kv_ps,
+                                             tp_pf_ps});
   split128(o.t_tp, out128);
   split128(o.t_dp, out128 + 2);
   split128(o.t_all, out128 + 4);

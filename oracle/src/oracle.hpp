@@ -21,6 +21,8 @@ namespace oracle {
 // ---------------------------------------------------------------------------
 struct Profile {
   int64_t t0_ns, k0_ps, b_star, k1_ps;
+  int64_t kv_ps = 0;  // R27 predictions: ps per cached context token per iteration (0: T(b) alone)
+  int64_t pf_ps = 0;  // R27 predictions: ps per prompt token prefilled in the iteration
 };
 __int128 T_ps(const Profile& p, int64_t b);
 

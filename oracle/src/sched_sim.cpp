@@ -91,6 +91,7 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
     if (active == 0 && qhead < (size_t)n && s[order[qhead]].arrival_after > horizon)
       horizon = s[order[qhead]].arrival_after;
     std::vector<int64_t> adm, comp, alloc_log, free_log;
+    int64_t pf_tokens = 0;  // prompt tokens prefilled this iteration (R27 predictions)
     std::vector<bool> is_new(n, false);
     // (ii) admission, strict longest-first, lowest free slot
     while (active < B && qhead < (size_t)n) {
@@ -109,6 +110,7 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
       ++active;
       ++qhead;
       adm.push_back(s[h].id);
+      if (first || s[h].group < 0) pf_tokens += s[h].P;
       if (s[h].group >= 0) {
         auto& gp = gpages[s[h].group];
         if (first) {  // the group's prompt pages
@@ -170,7 +172,9 @@ SimResult sched_sim(const std::vector<SimSample>& s, int B, int page, int64_t po
       --active;
       ++done;
     }
-    if (prof) r.time_ps += T_ps(*prof, active + (int64_t)fin.size());
+    if (prof)
+      r.time_ps += T_ps(*prof, active + (int64_t)fin.size()) + (__int128)prof->kv_ps * sumctx +
+                   (__int128)prof->pf_ps * pf_tokens;
     auto& o = r.iters;
     o.push_back(t);
     o.push_back(active + (int64_t)fin.size());

@@ -308,10 +308,12 @@ sgs_status sgs_elastic_plan(const sgs_engine_cfg* e, int32_t n, const uint64_t* 
 }
 
 sgs_status sgs_tp_tail_plan(const sgs_engine_cfg* e, int64_t pool_pages, int32_t tp_size, int32_t tp_max_batch,
-                            int64_t tp_pool_pages, const sgs_tb_profile* tp_profile, int32_t n, const uint64_t* ids,
+                            int64_t tp_pool_pages, const sgs_tb_profile* tp_profile, int64_t kv_ps, int64_t tp_kv_ps,
+                            int64_t pf_ps, int64_t tp_pf_ps, int32_t n, const uint64_t* ids,
                             const int32_t* prompt_len, const int32_t* hint, int32_t* n_tail, int64_t t_ps[3]) {
   if (!e || !tp_profile || n < 0 || (n > 0 && (!ids || !prompt_len || !hint)) || e->n_instances < 1 ||
-      pool_pages < 1 || e->max_batch < 1 || e->page_size < 1 || tp_size < 1 || tp_max_batch < 1 || tp_pool_pages < 1)
+      pool_pages < 1 || e->max_batch < 1 || e->page_size < 1 || tp_size < 1 || tp_max_batch < 1 || tp_pool_pages < 1 ||
+      kv_ps < 0 || tp_kv_ps < 0 || pf_ps < 0 || tp_pf_ps < 0)
     return SGS_E_INVAL;
   sgs::DispatchCfg dp{e->n_instances, e->max_batch, e->page_size, pool_pages, e->profile.t0_ns, e->profile.k0_ps,
                       e->profile.b_star, e->profile.k1_ps, e->alpha_pct, e->score, e->tail_ceil, e->dispatch,
@@ -319,6 +321,8 @@ sgs_status sgs_tp_tail_plan(const sgs_engine_cfg* e, int64_t pool_pages, int32_t
   sgs::DispatchCfg tp{1, tp_max_batch, e->page_size, tp_pool_pages, tp_profile->t0_ns, tp_profile->k0_ps,
                       tp_profile->b_star, tp_profile->k1_ps, e->alpha_pct, e->score, e->tail_ceil, e->dispatch,
                       e->sample_seed};
+  dp.kv_ps = kv_ps, dp.pf_ps = pf_ps;
+  tp.kv_ps = tp_kv_ps, tp.pf_ps = tp_pf_ps;
   const sgs::TailPlan p = sgs::tp_tail_plan(dp, tp, tp_size, n, ids, prompt_len, hint);
   if (n_tail) *n_tail = p.n_tail;
   if (t_ps) t_ps[0] = (int64_t)p.t_tp, t_ps[1] = (int64_t)p.t_dp, t_ps[2] = (int64_t)p.t_all;

@@ -357,7 +357,14 @@ __int128 predicted_generation_ps(const DispatchCfg& c, int n, const uint64_t* id
     sch.submit(std::move(mine));
     IterPlan plan;
     __int128 t = 0;
-    while (sch.plan(&plan)) t += tb_ps(c, plan.b);  // b = samples that ran in the iteration
+    while (sch.plan(&plan)) {  // b = samples that ran in the iteration, sumctx = their cached tokens
+      int64_t pf = 0;          // prompt tokens prefilled in it
+      for (int32_t i : plan.admitted) {
+        const Sample& a = sch.samples()[i];
+        if (a.group < 0 || a.group_first) pf += a.P;  // later group members share the prefill (R26)
+      }
+      t += tb_ps(c, plan.b) + (__int128)c.kv_ps * plan.sumctx + (__int128)c.pf_ps * pf;
+    }
     makespan = std::max(makespan, t);
   }
   return makespan;

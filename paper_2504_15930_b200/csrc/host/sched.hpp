@@ -108,6 +108,10 @@ struct DispatchCfg {
   int64_t t0_ns, k0_ps, b_star, k1_ps;
   int alpha_pct, score_max, tail_ceil, policy;  // policy: 0 skew, 1 round robin, 2 random
   uint64_t seed;
+  // predictions only (R27): ps per cached context token per iteration added to
+  // T(b) (the KV stream of the decode attention); 0 = the paper's T(b) alone
+  int64_t kv_ps = 0;
+  int64_t pf_ps = 0;  // predictions only: ps per prompt token prefilled in the iteration
 };
 // instance[i] for each sample i; returns N_l.
 int dispatch_alg2(const DispatchCfg& c, int n, const uint64_t* ids, const int32_t* P, const int32_t* hint,

@@ -108,8 +108,8 @@ def _declare(L):
     L.sgs_host_state.argtypes = [vp, P(i64), P(i64), P(i64)]
     L.sgs_elastic_plan.argtypes = [P(EngineCfg), i32, P(u64), P(i32), P(i32), i64, i64, P(i64), P(i64), P(i32)]
     L.sgs_set_instances.argtypes = [vp, i32, i32]
-    L.sgs_tp_tail_plan.argtypes = [P(EngineCfg), i64, i32, i32, i64, P(TbProfile), i32, P(u64), P(i32), P(i32), P(i32),
-                                   P(i64)]
+    L.sgs_tp_tail_plan.argtypes = [P(EngineCfg), i64, i32, i32, i64, P(TbProfile), i64, i64, i64, i64, i32, P(u64),
+                                   P(i32), P(i32), P(i32), P(i64)]
     L.sgs_tp_comm_init.argtypes = [vp, P(ctypes.c_uint8)]
     L.sgs_prefill_workspace_bytes.argtypes = [i32, i32, i32, i32]
     L.sgs_prefill_workspace_bytes.restype = i64
@@ -540,7 +540,8 @@ def elastic_plan(ids, prompt_len, hint, n_instances, max_batch, page, pool_pages
 
 
 def tp_tail_plan(ids, prompt_len, hint, n_dp, max_batch, page, pool_pages, profile, tp_size, tp_max_batch,
-                 tp_pool_pages, tp_profile, dispatch="round_robin", alpha_pct=20, score=0, tail_ceil=0):
+                 tp_pool_pages, tp_profile, dispatch="round_robin", alpha_pct=20, score=0, tail_ceil=0, kv_ps=0,
+                 tp_kv_ps=0, pf_ps=0, tp_pf_ps=0):
     """NEXT-2 two-dimensional dispatch (R27): how many of the longest samples go to one
     tensor-parallel instance; predicted ps of the TP instance, of the DP instances, and of DP only."""
     e = EngineCfg()
@@ -555,7 +556,7 @@ def tp_tail_plan(ids, prompt_len, hint, n_dp, max_batch, page, pool_pages, profi
     t = np.zeros(3, np.int64)
     k = ctypes.c_int32()
     _check(lib().sgs_tp_tail_plan(ctypes.byref(e), pool_pages, tp_size, tp_max_batch, tp_pool_pages, ctypes.byref(tpp),
-                                  n, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _i32p(P), _i32p(h),
+                                  int(kv_ps), int(tp_kv_ps), int(pf_ps), int(tp_pf_ps), n, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _i32p(P), _i32p(h),
                                   ctypes.byref(k), t.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
     return dict(n_tail=k.value, t_tp_ps=int(t[0]), t_dp_ps=int(t[1]), t_all_ps=int(t[2]),
                 use_tp=bool(max(t[0], t[1]) < t[2]))

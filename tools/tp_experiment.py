@@ -34,6 +34,12 @@ def main():
     ap.add_argument("--prompts", type=int, default=1024)
     ap.add_argument("--alpha-pct", type=int, default=20, help="< 0: sgs_tp_tail_plan chooses the split")
     ap.add_argument("--phases", default="A_tp2_tail,B_dp4_round_robin")
+    ap.add_argument("--dp-prof", default=None, help="t0_ns,k0_ps,b_star,k1_ps of one GPU (planner; else fitted)")
+    ap.add_argument("--tp-prof", default=None, help="the same for the TP pair")
+    ap.add_argument("--dp-kv", type=int, default=0, help="ps per cached context token per iteration, one GPU")
+    ap.add_argument("--tp-kv", type=int, default=0, help="the same for the TP pair")
+    ap.add_argument("--dp-pf", type=int, default=0, help="ps per prefilled prompt token, one GPU")
+    ap.add_argument("--tp-pf", type=int, default=0, help="the same for the TP pair")
     ap.add_argument("--dp-ctx", type=int, default=2048, help="context of the DP side's T(b) points (planner)")
     ap.add_argument("--tp-ctx", type=int, default=2048, help="context of the TP side's T(b) points (planner)")
     ap.add_argument("--dp-pool", type=int, default=150000, help="KV pages of one DP instance (planner)")
@@ -106,13 +112,20 @@ def main():
                 return tuple(sgs.fit_profile(np.array([p["b"] for p in pts], float),
                                              np.array([p.get("T_us", p.get("T_us_tp2")) * 1e3 for p in pts],
                                                       float))["profile"])
-            dp_prof = fit(a.dp_profile_file, lambda p: p.get("ctx", 2048) == a.dp_ctx)
-            tp_prof = fit(a.tp_profile_file, lambda p: p.get("exchange") == "p2p" and p.get("ctx", 2048) == a.tp_ctx)
+            if a.dp_prof:  # fixed profiles (e.g. tools/fit_kv_profile.py over several contexts)
+                dp_prof = tuple(int(x) for x in a.dp_prof.split(","))
+                tp_prof = tuple(int(x) for x in a.tp_prof.split(","))
+            else:
+                dp_prof = fit(a.dp_profile_file, lambda p: p.get("ctx", 2048) == a.dp_ctx)
+                tp_prof = fit(a.tp_profile_file,
+                              lambda p: p.get("exchange") == "p2p" and p.get("ctx", 2048) == a.tp_ctx)
             plan = sgs.tp_tail_plan(tr.ids, tr.prompt_len, tr.hint, 2, 256, 16, a.dp_pool, dp_prof, 2, 256, a.tp_pool,
-                                    tp_prof, dispatch="round_robin")
+                                    tp_prof, dispatch="round_robin", kv_ps=a.dp_kv, tp_kv_ps=a.tp_kv, pf_ps=a.dp_pf,
+                                    tp_pf_ps=a.tp_pf)
             n_tail = plan["n_tail"]
             out["plan"] = {**plan, "dp_profile": dp_prof, "tp_profile": tp_prof, "dp_ctx": a.dp_ctx, "tp_ctx": a.tp_ctx,
-                           "dp_pool": a.dp_pool, "tp_pool": a.tp_pool}
+                           "dp_pool": a.dp_pool, "tp_pool": a.tp_pool, "dp_kv": a.dp_kv, "tp_kv": a.tp_kv,
+                           "dp_pf": a.dp_pf, "tp_pf": a.tp_pf}
             if rank == 0:
                 print(json.dumps({"plan": out["plan"]}), flush=True)
         tail, reg = tr.subset(order[:n_tail]), tr.subset(order[n_tail:])
